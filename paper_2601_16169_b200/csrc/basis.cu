@@ -1,0 +1,498 @@
+// Device basis construction: helper lists, pair tables, J tables, the mixed
+// SELL table, the diagonal and the alpha-block partition (build_basis,
+// basis.cpp:78-148; generate_singles/doubles, connectivity.cpp:64-122).
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "formulas.cuh"
+#include "handle.hpp"
+
+namespace detci_gpu {
+
+// alpha-block boundaries: reference formula na*g/P (matvec.cpp:108-111) or
+// balanced by each row's element count.
+void plan_partition(uint64_t na, uint64_t nb, const uint32_t* sa, const uint32_t* da,
+                    const uint32_t* sb, const uint32_t* db, int P, int weighted, uint64_t* blk) {
+    if (P < 1) fail(DETCI_GPU_E_INPUT, "partition: P must be positive");
+    if (static_cast<uint64_t>(P) > na)
+        fail(DETCI_GPU_E_INPUT, "partition: " + std::to_string(P) + " alpha blocks exceed n_alpha " +
+                                    std::to_string(na));
+    if (!weighted || P == 1) {
+        for (int g = 0; g <= P; ++g) blk[g] = na * static_cast<uint64_t>(g) / P;
+        return;
+    }
+    uint64_t sum_sb = 0, sum_db = 0;
+    for (uint64_t i = 0; i < nb; ++i) {
+        sum_sb += sb[i];
+        sum_db += db[i];
+    }
+    std::vector<double> prefix(na + 1, 0.0);
+    for (uint64_t i = 0; i < na; ++i)
+        prefix[i + 1] = prefix[i] + static_cast<double>(sa[i] + da[i]) * nb +
+                        static_cast<double>(sum_sb + sum_db) + static_cast<double>(sa[i]) * sum_sb;
+    blk[0] = 0;
+    blk[P] = na;
+    for (int g = 1; g < P; ++g) {
+        const double target = prefix[na] * g / P;
+        uint64_t cut = std::lower_bound(prefix.begin(), prefix.end(), target) - prefix.begin();
+        cut = std::max<uint64_t>(cut, blk[g - 1] + 1);
+        cut = std::min<uint64_t>(cut, na - (P - g));
+        blk[g] = cut;
+    }
+}
+
+namespace {
+
+constexpr int kPairTile = 2048;   // strings staged in smem per pass (16 KB)
+constexpr int kPairBlock = 512;   // 16 warps = 16 source rows per CTA
+
+// Helper lists by pairwise comparison.  For source row i every string j is
+// tested with popc(s_i ^ s_j): 2 = one electron moved (singles), 4 = two
+// (doubles) -- equivalent to the reference's move probing because every
+// string of a channel has the same electron count (basis.cpp:39-44).  Rows
+// come out ascending by construction: a warp tests 32 consecutive j, and a
+// ballot + prefix popcount compacts the hits in order.  Pass 1 counts,
+// pass 2 fills at the scanned offsets.
+template <bool kFill>
+__global__ void __launch_bounds__(kPairBlock)
+k_pair_scan(const uint64_t* __restrict__ s, uint32_t n, uint32_t* __restrict__ len_s,
+            uint32_t* __restrict__ len_d, const uint64_t* __restrict__ off_s,
+            const uint64_t* __restrict__ off_d, uint32_t* __restrict__ flat_s,
+            uint32_t* __restrict__ flat_d, unsigned int* __restrict__ dup_index) {
+    __shared__ uint64_t tile[kPairTile];
+    const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+    const uint32_t i = blockIdx.x * (kPairBlock / kWarp) + warp;
+    const uint64_t si = i < n ? s[i] : 0ull;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    uint32_t cs = 0, cd = 0;
+    uint64_t base_s = 0, base_d = 0;
+    if (kFill && i < n) {
+        base_s = off_s[i];
+        base_d = off_d[i];
+    }
+    for (uint32_t t0 = 0; t0 < n; t0 += kPairTile) {
+        const uint32_t tn = min(static_cast<uint32_t>(kPairTile), n - t0);
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < tn; k += kPairBlock) tile[k] = s[t0 + k];
+        __syncthreads();
+        if (i >= n) continue;
+        for (uint32_t k = 0; k < tn; k += kWarp) {
+            const uint32_t kk = k + lane;
+            const int d = kk < tn ? __popcll(si ^ tile[kk]) : -1;
+            const unsigned bs = __ballot_sync(0xffffffffu, d == 2);
+            const unsigned bd = __ballot_sync(0xffffffffu, d == 4);
+            if (kFill) {
+                if (d == 2) flat_s[base_s + cs + __popc(bs & lt_mask)] = t0 + kk;
+                if (d == 4) flat_d[base_d + cd + __popc(bd & lt_mask)] = t0 + kk;
+            } else {
+                const unsigned b0 = __ballot_sync(0xffffffffu, d == 0 && t0 + kk != i);
+                if (b0 && lane == 0) {
+                    const uint32_t j = t0 + k + static_cast<uint32_t>(__ffs(b0) - 1);
+                    atomicMin(dup_index, max(i, j));
+                }
+            }
+            cs += __popc(bs);
+            cd += __popc(bd);
+        }
+    }
+    if (!kFill && i < n && lane == 0) {
+        len_s[i] = cs;
+        len_d[i] = cd;
+    }
+}
+
+// Exclusive scan of u32 counts into u64 offsets (FlatExcitationTable::offset
+// has size n, connectivity.cpp:41-54); one CTA, total in out[n].
+__global__ void __launch_bounds__(1024)
+k_scan_offsets(const uint32_t* __restrict__ len, uint64_t* __restrict__ off, uint32_t n) {
+    __shared__ uint64_t sums[1024];
+    const uint32_t t = threadIdx.x;
+    const uint32_t chunk = (n + 1023) / 1024;
+    const uint32_t b = min(n, t * chunk), e = min(n, b + chunk);
+    uint64_t local = 0;
+    for (uint32_t i = b; i < e; ++i) local += len[i];
+    sums[t] = local;
+    __syncthreads();
+    for (int stride = 1; stride < 1024; stride <<= 1) {
+        const uint64_t v = t >= static_cast<uint32_t>(stride) ? sums[t - stride] : 0;
+        __syncthreads();
+        sums[t] += v;
+        __syncthreads();
+    }
+    uint64_t run = sums[t] - local;
+    for (uint32_t i = b; i < e; ++i) {
+        off[i] = run;
+        run += len[i];
+    }
+    if (t == 1023) off[n] = sums[1023];
+}
+
+// Same-spin pair tables, one warp per source row, lanes over entries.
+__global__ void k_pair_tables(int ch, int kind, const uint64_t* __restrict__ s, uint32_t n,
+                              const uint32_t* __restrict__ flat, const uint64_t* __restrict__ off,
+                              const uint32_t* __restrict__ len, const double* __restrict__ h1,
+                              const double* __restrict__ eri, int norbs, double* __restrict__ pv,
+                              uint64_t* __restrict__ pmask, uint32_t* __restrict__ pab) {
+    const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
+    const int lane = threadIdx.x % kWarp;
+    if (i >= n) return;
+    const uint64_t si = s[i];
+    const uint64_t o = off[i];
+    for (uint32_t k = lane; k < len[i]; k += kWarp) {
+        const PairEntry e = make_pair_entry(ch, kind, si, s[flat[o + k]], h1, eri, norbs);
+        pv[o + k] = e.v;
+        pmask[o + k] = e.mask;
+        if (kind == 0) pab[o + k] = e.ab_sign;
+    }
+}
+
+// J[t * n + i] = sum_{r in s_i} (p q | r r), t = tri(p, q), p > q.
+__global__ void k_jtable(const uint64_t* __restrict__ s, uint32_t n,
+                         const double* __restrict__ eri, int norbs, double* __restrict__ J) {
+    const uint32_t t = blockIdx.y;
+    int p = 1;
+    while ((p + 1) * p / 2 <= static_cast<int>(t)) ++p;
+    const int q = static_cast<int>(t) - p * (p - 1) / 2;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        uint64_t bits = s[i];
+        double acc = 0.0;
+        while (bits) {
+            const int r = __ffsll(static_cast<long long>(bits)) - 1;
+            bits &= bits - 1;
+            acc += eri_at(eri, norbs, p, q, r, r);
+        }
+        J[static_cast<size_t>(t) * n + i] = acc;
+    }
+}
+
+// Per (beta row, column segment) counts of beta singles -> per (slice, seg)
+// maxima (the SELL-32 padded lengths).
+__global__ void k_sell_count(const uint32_t* __restrict__ flat, const uint64_t* __restrict__ off,
+                             const uint32_t* __restrict__ len, uint32_t n, uint32_t seg_cols,
+                             uint32_t nseg, uint32_t* __restrict__ slice_len) {
+    const uint32_t ib = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x % kWarp;
+    for (uint32_t g = 0; g < nseg; ++g) {
+        uint32_t c = 0;
+        if (ib < n)
+            for (uint32_t k = 0; k < len[ib]; ++k) c += flat[off[ib] + k] / seg_cols == g;
+        for (int sh = 16; sh > 0; sh >>= 1) c = max(c, __shfl_xor_sync(0xffffffffu, c, sh));
+        if (lane == 0 && ib / kWarp < (n + kWarp - 1) / kWarp)
+            slice_len[(ib / kWarp) * nseg + g] = c;
+    }
+}
+
+__global__ void k_sell_fill(const uint64_t* __restrict__ s, const uint32_t* __restrict__ flat,
+                            const uint64_t* __restrict__ off, const uint32_t* __restrict__ len,
+                            uint32_t n, uint32_t seg_cols, uint32_t nseg, int norbs,
+                            const uint64_t* __restrict__ sell_off, uint32_t* __restrict__ sell) {
+    const uint32_t ib = blockIdx.x * blockDim.x + threadIdx.x;
+    if (ib >= n) return;
+    const uint32_t slice = ib / kWarp, lane = ib % kWarp;
+    uint32_t cnt[16];
+    for (uint32_t g = 0; g < nseg; ++g) cnt[g] = 0;
+    const uint64_t b = s[ib];
+    for (uint32_t k = 0; k < len[ib]; ++k) {
+        const uint32_t jb = flat[off[ib] + k];
+        const uint32_t g = jb / seg_cols;
+        const uint64_t pos = sell_off[slice * nseg + g] + static_cast<uint64_t>(cnt[g]) * kWarp + lane;
+        sell[pos] = make_mixed_entry(b, s[jb], jb - g * seg_cols, norbs);
+        ++cnt[g];
+    }
+}
+
+// Diagonal pieces: E[i] = sum_{p in s} h_pp + sum_{p<q in s} [(pp|qq) - (pq|qp)].
+__global__ void k_string_energy(const uint64_t* __restrict__ s, uint32_t n,
+                                const double* __restrict__ h1, const double* __restrict__ eri,
+                                int norbs, double* __restrict__ E) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t si = s[i];
+    double acc = 0.0;
+    uint64_t a = si;
+    while (a) {
+        const int p = __ffsll(static_cast<long long>(a)) - 1;
+        a &= a - 1;
+        acc += h1[p * norbs + p];
+        uint64_t b = a;
+        while (b) {
+            const int q = __ffsll(static_cast<long long>(b)) - 1;
+            b &= b - 1;
+            acc += eri_at(eri, norbs, p, p, q, q) - eri_at(eri, norbs, p, q, q, p);
+        }
+    }
+    E[i] = acc;
+}
+
+// U[p * nb + ib] = sum_{q in B_ib} (pp|qq): the opposite-spin Coulomb part.
+__global__ void k_u_table(const uint64_t* __restrict__ sb, uint32_t nb,
+                          const double* __restrict__ eri, int norbs, double* __restrict__ U) {
+    const uint32_t ib = blockIdx.x * blockDim.x + threadIdx.x;
+    const int p = blockIdx.y;
+    if (ib >= nb) return;
+    uint64_t b = sb[ib];
+    double acc = 0.0;
+    while (b) {
+        const int q = __ffsll(static_cast<long long>(b)) - 1;
+        b &= b - 1;
+        acc += eri_at(eri, norbs, p, p, q, q);
+    }
+    U[static_cast<size_t>(p) * nb + ib] = acc;
+}
+
+// diag[ia, ib] = core + E_A[ia] + E_B[ib] + sum_{p in A} U[p][ib]
+// (zero_excite_words, slater_condon.cpp:23-39, regrouped by channel).
+__global__ void k_diag(const uint64_t* __restrict__ sa, const double* __restrict__ EA,
+                       uint32_t nloc, const double* __restrict__ EB, const double* __restrict__ U,
+                       uint32_t nb, double core, double* __restrict__ diag) {
+    const uint32_t ib = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t ia = blockIdx.y;
+    if (ib >= nb || ia >= nloc) return;
+    uint64_t a = sa[ia];
+    double x = 0.0;
+    while (a) {
+        const int p = __ffsll(static_cast<long long>(a)) - 1;
+        a &= a - 1;
+        x += U[static_cast<size_t>(p) * nb + ib];
+    }
+    diag[static_cast<size_t>(ia) * nb + ib] = core + EA[ia] + EB[ib] + x;
+}
+
+template <class T>
+void upload(DevBuf<T>& d, const std::vector<T>& v, cudaStream_t st) {
+    d.alloc(v.size());
+    if (!v.empty())
+        CUDA_CHECK(cudaMemcpyAsync(d.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+}
+
+void build_helper_lists(Handle& h, int c) {
+    ChannelTables& t = h.ch[c];
+    const uint32_t n = static_cast<uint32_t>(t.n);
+    DevBuf<unsigned int> dup;
+    dup.alloc(1);
+    const unsigned int none = 0xffffffffu;
+    CUDA_CHECK(cudaMemcpyAsync(dup.p, &none, sizeof(none), cudaMemcpyHostToDevice, h.stream));
+    for (int k = 0; k < 2; ++k) {
+        t.len[k].alloc(n);
+        t.offset[k].alloc(static_cast<size_t>(n) + 1);  // [n] holds the total
+    }
+    const unsigned grid = (n + kPairBlock / kWarp - 1) / (kPairBlock / kWarp);
+    k_pair_scan<false><<<grid, kPairBlock, 0, h.stream>>>(t.strings.p, n, t.len[0].p, t.len[1].p,
+                                                          nullptr, nullptr, nullptr, nullptr, dup.p);
+    CUDA_LAUNCH_CHECK();
+    unsigned int dup_host = none;
+    CUDA_CHECK(cudaMemcpyAsync(&dup_host, dup.p, sizeof(dup_host), cudaMemcpyDeviceToHost, h.stream));
+    for (int k = 0; k < 2; ++k) {
+        k_scan_offsets<<<1, 1024, 0, h.stream>>>(t.len[k].p, t.offset[k].p, n);
+        CUDA_LAUNCH_CHECK();
+        CUDA_CHECK(cudaMemcpyAsync(&t.nflat[k], t.offset[k].p + n, sizeof(uint64_t),
+                                   cudaMemcpyDeviceToHost, h.stream));
+    }
+    CUDA_CHECK(cudaStreamSynchronize(h.stream));
+    if (dup_host != none)  // index_strings, connectivity.cpp:35-37
+        fail(DETCI_GPU_E_INPUT, "excitation tables: duplicate string at index " +
+                                    std::to_string(dup_host));
+    for (int k = 0; k < 2; ++k) t.flat[k].alloc(std::max<uint64_t>(t.nflat[k], 1));
+    k_pair_scan<true><<<grid, kPairBlock, 0, h.stream>>>(t.strings.p, n, nullptr, nullptr,
+                                                         t.offset[0].p, t.offset[1].p, t.flat[0].p,
+                                                         t.flat[1].p, nullptr);
+    CUDA_LAUNCH_CHECK();
+    for (int k = 0; k < 2; ++k) {
+        t.h_len[k].resize(n);
+        CUDA_CHECK(cudaMemcpyAsync(t.h_len[k].data(), t.len[k].p, n * sizeof(uint32_t),
+                                   cudaMemcpyDeviceToHost, h.stream));
+    }
+}
+
+void build_pair_tables(Handle& h, int c) {
+    ChannelTables& t = h.ch[c];
+    const uint32_t n = static_cast<uint32_t>(t.n);
+    for (int k = 0; k < 2; ++k) {
+        const size_t m = std::max<uint64_t>(t.nflat[k], 1);
+        t.pv[k].alloc(m);
+        t.pmask[k].alloc(m);
+        if (k == 0) t.pab.alloc(m);
+        const unsigned grid = (n * kWarp + 255) / 256;
+        k_pair_tables<<<grid, 256, 0, h.stream>>>(c, k, t.strings.p, n, t.flat[k].p,
+                                                  t.offset[k].p, t.len[k].p, h.d_h1.p, h.d_eri.p,
+                                                  h.norbs, t.pv[k].p, t.pmask[k].p, t.pab.p);
+        CUDA_LAUNCH_CHECK();
+    }
+    const uint32_t ntri = static_cast<uint32_t>(h.norbs * (h.norbs - 1) / 2);
+    t.J.alloc(std::max<size_t>(static_cast<size_t>(ntri) * n, 1));
+    if (ntri > 0) {
+        dim3 grid(std::min<uint32_t>((n + 255) / 256, 64), ntri);
+        k_jtable<<<grid, 256, 0, h.stream>>>(t.strings.p, n, h.d_eri.p, h.norbs, t.J.p);
+        CUDA_LAUNCH_CHECK();
+    }
+}
+
+void build_mixed_sell(Handle& h) {
+    ChannelTables& b = h.ch[1];
+    const uint32_t nb = static_cast<uint32_t>(b.n);
+    // Column segment of the staged C row: <= 12288 doubles (96 KB) so two
+    // mixed CTAs fit per SM.
+    const uint32_t max_seg = 12288;
+    h.nseg = (nb + max_seg - 1) / max_seg;
+    if (h.nseg > 16) fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: more than 16 column segments");
+    h.seg_cols = (nb + h.nseg - 1) / h.nseg;
+    h.nslices = (nb + kWarp - 1) / kWarp;
+    const uint32_t nsl = h.nslices * h.nseg;
+    h.sell_len.alloc(nsl);
+    k_sell_count<<<(h.nslices * kWarp + 255) / 256, 256, 0, h.stream>>>(
+        b.flat[0].p, b.offset[0].p, b.len[0].p, nb, h.seg_cols, h.nseg, h.sell_len.p);
+    CUDA_LAUNCH_CHECK();
+    std::vector<uint32_t> sl(nsl);
+    CUDA_CHECK(cudaMemcpyAsync(sl.data(), h.sell_len.p, nsl * sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, h.stream));
+    CUDA_CHECK(cudaStreamSynchronize(h.stream));
+    std::vector<uint64_t> so(nsl);
+    uint64_t total = 0;
+    for (uint32_t i = 0; i < nsl; ++i) {
+        so[i] = total;
+        total += static_cast<uint64_t>(sl[i]) * kWarp;
+    }
+    upload(h.sell_off, so, h.stream);
+    h.sell.alloc(std::max<uint64_t>(total, 1));
+    CUDA_CHECK(cudaMemsetAsync(h.sell.p, 0, h.sell.bytes(), h.stream));  // padding: jb 0, cd 0 -> W = 0
+    k_sell_fill<<<(nb + 255) / 256, 256, 0, h.stream>>>(b.strings.p, b.flat[0].p, b.offset[0].p,
+                                                       b.len[0].p, nb, h.seg_cols, h.nseg,
+                                                       h.norbs, h.sell_off.p, h.sell.p);
+    CUDA_LAUNCH_CHECK();
+}
+
+void build_partition(Handle& h) {
+    const int P = std::max(h.world, h.vblocks);
+    const uint64_t na = h.na(), nb = h.nb();
+    h.blk.assign(P + 1, 0);
+    plan_partition(na, nb, h.ch[0].h_len[0].data(), h.ch[0].h_len[1].data(), h.ch[1].h_len[0].data(),
+                   h.ch[1].h_len[1].data(), P, h.weighted, h.blk.data());
+    uint64_t sum_sb = 0, sum_db = 0, sum_sa = 0, sum_da = 0;
+    for (uint64_t i = 0; i < nb; ++i) {
+        sum_sb += h.ch[1].h_len[0][i];
+        sum_db += h.ch[1].h_len[1][i];
+    }
+    for (uint64_t i = 0; i < na; ++i) {
+        sum_sa += h.ch[0].h_len[0][i];
+        sum_da += h.ch[0].h_len[1][i];
+    }
+    h.nnz_alpha = (sum_sa + sum_da) * nb;
+    h.nnz_beta = (sum_sb + sum_db) * na;
+    h.nnz_mixed = sum_sa * sum_sb;
+    h.max_blk = 0;
+    for (int g = 0; g < P; ++g) h.max_blk = std::max(h.max_blk, h.blk[g + 1] - h.blk[g]);
+    if (h.world > 1) {
+        h.a0 = h.blk[h.rank];
+        h.a1 = h.blk[h.rank + 1];
+    } else {
+        h.a0 = 0;
+        h.a1 = na;  // virtual blocks: this process owns every row
+    }
+}
+
+void build_diag(Handle& h) {
+    const uint32_t na = static_cast<uint32_t>(h.na()), nb = static_cast<uint32_t>(h.nb());
+    DevBuf<double> EA, EB, U;
+    EA.alloc(na);
+    EB.alloc(nb);
+    U.alloc(static_cast<size_t>(h.norbs) * nb);
+    k_string_energy<<<(na + 255) / 256, 256, 0, h.stream>>>(h.ch[0].strings.p, na, h.d_h1.p,
+                                                            h.d_eri.p, h.norbs, EA.p);
+    k_string_energy<<<(nb + 255) / 256, 256, 0, h.stream>>>(h.ch[1].strings.p, nb, h.d_h1.p,
+                                                            h.d_eri.p, h.norbs, EB.p);
+    k_u_table<<<dim3((nb + 255) / 256, h.norbs), 256, 0, h.stream>>>(h.ch[1].strings.p, nb,
+                                                                      h.d_eri.p, h.norbs, U.p);
+    CUDA_LAUNCH_CHECK();
+    const uint32_t nloc = static_cast<uint32_t>(h.nloc());
+    h.diag.alloc(std::max<size_t>(h.local_len(), 1));
+    for (uint32_t r0 = 0; r0 < nloc; r0 += 65535) {
+        const uint32_t rows = std::min<uint32_t>(65535, nloc - r0);
+        k_diag<<<dim3((nb + 255) / 256, rows), 256, 0, h.stream>>>(
+            h.ch[0].strings.p + h.a0 + r0, EA.p + h.a0 + r0, rows, EB.p, U.p, nb, h.core,
+            h.diag.p + static_cast<size_t>(r0) * nb);
+        CUDA_LAUNCH_CHECK();
+    }
+    CUDA_CHECK(cudaStreamSynchronize(h.stream));
+}
+
+size_t estimate_bytes(const Handle& h) {
+    const size_t na = h.na(), nb = h.nb();
+    const size_t ntri = static_cast<size_t>(h.norbs) * (h.norbs - 1) / 2;
+    size_t b = static_cast<size_t>(h.norbs) * h.norbs * h.norbs * h.norbs * 8;
+    for (int c = 0; c < 2; ++c) {
+        const auto& t = h.ch[c];
+        const size_t e = t.nflat[0] + t.nflat[1];
+        b += e * (4 + 8 + 8) + t.nflat[0] * 4 + t.n * (8 + 2 * (12 + 4)) + ntri * t.n * 8;
+    }
+    b += (h.ch[1].nflat[0] * 4) * 2;             // SELL incl. padding slack
+    const int P = std::max(h.world, h.vblocks);
+    size_t max_blk = (na + P - 1) / P + 1;
+    if (P > 1) max_blk = std::max<size_t>(max_blk, na / P + 2);
+    const size_t loc = (h.world > 1 ? max_blk : na) * nb;
+    b += loc * 8;                                 // diag
+    b += 2 * max_blk * nb * 8;                    // ct, yt
+    if (P > 1) b += 2 * max_blk * nb * 8;         // ring buffers
+    return b;
+}
+
+} // namespace
+
+void release_basis(Handle& h) {
+    for (auto& t : h.ch) {
+        for (int k = 0; k < 2; ++k) {
+            t.flat[k].reset();
+            t.offset[k].reset();
+            t.len[k].reset();
+            t.pv[k].reset();
+            t.pmask[k].reset();
+        }
+        t.pab.reset();
+        t.J.reset();
+    }
+    h.sell.reset();
+    h.sell_off.reset();
+    h.sell_len.reset();
+    h.diag.reset();
+    h.ct.reset();
+    h.yt.reset();
+    h.ring[0].reset();
+    h.ring[1].reset();
+    h.xbuf.reset();
+    h.ybuf.reset();
+    h.built = false;
+}
+
+void build_device_basis(Handle& h) {
+    if (!h.have_strings) fail(DETCI_GPU_E_INPUT, "build_basis: strings not set");
+    if (!h.have_ints) fail(DETCI_GPU_E_INPUT, "build_basis: integrals not set");
+    release_basis(h);
+    for (int c = 0; c < 2; ++c) build_helper_lists(h, c);
+    CUDA_CHECK(cudaStreamSynchronize(h.stream));
+    build_partition(h);
+
+    size_t free_b = 0, total_b = 0;
+    CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t budget = h.budget ? h.budget : free_b;
+    const size_t need = estimate_bytes(h);
+    if (need > budget)  // basis.cpp:113-118 convention
+        fail(DETCI_GPU_E_CAPACITY, "device basis requires " + std::to_string(need) +
+                                       " bytes, budget is " + std::to_string(budget) + " bytes");
+
+    for (int c = 0; c < 2; ++c) build_pair_tables(h, c);
+    build_mixed_sell(h);
+    build_diag(h);
+    const size_t scratch = static_cast<size_t>(h.max_blk) * h.nb();
+    h.ct.alloc(std::max<size_t>(scratch, 1));
+    h.yt.alloc(std::max<size_t>(scratch, 1));
+    if (std::max(h.world, h.vblocks) > 1) {
+        h.ring[0].alloc(scratch);
+        h.ring[1].alloc(scratch);
+    }
+    CUDA_CHECK(cudaStreamSynchronize(h.stream));
+    h.built = true;
+}
+
+} // namespace detci_gpu

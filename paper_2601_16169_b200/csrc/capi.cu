@@ -1,0 +1,512 @@
+// extern "C" boundary of libdetci_gpu.so (include/detci_gpu.h).  Every entry
+// point converts internal failures to a status code (no exception crosses
+// the ABI) and records the message for detci_gpu_last_error.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "formulas.cuh"
+#include "handle.hpp"
+
+using namespace detci_gpu;
+
+struct detci_gpu_handle {
+    Handle h;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(detci_gpu_handle* hh, F&& body) {
+    try {
+        body();
+        return DETCI_GPU_OK;
+    } catch (const Failure& f) {
+        if (hh) hh->h.err = f.what();
+        g_last_error = f.what();
+        return f.code;
+    } catch (const std::bad_alloc&) {
+        const char* msg = "host allocation failed";
+        if (hh) hh->h.err = msg;
+        g_last_error = msg;
+        return DETCI_GPU_E_CAPACITY;
+    } catch (const std::exception& e) {
+        if (hh) hh->h.err = e.what();
+        g_last_error = e.what();
+        return DETCI_GPU_E_ERROR;
+    }
+}
+
+void require(bool ok, int code, const std::string& msg) {
+    if (!ok) fail(code, msg);
+}
+
+void activate(const Handle& h) { CUDA_CHECK(cudaSetDevice(h.device)); }
+
+__global__ void k_precondition(const double* __restrict__ r, const double* __restrict__ d, uint64_t n,
+                               double theta, double* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        double denom = d[i] - theta;
+        if (fabs(denom) < 1e-8) denom = copysign(1e-8, denom);
+        out[i] = r[i] / denom;
+    }
+}
+
+__global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, uint64_t n, double a) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        y[i] -= a * x[i];
+}
+
+__global__ void k_div(double* __restrict__ y, uint64_t n, double a) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        y[i] /= a;
+}
+
+double host_j(const double* eri, int n, int p, int q, uint64_t spec) {
+    double acc = 0.0;
+    while (spec) {
+        const int r = __builtin_ctzll(spec);
+        spec &= spec - 1;
+        acc += eri_at(eri, n, p, q, r, r);
+    }
+    return acc;
+}
+
+} // namespace
+
+extern "C" {
+
+int detci_gpu_abi_version(void) { return DETCI_GPU_ABI_VERSION; }
+
+const char* detci_gpu_last_error(const detci_gpu_handle* h) {
+    return h ? h->h.err.c_str() : g_last_error.c_str();
+}
+
+int detci_gpu_nccl_unique_id(uint8_t out[128]) {
+    return guarded(nullptr, [&] {
+        ncclUniqueId id;
+        if (ncclGetUniqueId(&id) != ncclSuccess) fail(DETCI_GPU_E_CUDA, "ncclGetUniqueId failed");
+        static_assert(sizeof(id) == 128, "ncclUniqueId size");
+        std::memcpy(out, &id, 128);
+    });
+}
+
+int detci_gpu_create(const detci_gpu_desc* desc, detci_gpu_handle** out) {
+    return guarded(nullptr, [&] {
+        require(desc && out, DETCI_GPU_E_INPUT, "create: null argument");
+        *out = nullptr;
+        require(desc->world_size >= 1 && desc->rank >= 0 && desc->rank < desc->world_size,
+                DETCI_GPU_E_CONFIG, "create: invalid rank/world_size");
+        require(desc->virtual_blocks >= 0, DETCI_GPU_E_CONFIG, "create: negative virtual_blocks");
+        require(!(desc->world_size > 1 && desc->virtual_blocks > 1), DETCI_GPU_E_CONFIG,
+                "create: virtual_blocks requires world_size 1");
+        int ndev = 0;
+        CUDA_CHECK(cudaGetDeviceCount(&ndev));
+        require(ndev > 0, DETCI_GPU_E_CUDA, "create: no CUDA device");
+        auto* hh = new detci_gpu_handle();
+        Handle& h = hh->h;
+        try {
+            h.device = desc->device >= 0 ? desc->device : 0;
+            if (desc->device < 0) CUDA_CHECK(cudaGetDevice(&h.device));
+            require(h.device < ndev, DETCI_GPU_E_CONFIG, "create: device ordinal out of range");
+            CUDA_CHECK(cudaSetDevice(h.device));
+            h.rank = desc->rank;
+            h.world = desc->world_size;
+            h.vblocks = std::max(1, desc->virtual_blocks);
+            h.weighted = desc->weighted_partition;
+            h.budget = desc->memory_budget_bytes;
+            CUDA_CHECK(cudaStreamCreateWithFlags(&h.stream, cudaStreamNonBlocking));
+            CUDA_CHECK(cudaStreamCreateWithFlags(&h.comm_stream, cudaStreamNonBlocking));
+            for (auto& e : h.ev) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            if (h.world > 1) {
+                require(desc->nccl_id != nullptr, DETCI_GPU_E_CONFIG, "create: nccl_id required");
+                ncclUniqueId id;
+                std::memcpy(&id, desc->nccl_id, sizeof(id));
+                if (ncclCommInitRank(&h.nccl, h.world, id, h.rank) != ncclSuccess)
+                    fail(DETCI_GPU_E_CUDA, "ncclCommInitRank failed");
+            }
+        } catch (...) {
+            detci_gpu_destroy(hh);
+            throw;
+        }
+        *out = hh;
+    });
+}
+
+void detci_gpu_destroy(detci_gpu_handle* hh) {
+    if (!hh) return;
+    Handle& h = hh->h;
+    cudaSetDevice(h.device);
+    if (h.stream) cudaStreamSynchronize(h.stream);
+    if (h.comm_stream) cudaStreamSynchronize(h.comm_stream);
+    release_basis(h);
+    for (auto& c : h.ch) c.strings.reset();
+    h.d_h1.reset();
+    h.d_eri.reset();
+    h.red.reset();
+    h.red_count.reset();
+    if (h.nccl) ncclCommDestroy(h.nccl);
+    for (auto& e : h.ev)
+        if (e) cudaEventDestroy(e);
+    if (h.stream) cudaStreamDestroy(h.stream);
+    if (h.comm_stream) cudaStreamDestroy(h.comm_stream);
+    delete hh;
+}
+
+int detci_gpu_set_strings(detci_gpu_handle* hh, int norbs, const uint64_t* alpha, size_t na,
+                          const uint64_t* beta, size_t nb) {
+    return guarded(hh, [&] {
+        require(hh != nullptr, DETCI_GPU_E_INPUT, "set_strings: null handle");
+        Handle& h = hh->h;
+        require(norbs >= 1, DETCI_GPU_E_INPUT, "set_strings: norbs must be positive");
+        // Reference limit is kMaxKernelBits = 256 spin-orbitals (basis.cpp:83-87);
+        // the device kernels hold one uint64 per channel string.
+        require(2 * norbs <= 256, DETCI_GPU_E_INPUT,
+                "build_basis: " + std::to_string(2 * norbs) + " spin-orbitals exceed the kernel limit of 256");
+        require(norbs <= 64, DETCI_GPU_E_UNSUPPORTED, "set_strings: norbs > 64 is not supported on the GPU path");
+        require(h.have_ints == false || norbs == h.norbs, DETCI_GPU_E_INPUT,
+                "set_strings: norbs does not match the integrals");
+        const char* names[2] = {"alpha", "beta"};
+        const uint64_t* src[2] = {alpha, beta};
+        const size_t cnt[2] = {na, nb};
+        const uint64_t allowed = norbs == 64 ? ~0ull : ((1ull << norbs) - 1);
+        for (int c = 0; c < 2; ++c) {
+            require(cnt[c] > 0 && src[c] != nullptr, DETCI_GPU_E_INPUT,
+                    std::string("build_basis: empty ") + names[c] + " string list");
+            require(cnt[c] < (1ull << 31), DETCI_GPU_E_UNSUPPORTED, "set_strings: more than 2^31 strings");
+            int ne = -1;
+            for (size_t i = 0; i < cnt[c]; ++i) {
+                require((src[c][i] & ~allowed) == 0, DETCI_GPU_E_INPUT,
+                        std::string("build_basis: ") + names[c] + " string " + std::to_string(i) +
+                            " has wrong orbital count");
+                const int pc = __builtin_popcountll(src[c][i]);
+                if (ne < 0) ne = pc;
+                require(pc == ne, DETCI_GPU_E_INPUT,
+                        std::string("build_basis: inconsistent electron count in ") + names[c] +
+                            " strings (string " + std::to_string(i) + ")");
+            }
+            h.ch[c].n_elec = ne;
+        }
+        activate(h);
+        release_basis(h);
+        h.norbs = norbs;
+        for (int c = 0; c < 2; ++c) {
+            ChannelTables& t = h.ch[c];
+            t.n = cnt[c];
+            t.h_strings.assign(src[c], src[c] + cnt[c]);
+            t.strings.alloc(t.n);
+            CUDA_CHECK(cudaMemcpy(t.strings.p, t.h_strings.data(), t.n * sizeof(uint64_t),
+                                  cudaMemcpyHostToDevice));
+        }
+        h.have_strings = true;
+    });
+}
+
+int detci_gpu_set_integrals(detci_gpu_handle* hh, double core, const double* h1, const double* eri) {
+    return guarded(hh, [&] {
+        require(hh != nullptr, DETCI_GPU_E_INPUT, "set_integrals: null handle");
+        Handle& h = hh->h;
+        require(h.have_strings, DETCI_GPU_E_INPUT, "set_integrals: call set_strings first");
+        require(h1 && eri, DETCI_GPU_E_INPUT, "set_integrals: null integrals");
+        activate(h);
+        release_basis(h);
+        const size_t n = static_cast<size_t>(h.norbs);
+        h.core = core;
+        h.h1.assign(h1, h1 + n * n);
+        h.eri.assign(eri, eri + n * n * n * n);
+        h.d_h1.alloc(n * n);
+        h.d_eri.alloc(n * n * n * n);
+        CUDA_CHECK(cudaMemcpy(h.d_h1.p, h.h1.data(), n * n * 8, cudaMemcpyHostToDevice));
+        CUDA_CHECK(cudaMemcpy(h.d_eri.p, h.eri.data(), n * n * n * n * 8, cudaMemcpyHostToDevice));
+        h.have_ints = true;
+    });
+}
+
+int detci_gpu_build_basis(detci_gpu_handle* hh) {
+    return guarded(hh, [&] {
+        require(hh != nullptr, DETCI_GPU_E_INPUT, "build_basis: null handle");
+        activate(hh->h);
+        build_device_basis(hh->h);
+    });
+}
+
+int detci_gpu_helper_size(const detci_gpu_handle* hh, int channel, int kind, uint64_t* nflat) {
+    return guarded(const_cast<detci_gpu_handle*>(hh), [&] {
+        require(hh && hh->h.built, DETCI_GPU_E_INPUT, "helpers: basis not built");
+        require(channel >= 0 && channel < 2 && kind >= 0 && kind < 2, DETCI_GPU_E_INPUT,
+                "helpers: bad channel/kind");
+        *nflat = hh->h.ch[channel].nflat[kind];
+    });
+}
+
+int detci_gpu_get_helpers(const detci_gpu_handle* hh, int channel, int kind, uint32_t* flat,
+                          uint64_t* offset, uint32_t* len) {
+    return guarded(const_cast<detci_gpu_handle*>(hh), [&] {
+        require(hh && hh->h.built, DETCI_GPU_E_INPUT, "helpers: basis not built");
+        require(channel >= 0 && channel < 2 && kind >= 0 && kind < 2, DETCI_GPU_E_INPUT,
+                "helpers: bad channel/kind");
+        const Handle& h = hh->h;
+        activate(h);
+        const ChannelTables& t = h.ch[channel];
+        if (flat && t.nflat[kind])
+            CUDA_CHECK(cudaMemcpy(flat, t.flat[kind].p, t.nflat[kind] * 4, cudaMemcpyDeviceToHost));
+        if (offset) CUDA_CHECK(cudaMemcpy(offset, t.offset[kind].p, t.n * 8, cudaMemcpyDeviceToHost));
+        if (len) CUDA_CHECK(cudaMemcpy(len, t.len[kind].p, t.n * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+int detci_gpu_local_rows(const detci_gpu_handle* hh, uint64_t* row_begin, uint64_t* row_end,
+                         uint64_t* n_beta) {
+    return guarded(const_cast<detci_gpu_handle*>(hh), [&] {
+        require(hh && hh->h.built, DETCI_GPU_E_INPUT, "local_rows: basis not built");
+        *row_begin = hh->h.a0;
+        *row_end = hh->h.a1;
+        *n_beta = hh->h.nb();
+    });
+}
+
+int detci_gpu_nnz(const detci_gpu_handle* hh, uint64_t* total, uint64_t* a, uint64_t* b, uint64_t* m) {
+    return guarded(const_cast<detci_gpu_handle*>(hh), [&] {
+        require(hh && hh->h.built, DETCI_GPU_E_INPUT, "nnz: basis not built");
+        const Handle& h = hh->h;
+        if (a) *a = h.nnz_alpha;
+        if (b) *b = h.nnz_beta;
+        if (m) *m = h.nnz_mixed;
+        if (total) *total = h.nnz_alpha + h.nnz_beta + h.nnz_mixed;
+    });
+}
+
+int detci_gpu_diag(const detci_gpu_handle* hh, double* out) {
+    return guarded(const_cast<detci_gpu_handle*>(hh), [&] {
+        require(hh && hh->h.built, DETCI_GPU_E_INPUT, "diag: basis not built");
+        activate(hh->h);
+        CUDA_CHECK(cudaMemcpy(out, hh->h.diag.p, hh->h.local_len() * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+int detci_gpu_plan_partition(uint64_t na, uint64_t nb, const uint32_t* sa, const uint32_t* da,
+                             const uint32_t* sb, const uint32_t* db, int P, int weighted, uint64_t* blk) {
+    return guarded(nullptr, [&] {
+        require(blk && (!weighted || (sa && da && sb && db)), DETCI_GPU_E_INPUT,
+                "plan_partition: null argument");
+        plan_partition(na, nb, sa, da, sb, db, P, weighted, blk);
+    });
+}
+
+int detci_gpu_sigma_device(detci_gpu_handle* hh, const double* dx, double* dy, detci_gpu_timings* tm) {
+    return guarded(hh, [&] {
+        require(hh != nullptr && dx && dy, DETCI_GPU_E_INPUT, "sigma: null argument");
+        require(dx != dy, DETCI_GPU_E_INPUT, "sigma: x and y must not alias");
+        activate(hh->h);
+        if (tm) *tm = detci_gpu_timings{};
+        sigma_device(hh->h, dx, dy, tm);
+    });
+}
+
+int detci_gpu_sigma(detci_gpu_handle* hh, const double* x, double* y, detci_gpu_timings* tm) {
+    return guarded(hh, [&] {
+        require(hh != nullptr && x && y, DETCI_GPU_E_INPUT, "sigma: null argument");
+        Handle& h = hh->h;
+        require(h.built, DETCI_GPU_E_INPUT, "sigma: basis not built");
+        activate(h);
+        const size_t n = h.local_len();
+        h.xbuf.alloc(n);
+        h.ybuf.alloc(n);
+        cudaEvent_t e[4];
+        for (auto& ev : e) CUDA_CHECK(cudaEventCreate(&ev));
+        CUDA_CHECK(cudaEventRecord(e[0], h.stream));
+        CUDA_CHECK(cudaMemcpyAsync(h.xbuf.p, x, n * 8, cudaMemcpyHostToDevice, h.stream));
+        CUDA_CHECK(cudaEventRecord(e[1], h.stream));
+        if (tm) *tm = detci_gpu_timings{};
+        sigma_device(h, h.xbuf.p, h.ybuf.p, tm);
+        CUDA_CHECK(cudaEventRecord(e[2], h.stream));
+        CUDA_CHECK(cudaMemcpyAsync(y, h.ybuf.p, n * 8, cudaMemcpyDeviceToHost, h.stream));
+        CUDA_CHECK(cudaEventRecord(e[3], h.stream));
+        CUDA_CHECK(cudaEventSynchronize(e[3]));
+        if (tm) {
+            float a = 0.f, b = 0.f, c = 0.f;
+            CUDA_CHECK(cudaEventElapsedTime(&a, e[0], e[1]));
+            CUDA_CHECK(cudaEventElapsedTime(&b, e[2], e[3]));
+            CUDA_CHECK(cudaEventElapsedTime(&c, e[0], e[3]));
+            tm->h2d_seconds = a * 1e-3;
+            tm->d2h_seconds = b * 1e-3;
+            tm->total_seconds = c * 1e-3;
+        }
+        for (auto& ev : e) cudaEventDestroy(ev);
+    });
+}
+
+int detci_gpu_alloc_vector(detci_gpu_handle* hh, double** dptr) {
+    return guarded(hh, [&] {
+        require(hh && hh->h.built && dptr, DETCI_GPU_E_INPUT, "alloc_vector: basis not built");
+        activate(hh->h);
+        CUDA_CHECK(cudaMalloc(dptr, std::max<size_t>(hh->h.local_len(), 1) * 8));
+    });
+}
+
+int detci_gpu_free_vector(detci_gpu_handle* hh, double* dptr) {
+    return guarded(hh, [&] {
+        require(hh != nullptr, DETCI_GPU_E_INPUT, "free_vector: null handle");
+        activate(hh->h);
+        CUDA_CHECK(cudaFree(dptr));
+    });
+}
+
+// kind: 0 host->device, 1 device->host, 2 device->device (local length)
+int detci_gpu_copy_vector(detci_gpu_handle* hh, double* dst, const double* src, int kind) {
+    return guarded(hh, [&] {
+        require(hh && hh->h.built && dst && src, DETCI_GPU_E_INPUT, "copy_vector: bad argument");
+        activate(hh->h);
+        const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice
+                                          : (kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice);
+        CUDA_CHECK(cudaMemcpyAsync(dst, src, hh->h.local_len() * 8, k, hh->h.stream));
+        CUDA_CHECK(cudaStreamSynchronize(hh->h.stream));
+    });
+}
+
+int detci_gpu_davidson(detci_gpu_handle* hh, const detci_dav_opts* opts, detci_dav_result* res,
+                       detci_trace_cb cb, void* user) {
+    return guarded(hh, [&] {
+        require(hh && opts && res, DETCI_GPU_E_INPUT, "davidson: null argument");
+        activate(hh->h);
+        davidson_device(hh->h, *opts, res, cb, user);
+    });
+}
+
+int detci_gpu_inner_product(detci_gpu_handle* hh, const double* x, const double* y, uint64_t n,
+                            double* out) {
+    return guarded(hh, [&] {
+        require(hh && x && y && out, DETCI_GPU_E_INPUT, "inner_product: null argument");
+        require(hh->h.world == 1, DETCI_GPU_E_UNSUPPORTED, "inner_product: single-GPU helper");
+        activate(hh->h);
+        DevBuf<double> dx, dy;
+        dx.alloc(std::max<uint64_t>(n, 1));
+        dy.alloc(std::max<uint64_t>(n, 1));
+        CUDA_CHECK(cudaMemcpy(dx.p, x, n * 8, cudaMemcpyHostToDevice));
+        CUDA_CHECK(cudaMemcpy(dy.p, y, n * 8, cudaMemcpyHostToDevice));
+        *out = device_dot(hh->h, dx.p, dy.p, n);
+    });
+}
+
+int detci_gpu_orthonormalize(detci_gpu_handle* hh, const double* vs, int k, uint64_t n,
+                             const double* candidate, double* out, int* accepted) {
+    return guarded(hh, [&] {
+        require(hh && candidate && out && accepted && (k == 0 || vs), DETCI_GPU_E_INPUT,
+                "orthonormalize: null argument");
+        require(hh->h.world == 1, DETCI_GPU_E_UNSUPPORTED, "orthonormalize: single-GPU helper");
+        Handle& h = hh->h;
+        activate(h);
+        DevBuf<double> dv, dc;
+        dv.alloc(std::max<uint64_t>(static_cast<uint64_t>(k) * n, 1));
+        dc.alloc(std::max<uint64_t>(n, 1));
+        if (k) CUDA_CHECK(cudaMemcpy(dv.p, vs, static_cast<size_t>(k) * n * 8, cudaMemcpyHostToDevice));
+        CUDA_CHECK(cudaMemcpy(dc.p, candidate, n * 8, cudaMemcpyHostToDevice));
+        for (int pass = 0; pass < 2; ++pass)
+            for (int j = 0; j < k; ++j) {
+                const double* bv = dv.p + static_cast<size_t>(j) * n;
+                const double o = device_dot(h, bv, dc.p, n);
+                k_axpy<<<592, 256, 0, h.stream>>>(dc.p, bv, n, o);
+                CUDA_LAUNCH_CHECK();
+            }
+        const double norm = std::sqrt(device_dot(h, dc.p, dc.p, n));
+        *accepted = norm >= 1e-10 ? 1 : 0;
+        if (*accepted) {
+            k_div<<<592, 256, 0, h.stream>>>(dc.p, n, norm);
+            CUDA_LAUNCH_CHECK();
+        }
+        CUDA_CHECK(cudaStreamSynchronize(h.stream));
+        CUDA_CHECK(cudaMemcpy(out, dc.p, n * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+int detci_gpu_precondition(detci_gpu_handle* hh, const double* residual, const double* diag,
+                           uint64_t n, double theta, double* out) {
+    return guarded(hh, [&] {
+        require(hh && residual && diag && out, DETCI_GPU_E_INPUT, "precondition: null argument");
+        Handle& h = hh->h;
+        activate(h);
+        DevBuf<double> dr, dd;
+        dr.alloc(std::max<uint64_t>(n, 1));
+        dd.alloc(std::max<uint64_t>(n, 1));
+        CUDA_CHECK(cudaMemcpy(dr.p, residual, n * 8, cudaMemcpyHostToDevice));
+        CUDA_CHECK(cudaMemcpy(dd.p, diag, n * 8, cudaMemcpyHostToDevice));
+        k_precondition<<<592, 256, 0, h.stream>>>(dr.p, dd.p, n, theta, dr.p);
+        CUDA_LAUNCH_CHECK();
+        CUDA_CHECK(cudaStreamSynchronize(h.stream));
+        CUDA_CHECK(cudaMemcpy(out, dr.p, n * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+// Diagnostic (host execution, no GPU): the element <bra|H|ket> as the sigma
+// kernels assemble it from the factorized closed forms of formulas.cuh.
+// E_INPUT when the pair is not connected by <= 2 spin-conserving moves.
+int detci_gpu_factorized_element(int norbs, double core, const double* h1, const double* eri,
+                                 uint64_t bra_a, uint64_t bra_b, uint64_t ket_a, uint64_t ket_b,
+                                 double* out) {
+    return guarded(nullptr, [&] {
+        const int da = __builtin_popcountll(bra_a ^ ket_a) / 2;
+        const int db = __builtin_popcountll(bra_b ^ ket_b) / 2;
+        require(__builtin_popcountll(bra_a) == __builtin_popcountll(ket_a) &&
+                    __builtin_popcountll(bra_b) == __builtin_popcountll(ket_b),
+                DETCI_GPU_E_INPUT, "factorized_element: spin-nonconserving pair");
+        if (da + db > 2) {
+            *out = 0.0;
+            return;
+        }
+        if (da == 0 && db == 0) {  // diagonal, regrouped as in k_diag
+            auto energy = [&](uint64_t s) {
+                double acc = 0.0;
+                for (uint64_t a = s; a; a &= a - 1) {
+                    const int p = __builtin_ctzll(a);
+                    acc += h1[p * norbs + p];
+                    for (uint64_t b = a & (a - 1); b; b &= b - 1) {
+                        const int q = __builtin_ctzll(b);
+                        acc += eri_at(eri, norbs, p, p, q, q) - eri_at(eri, norbs, p, q, q, p);
+                    }
+                }
+                return acc;
+            };
+            double x = 0.0;
+            for (uint64_t a = bra_a; a; a &= a - 1) {
+                const int p = __builtin_ctzll(a);
+                for (uint64_t b = bra_b; b; b &= b - 1)
+                    x += eri_at(eri, norbs, p, p, __builtin_ctzll(b), __builtin_ctzll(b));
+            }
+            *out = core + energy(bra_a) + energy(bra_b) + x;
+            return;
+        }
+        if (db == 0 || da == 0) {  // same-spin: alpha (ch 0) or beta (ch 1)
+            const int ch = db == 0 ? 0 : 1;
+            const uint64_t si = ch == 0 ? bra_a : bra_b, sj = ch == 0 ? ket_a : ket_b;
+            const uint64_t spec = ch == 0 ? bra_b : bra_a;
+            const int kind = (ch == 0 ? da : db) - 1;
+            const PairEntry e = make_pair_entry(ch, kind, si, sj, h1, eri, norbs);
+            double v = e.v;
+            if (kind == 0) {
+                const uint64_t x = si & ~sj, y = sj & ~si;
+                const double j = host_j(eri, norbs, __builtin_ctzll(x), __builtin_ctzll(y), spec);
+                v += (e.ab_sign >> 31) ? -j : j;
+            }
+            *out = (popc64(spec & e.mask) & 1) ? -v : v;
+            return;
+        }
+        // mixed alpha single x beta single
+        const int pa = __builtin_ctzll(bra_a & ~ket_a), qa = __builtin_ctzll(ket_a & ~bra_a);
+        const uint32_t ent = make_mixed_entry(bra_b, ket_b, 0, norbs);
+        const int cd = static_cast<int>((ent >> 18) & 0xfffu);
+        double w = mixed_weight(eri, norbs, pa, qa, ket_a, cd / norbs, cd % norbs);
+        if (ent >> 31) w = -w;
+        if (mixed_outer_parity(bra_a, bra_b, pa, qa)) w = -w;
+        *out = w;
+    });
+}
+
+} // extern "C"

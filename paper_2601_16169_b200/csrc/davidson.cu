@@ -1,0 +1,528 @@
+// Device-resident Davidson (davidson_solve, davidson.cpp:73-206).
+//
+// Every per-iteration vector operation is a fused, bandwidth-bound kernel
+// over HBM-resident vectors; only scalars (<= 2k dot products, two norms)
+// cross to the host, where the k x k Rayleigh-Ritz problem is solved
+// (Jacobi on the lower triangle, as Eigen's SelfAdjointEigenSolver reads
+// it).  Reductions are two-stage with a fixed order, so a run is bitwise
+// reproducible; with several GPUs the per-rank partials are summed with
+// ncclAllReduce before use.  Algorithmic rules kept from the reference:
+// argmin-diagonal guess with lowest-index ties, lower-triangle projected
+// fill, 2-pass modified Gram-Schmidt with the 1e-10 dependence threshold,
+// the 1e-8 preconditioner clamp, collapse to the Ritz pair at
+// max_subspace, and the per-iteration trace (Gram deviation included).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <vector>
+
+#include "handle.hpp"
+
+namespace detci_gpu {
+
+namespace {
+
+constexpr int kRedBlocks = 592;   // 4 x 148 SMs
+constexpr int kRedThreads = 256;
+constexpr int kDotTile = 2048;
+constexpr int kMaxVec = 64;
+
+struct VecList {
+    const double* p[2 * kMaxVec];
+};
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+    for (int s = 16; s > 0; s >>= 1) v += __shfl_down_sync(0xffffffffu, v, s);
+    const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x < 32) {
+        t = threadIdx.x < blockDim.x / 32 ? sh[threadIdx.x] : 0.0;
+        for (int s = 16; s > 0; s >>= 1) t += __shfl_down_sync(0xffffffffu, t, s);
+    }
+    return t;  // valid in thread 0
+}
+
+// partial[j * gridDim.x + blk] = sum over this block's chunk of x * y_j
+__global__ void __launch_bounds__(kRedThreads)
+k_dot_many(const double* __restrict__ x, VecList ys, int k, uint64_t n, double* __restrict__ partial) {
+    __shared__ double xt[kDotTile];
+    __shared__ double sh[32];
+    const uint64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    const uint64_t b = min(n, chunk * blockIdx.x), e = min(n, b + chunk);
+    double acc[8];
+    for (int j0 = 0; j0 < k; j0 += 8) {
+        for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+        for (uint64_t t0 = b; t0 < e; t0 += kDotTile) {
+            const int tn = static_cast<int>(min(static_cast<uint64_t>(kDotTile), e - t0));
+            __syncthreads();
+            for (int i = threadIdx.x; i < tn; i += kRedThreads) xt[i] = x[t0 + i];
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (j0 + j >= k) break;
+                const double* y = ys.p[j0 + j] + t0;
+                for (int i = threadIdx.x; i < tn; i += kRedThreads) acc[j] = fma(xt[i], y[i], acc[j]);
+            }
+        }
+        for (int j = 0; j < 8 && j0 + j < k; ++j) {
+            const double s = block_sum(acc[j], sh);
+            if (threadIdx.x == 0) partial[static_cast<size_t>(j0 + j) * gridDim.x + blockIdx.x] = s;
+        }
+    }
+}
+
+// out[j] = sum_b partial[j * nblk + b], fixed order (one warp per j)
+__global__ void k_finalize(const double* __restrict__ partial, int nblk, int k, double* __restrict__ out) {
+    const int j = blockIdx.x;
+    if (j >= k) return;
+    double v = 0.0;
+    for (int b = threadIdx.x; b < nblk; b += 32) v += partial[static_cast<size_t>(j) * nblk + b];
+    for (int s = 16; s > 0; s >>= 1) v += __shfl_down_sync(0xffffffffu, v, s);
+    if (threadIdx.x == 0) out[j] = v;
+}
+
+struct RitzArgs {
+    const double* v[kMaxVec];
+    const double* w[kMaxVec];
+    double c[kMaxVec];
+    int k;
+    double theta;
+};
+
+// ritz = sum c_j v_j, img = sum c_j w_j, res = img - theta ritz,
+// corr = res / clamp(diag - theta); partials of |res|^2 and |corr|^2.
+// (davidson.cpp:134-146 and precondition, :59-71)
+__global__ void __launch_bounds__(kRedThreads)
+k_ritz(const RitzArgs a, const double* __restrict__ diag, uint64_t n, double* __restrict__ ritz,
+       double* __restrict__ img, double* __restrict__ corr, double* __restrict__ partial) {
+    __shared__ double sh[32];
+    double rr = 0.0, cc = 0.0;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        double r = 0.0, m = 0.0;
+        for (int j = 0; j < a.k; ++j) {
+            r += a.c[j] * a.v[j][i];
+            m += a.c[j] * a.w[j][i];
+        }
+        ritz[i] = r;
+        img[i] = m;
+        const double res = m - a.theta * r;
+        double denom = diag[i] - a.theta;
+        if (fabs(denom) < 1e-8) denom = copysign(1e-8, denom);
+        const double cr = res / denom;
+        corr[i] = cr;
+        rr += res * res;
+        cc += cr * cr;
+    }
+    const double s1 = block_sum(rr, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s1;
+    const double s2 = block_sum(cc, sh);
+    if (threadIdx.x == 0) partial[gridDim.x + blockIdx.x] = s2;
+}
+
+// One modified Gram-Schmidt step: cand -= (*o_prev) vprev (if vprev), then
+// partial of <vnext, cand> (or |cand|^2 when vnext is null).  When src is
+// set the step starts from cand = src / divisor.
+__global__ void __launch_bounds__(kRedThreads)
+k_mgs_step(double* __restrict__ cand, const double* __restrict__ src, double divisor,
+           const double* __restrict__ vprev, const double* __restrict__ o_prev,
+           const double* __restrict__ vnext, uint64_t n, double* __restrict__ partial) {
+    __shared__ double sh[32];
+    const double o = vprev ? *o_prev : 0.0;
+    double acc = 0.0;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        double c = src ? src[i] / divisor : cand[i];
+        if (vprev) c -= o * vprev[i];
+        cand[i] = c;
+        acc += (vnext ? vnext[i] : c) * c;
+    }
+    const double s = block_sum(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+__global__ void k_scale_div(double* __restrict__ x, uint64_t n, double divisor) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        x[i] /= divisor;
+}
+
+__global__ void k_set_unit(double* __restrict__ x, uint64_t n, uint64_t at) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        x[i] = i == at ? 1.0 : 0.0;
+}
+
+// Per-block (min value, lowest index) of diag, then a final pass.
+__global__ void k_argmin(const double* __restrict__ d, uint64_t n, double* __restrict__ pv,
+                         uint64_t* __restrict__ pi) {
+    __shared__ double sv[kRedThreads];
+    __shared__ uint64_t si[kRedThreads];
+    double bv = INFINITY;
+    uint64_t bi = ~0ull;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const double v = d[i];
+        if (v < bv || (v == bv && i < bi)) {
+            bv = v;
+            bi = i;
+        }
+    }
+    sv[threadIdx.x] = bv;
+    si[threadIdx.x] = bi;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            const double ov = sv[threadIdx.x + s];
+            const uint64_t oi = si[threadIdx.x + s];
+            if (ov < sv[threadIdx.x] || (ov == sv[threadIdx.x] && oi < si[threadIdx.x])) {
+                sv[threadIdx.x] = ov;
+                si[threadIdx.x] = oi;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        pv[blockIdx.x] = sv[0];
+        pi[blockIdx.x] = si[0];
+    }
+}
+
+double seconds_since(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void ensure_red(Handle& h) {
+    if (h.red.n < static_cast<size_t>(2 * kMaxVec * kRedBlocks + 4 * kMaxVec))
+        h.red.alloc(static_cast<size_t>(2 * kMaxVec * kRedBlocks + 4 * kMaxVec));
+}
+
+// Device scalar slot (after the partials region) for MGS overlaps.
+double* scalar_slot(Handle& h, int i) { return h.red.p + 2 * kMaxVec * kRedBlocks + i; }
+
+void allreduce_device(Handle& h, double* dptr, int count) {
+    if (h.world <= 1) return;
+    if (ncclAllReduce(dptr, dptr, count, ncclDouble, ncclSum, h.nccl, h.stream) != ncclSuccess)
+        fail(DETCI_GPU_E_CUDA, "ncclAllReduce failed");
+}
+
+// Finalize `k` partial rows into device slots [slot, slot + k), allreduced.
+void finalize_to(Handle& h, int k, int slot) {
+    k_finalize<<<k, 32, 0, h.stream>>>(h.red.p, kRedBlocks, k, scalar_slot(h, slot));
+    CUDA_LAUNCH_CHECK();
+    allreduce_device(h, scalar_slot(h, slot), k);
+}
+
+void read_slots(Handle& h, int slot, int k, double* out) {
+    CUDA_CHECK(cudaMemcpyAsync(out, scalar_slot(h, slot), k * sizeof(double), cudaMemcpyDeviceToHost,
+                               h.stream));
+    CUDA_CHECK(cudaStreamSynchronize(h.stream));
+}
+
+} // namespace
+
+void allreduce_sum(Handle& h, double* host_vals, int count) {
+    if (h.world <= 1) return;
+    ensure_red(h);
+    double* d = scalar_slot(h, 3 * kMaxVec);
+    CUDA_CHECK(cudaMemcpyAsync(d, host_vals, count * sizeof(double), cudaMemcpyHostToDevice, h.stream));
+    allreduce_device(h, d, count);
+    CUDA_CHECK(cudaMemcpyAsync(host_vals, d, count * sizeof(double), cudaMemcpyDeviceToHost, h.stream));
+    CUDA_CHECK(cudaStreamSynchronize(h.stream));
+}
+
+void device_dot_many(Handle& h, const double* x, const double* const* ys, int k, uint64_t n,
+                     double* out_host) {
+    if (k > 2 * kMaxVec) fail(DETCI_GPU_E_CONFIG, "dot_many: too many vectors");
+    ensure_red(h);
+    VecList vl{};
+    for (int j = 0; j < k; ++j) vl.p[j] = ys[j];
+    k_dot_many<<<kRedBlocks, kRedThreads, 0, h.stream>>>(x, vl, k, n, h.red.p);
+    CUDA_LAUNCH_CHECK();
+    for (int j0 = 0; j0 < k; j0 += kMaxVec) {
+        const int kk = std::min(kMaxVec, k - j0);
+        k_finalize<<<kk, 32, 0, h.stream>>>(h.red.p + static_cast<size_t>(j0) * kRedBlocks, kRedBlocks,
+                                             kk, scalar_slot(h, 0));
+        CUDA_LAUNCH_CHECK();
+        allreduce_device(h, scalar_slot(h, 0), kk);
+        read_slots(h, 0, kk, out_host + j0);
+    }
+}
+
+double device_dot(Handle& h, const double* x, const double* y, uint64_t n) {
+    double v = 0.0;
+    device_dot_many(h, x, &y, 1, n, &v);
+    return v;
+}
+
+// Smallest eigenpair of the k x k symmetric matrix given by its lower
+// triangle lower[i * ld + j], j <= i.  Cyclic Jacobi to machine precision.
+double smallest_eigenpair(const std::vector<double>& lower, int ld, int k, std::vector<double>& vec) {
+    std::vector<double> a(static_cast<size_t>(k) * k), v(static_cast<size_t>(k) * k, 0.0);
+    for (int i = 0; i < k; ++i) {
+        for (int j = 0; j < k; ++j) a[i * k + j] = i >= j ? lower[i * ld + j] : lower[j * ld + i];
+        v[i * k + i] = 1.0;
+    }
+    for (int sweep = 0; sweep < 100; ++sweep) {
+        double off = 0.0, tot = 0.0;
+        for (int i = 0; i < k; ++i)
+            for (int j = 0; j < k; ++j) {
+                tot += a[i * k + j] * a[i * k + j];
+                if (i != j) off += a[i * k + j] * a[i * k + j];
+            }
+        if (off == 0.0 || off <= 1e-30 * tot) break;
+        for (int p = 0; p < k; ++p)
+            for (int q = p + 1; q < k; ++q) {
+                const double apq = a[p * k + q];
+                if (apq == 0.0) continue;
+                const double tau = (a[q * k + q] - a[p * k + p]) / (2.0 * apq);
+                const double t = (tau >= 0 ? 1.0 : -1.0) / (std::fabs(tau) + std::sqrt(1.0 + tau * tau));
+                const double c = 1.0 / std::sqrt(1.0 + t * t), s = t * c;
+                for (int r = 0; r < k; ++r) {
+                    const double arp = a[r * k + p], arq = a[r * k + q];
+                    a[r * k + p] = c * arp - s * arq;
+                    a[r * k + q] = s * arp + c * arq;
+                }
+                for (int r = 0; r < k; ++r) {
+                    const double apr = a[p * k + r], aqr = a[q * k + r];
+                    a[p * k + r] = c * apr - s * aqr;
+                    a[q * k + r] = s * apr + c * aqr;
+                }
+                for (int r = 0; r < k; ++r) {
+                    const double vrp = v[r * k + p], vrq = v[r * k + q];
+                    v[r * k + p] = c * vrp - s * vrq;
+                    v[r * k + q] = s * vrp + c * vrq;
+                }
+            }
+    }
+    int m = 0;
+    for (int i = 1; i < k; ++i)
+        if (a[i * k + i] < a[m * k + m]) m = i;
+    vec.assign(k, 0.0);
+    for (int i = 0; i < k; ++i) vec[i] = v[i * k + m];
+    return a[m * k + m];
+}
+
+void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* res,
+                     detci_trace_cb cb, void* user) {
+    if (!h.built) fail(DETCI_GPU_E_INPUT, "davidson_solve: basis not built");
+    const uint64_t n = h.local_len();
+    if (n == 0) fail(DETCI_GPU_E_INPUT, "davidson_solve: empty diagonal");
+    if (!(opts.tol > 0.0)) fail(DETCI_GPU_E_CONFIG, "davidson_solve: tol must be positive");
+    if (opts.max_subspace < 2) fail(DETCI_GPU_E_CONFIG, "davidson_solve: max_subspace must be >= 2");
+    if (opts.max_iter < 1) fail(DETCI_GPU_E_CONFIG, "davidson_solve: max_iter must be positive");
+    if (opts.max_subspace > kMaxVec)
+        fail(DETCI_GPU_E_UNSUPPORTED, "davidson_solve: max_subspace above 64");
+    ensure_red(h);
+    const int ms = opts.max_subspace;
+    const auto wall0 = std::chrono::steady_clock::now();
+
+    size_t free_b = 0, total_b = 0;
+    CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+    const size_t need = (2 * static_cast<size_t>(ms) + 3) * n * sizeof(double);
+    const uint64_t budget = h.budget ? h.budget : free_b;
+    if (need > std::min<uint64_t>(budget, free_b))
+        fail(DETCI_GPU_E_CAPACITY, "davidson vectors require " + std::to_string(need) +
+                                       " bytes, budget is " + std::to_string(std::min<uint64_t>(budget, free_b)) +
+                                       " bytes");
+    DevBuf<double> store;
+    store.alloc((2 * static_cast<size_t>(ms) + 3) * n);
+    auto V = [&](int j) { return store.p + static_cast<size_t>(j) * n; };
+    auto Wv = [&](int j) { return store.p + static_cast<size_t>(ms + j) * n; };
+    double* ritz = store.p + static_cast<size_t>(2 * ms) * n;
+    double* img = ritz + n;
+    double* corr = img + n;
+    const unsigned vgrid = kRedBlocks;
+
+    // Initial vector (davidson.cpp:84-97).
+    if (opts.initial_guess) {
+        CUDA_CHECK(cudaMemcpyAsync(V(0), opts.initial_guess, n * sizeof(double), cudaMemcpyHostToDevice,
+                                   h.stream));
+        const double nrm2 = device_dot(h, V(0), V(0), n);
+        const double norm = std::sqrt(nrm2);
+        if (!(norm > 0.0)) fail(DETCI_GPU_E_INPUT, "davidson_solve: zero initial guess");
+        k_scale_div<<<vgrid, kRedThreads, 0, h.stream>>>(V(0), n, norm);
+        CUDA_LAUNCH_CHECK();
+    } else {
+        DevBuf<double> pv;
+        DevBuf<uint64_t> pi;
+        pv.alloc(kRedBlocks);
+        pi.alloc(kRedBlocks);
+        k_argmin<<<kRedBlocks, kRedThreads, 0, h.stream>>>(h.diag.p, n, pv.p, pi.p);
+        CUDA_LAUNCH_CHECK();
+        std::vector<double> hv(kRedBlocks);
+        std::vector<uint64_t> hi(kRedBlocks);
+        CUDA_CHECK(cudaMemcpyAsync(hv.data(), pv.p, kRedBlocks * sizeof(double), cudaMemcpyDeviceToHost, h.stream));
+        CUDA_CHECK(cudaMemcpyAsync(hi.data(), pi.p, kRedBlocks * sizeof(uint64_t), cudaMemcpyDeviceToHost, h.stream));
+        CUDA_CHECK(cudaStreamSynchronize(h.stream));
+        double bv = INFINITY;
+        uint64_t bi = ~0ull;
+        for (int b = 0; b < kRedBlocks; ++b)
+            if (hv[b] < bv || (hv[b] == bv && hi[b] < bi)) {
+                bv = hv[b];
+                bi = hi[b];
+            }
+        // Global argmin across ranks: lowest value, then lowest global index.
+        uint64_t owner_index = bi + h.a0 * h.nb();
+        if (h.world > 1) {
+            std::vector<double> all(2 * h.world, 0.0);
+            all[2 * h.rank] = bv;
+            all[2 * h.rank + 1] = static_cast<double>(owner_index);
+            allreduce_sum(h, all.data(), 2 * h.world);
+            double gv = INFINITY;
+            double gi = 0;
+            for (int r = 0; r < h.world; ++r)
+                if (all[2 * r] < gv || (all[2 * r] == gv && all[2 * r + 1] < gi)) {
+                    gv = all[2 * r];
+                    gi = all[2 * r + 1];
+                }
+            owner_index = static_cast<uint64_t>(gi);
+        }
+        const uint64_t lo = h.a0 * h.nb(), local_at = owner_index >= lo && owner_index < lo + n
+                                                          ? owner_index - lo
+                                                          : ~0ull;
+        k_set_unit<<<vgrid, kRedThreads, 0, h.stream>>>(V(0), n, local_at);
+        CUDA_LAUNCH_CHECK();
+    }
+
+    std::vector<double> proj(static_cast<size_t>(ms) * ms, 0.0);
+    std::vector<double> gram(static_cast<size_t>(ms) * ms, 0.0);
+    std::vector<double> coeffs;
+    int k_sub = 1, k_img = 0;
+    bool restart_pending = false;
+    double theta = 0.0;
+    int status = 0, iters = 0;
+    std::vector<detci_dav_iter> trace;
+
+    for (int iter = 0; iter < opts.max_iter; ++iter) {
+        detci_dav_iter st{};
+        st.restarted = restart_pending ? 1 : 0;
+        restart_pending = false;
+
+        auto t0 = std::chrono::steady_clock::now();
+        while (k_img < k_sub) {
+            sigma_device(h, V(k_img), Wv(k_img), nullptr);
+            ++k_img;
+        }
+        st.matvec_seconds = seconds_since(t0);
+
+        const int k = k_sub;
+        t0 = std::chrono::steady_clock::now();
+        {
+            // projected row k-1 and Gram row k-1 in one pass over V[k-1]
+            std::vector<const double*> ys(2 * k);
+            for (int j = 0; j < k; ++j) {
+                ys[j] = Wv(j);
+                ys[k + j] = V(j);
+            }
+            std::vector<double> dots(2 * k);
+            device_dot_many(h, V(k - 1), ys.data(), 2 * k, n, dots.data());
+            for (int j = 0; j < k; ++j) {
+                proj[(k - 1) * ms + j] = dots[j];
+                gram[(k - 1) * ms + j] = dots[k + j];
+            }
+        }
+        theta = smallest_eigenpair(proj, ms, k, coeffs);
+        st.subspace_solve_seconds = seconds_since(t0);
+
+        t0 = std::chrono::steady_clock::now();
+        RitzArgs ra{};
+        for (int j = 0; j < k; ++j) {
+            ra.v[j] = V(j);
+            ra.w[j] = Wv(j);
+            ra.c[j] = coeffs[j];
+        }
+        ra.k = k;
+        ra.theta = theta;
+        k_ritz<<<kRedBlocks, kRedThreads, 0, h.stream>>>(ra, h.diag.p, n, ritz, img, corr, h.red.p);
+        CUDA_LAUNCH_CHECK();
+        finalize_to(h, 2, 0);
+        double norms2[2];
+        read_slots(h, 0, 2, norms2);
+        const double rnorm = std::sqrt(norms2[0]);
+        const double cnorm = std::sqrt(norms2[1]);
+
+        double gdev = 0.0;
+        for (int i = 0; i < k; ++i)
+            for (int j = 0; j <= i; ++j)
+                gdev = std::max(gdev, std::fabs(gram[i * ms + j] - (i == j ? 1.0 : 0.0)));
+        st.max_gram_deviation = gdev;
+        st.ritz_value = theta;
+        st.residual_norm = rnorm;
+
+        const bool converged = rnorm <= opts.tol;
+        const bool last = iter + 1 == opts.max_iter;
+        auto push = [&]() {
+            st.orthogonalization_seconds = seconds_since(t0);
+            trace.push_back(st);
+            if (cb) cb(&trace.back(), iters, user);
+            ++iters;
+        };
+        if (converged || last) {
+            push();
+            status = converged ? 0 : 1;
+            break;
+        }
+        if (!(cnorm > 0.0)) {
+            push();
+            status = 2;
+            break;
+        }
+        if (k_sub >= ms) {  // collapse (davidson.cpp:178-184)
+            CUDA_CHECK(cudaMemcpyAsync(V(0), ritz, n * sizeof(double), cudaMemcpyDeviceToDevice, h.stream));
+            CUDA_CHECK(cudaMemcpyAsync(Wv(0), img, n * sizeof(double), cudaMemcpyDeviceToDevice, h.stream));
+            k_sub = k_img = 1;
+            const double* y2[2] = {Wv(0), V(0)};
+            double d2[2];
+            device_dot_many(h, V(0), y2, 2, n, d2);
+            proj[0] = d2[0];
+            gram[0] = d2[1];
+            restart_pending = true;
+        }
+        // corr / |corr| then 2-pass MGS against V[0..k_sub) into V[k_sub]
+        double* cand = V(k_sub);
+        const int steps = 2 * k_sub;
+        for (int t = 0; t <= steps; ++t) {
+            const double* src = t == 0 ? corr : nullptr;
+            const double* vprev = t == 0 ? nullptr : V((t - 1) % k_sub);
+            const double* vnext = t == steps ? nullptr : V(t % k_sub);
+            k_mgs_step<<<kRedBlocks, kRedThreads, 0, h.stream>>>(cand, src, cnorm, vprev,
+                                                                  scalar_slot(h, 4 + (t + 1) % 2),
+                                                                  vnext, n, h.red.p);
+            CUDA_LAUNCH_CHECK();
+            finalize_to(h, 1, 4 + t % 2);
+        }
+        double nrm2 = 0.0;
+        read_slots(h, 4 + steps % 2, 1, &nrm2);
+        const double norm = std::sqrt(nrm2);
+        push();
+        if (!(norm >= 1e-10)) {
+            status = 2;
+            break;
+        }
+        k_scale_div<<<vgrid, kRedThreads, 0, h.stream>>>(cand, n, norm);
+        CUDA_LAUNCH_CHECK();
+        ++k_sub;
+    }
+
+    res->status = status;
+    res->converged = status == 0;
+    res->iterations = iters;
+    res->energy = theta;
+    if (res->eigenvector) {
+        const double nrm = std::sqrt(device_dot(h, ritz, ritz, n));
+        k_scale_div<<<vgrid, kRedThreads, 0, h.stream>>>(ritz, n, nrm);
+        CUDA_LAUNCH_CHECK();
+        CUDA_CHECK(cudaMemcpyAsync(res->eigenvector, ritz, n * sizeof(double), cudaMemcpyDeviceToHost,
+                                   h.stream));
+    }
+    if (res->trace)
+        for (int i = 0; i < std::min(res->trace_cap, iters); ++i) res->trace[i] = trace[i];
+    CUDA_CHECK(cudaStreamSynchronize(h.stream));
+    res->seconds = seconds_since(wall0);
+}
+
+} // namespace detci_gpu

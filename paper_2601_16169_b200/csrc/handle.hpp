@@ -1,0 +1,136 @@
+// Internal state of a detci_gpu_handle: the device-resident basis.
+//
+// HBM layout: per channel the uint64 string table,
+// the four helper lists exactly as FlatExcitationTable (flat u32, offset u64,
+// len u32; connectivity.hpp:24-33), a same-spin pair table parallel to each
+// list (value f64, spectator mask u64, J index u32), a spectator J table
+// J[tri(p,q)][string] = sum_{r in string} (pq|rr), the beta-singles SELL-32
+// table for the mixed term, this rank's diagonal and the C/sigma scratch.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/detci_gpu.h"
+#include "common.cuh"
+
+namespace detci_gpu {
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { reset(); }
+    void reset() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void alloc(size_t count) {
+        if (count == n && p) return;
+        reset();
+        if (count == 0) return;
+        CUDA_CHECK(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    size_t bytes() const { return n * sizeof(T); }
+};
+
+struct ChannelTables {
+    size_t n = 0;                      // strings in this channel (global)
+    int n_elec = 0;
+    std::vector<uint64_t> h_strings;
+    DevBuf<uint64_t> strings;
+    // kind 0 = singles, 1 = doubles
+    DevBuf<uint32_t> flat[2];
+    DevBuf<uint64_t> offset[2];
+    DevBuf<uint32_t> len[2];
+    uint64_t nflat[2] = {0, 0};
+    std::vector<uint32_t> h_len[2];
+    // same-spin pair tables (this channel moves, the other is spectator)
+    DevBuf<double> pv[2];
+    DevBuf<uint64_t> pmask[2];
+    DevBuf<uint32_t> pab;              // singles: tri(p,q) | sign << 31
+    // this channel as spectator: J[tri * n + i]
+    DevBuf<double> J;
+};
+
+struct Handle {
+    int device = 0;
+    int rank = 0;
+    int world = 1;
+    int vblocks = 1;   // virtual alpha blocks on one GPU (tests the ring schedule)
+    int weighted = 0;
+    uint64_t budget = 0;
+    std::string err;
+
+    int norbs = 0;
+    bool have_strings = false, have_ints = false, built = false;
+    double core = 0.0;
+    std::vector<double> h1, eri;
+    DevBuf<double> d_h1, d_eri;
+
+    ChannelTables ch[2];
+
+    // mixed term: beta singles in SELL-32, bucketed by jb segment
+    DevBuf<uint32_t> sell;
+    DevBuf<uint64_t> sell_off;         // [slice * nseg + seg]
+    DevBuf<uint32_t> sell_len;         // [slice * nseg + seg]
+    uint32_t seg_cols = 0, nseg = 1, nslices = 0;
+
+    // alpha-block partition: P = world (NCCL) or vblocks (virtual)
+    std::vector<uint64_t> blk;
+    uint64_t a0 = 0, a1 = 0;           // this rank's rows
+    uint64_t max_blk = 0;
+
+    DevBuf<double> diag;               // (a1 - a0) * nb
+
+    // sigma scratch
+    DevBuf<double> ct, yt;             // nb * max_blk
+    DevBuf<double> ring[2];            // max_blk * nb
+    DevBuf<double> xbuf, ybuf;         // host-pointer staging, local length
+    DevBuf<double> red;                // reduction partials
+    DevBuf<unsigned int> red_count;
+
+    cudaStream_t stream = nullptr, comm_stream = nullptr;
+    cudaEvent_t ev[16] = {};
+    ncclComm_t nccl = nullptr;
+
+    uint64_t nnz_alpha = 0, nnz_beta = 0, nnz_mixed = 0;
+
+    size_t na() const { return ch[0].n; }
+    size_t nb() const { return ch[1].n; }
+    uint64_t nloc() const { return a1 - a0; }
+    size_t local_len() const { return static_cast<size_t>(a1 - a0) * nb(); }
+};
+
+// basis.cu
+void plan_partition(uint64_t na, uint64_t nb, const uint32_t* sa, const uint32_t* da,
+                    const uint32_t* sb, const uint32_t* db, int P, int weighted, uint64_t* blk);
+void build_device_basis(Handle& h);
+void release_basis(Handle& h);
+
+// sigma.cu
+void sigma_device(Handle& h, const double* dx, double* dy, detci_gpu_timings* tm);
+
+// davidson.cu
+struct DavidsonOutcome {
+    int status = 0, iterations = 0;
+    double energy = 0.0, seconds = 0.0;
+};
+void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* res,
+                     detci_trace_cb cb, void* user);
+double device_dot(Handle& h, const double* x, const double* y, uint64_t n);
+void device_dot_many(Handle& h, const double* x, const double* const* ys, int k, uint64_t n,
+                     double* out_host);
+void allreduce_sum(Handle& h, double* host_vals, int count);
+double smallest_eigenpair(const std::vector<double>& lower, int ld, int k, std::vector<double>& vec);
+
+} // namespace detci_gpu

@@ -1,0 +1,307 @@
+"""Host-side mirror of the reference detci API for the sigma hot path.
+
+Same names, argument meaning and error behaviour as the reference C++ API
+(paths relative to /root/reference/proj/core):
+
+  Basis / build_basis      basis.hpp:42-90     -> GpuBasis / build_basis
+  matvec                   matvec.hpp:64-68    -> matvec
+  LinearOperator           davidson.hpp:28     -> GpuBasis.linear_operator()
+  DavidsonOptions/Result   davidson.hpp:30-65  -> DavidsonOptions / DavidsonResult
+  davidson_solve           davidson.hpp:85-86  -> davidson_solve
+  inner_product / orthonormalize / precondition  davidson.hpp:67-81
+
+Every call goes through libdetci_gpu.so (include/detci_gpu.h); there is no
+CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .errors import InputError, raise_for
+
+SOLVE_STATUS = {0: "converged", 1: "max_iterations", 2: "stagnated"}
+
+
+def _u64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint64))
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+@dataclass
+class BasisOptions:
+    """basis.hpp:24-34 (bit_length/cache are host-packing knobs with no
+    device meaning; the budget applies to device memory)."""
+
+    memory_budget_bytes: int = 0
+    device: int = 0
+    rank: int = 0
+    world_size: int = 1
+    nccl_id: Optional[bytes] = None
+    virtual_blocks: int = 1
+    weighted_partition: bool = False
+
+
+@dataclass
+class DavidsonOptions:
+    tol: float = 1e-8
+    max_iter: int = 200
+    max_subspace: int = 20
+    initial_guess: Optional[np.ndarray] = None
+
+
+@dataclass
+class IterationStats:
+    ritz_value: float
+    residual_norm: float
+    matvec_seconds: float
+    orthogonalization_seconds: float
+    subspace_solve_seconds: float
+    max_gram_deviation: float
+    restarted: bool
+
+
+@dataclass
+class DavidsonResult:
+    status: str
+    converged: bool
+    energy: float
+    eigenvector: Optional[np.ndarray]
+    iterations: List[IterationStats] = field(default_factory=list)
+    seconds: float = 0.0
+
+
+class GpuBasis:
+    """Device-resident tensor-product basis (the reference's Basis)."""
+
+    def __init__(self, norbs: int, alpha: Sequence[int], beta: Sequence[int], core: float,
+                 h1: np.ndarray, eri: np.ndarray, opts: BasisOptions = BasisOptions()):
+        self._lib = _lib.load()
+        self._h = C.c_void_p()
+        desc = _lib.Desc()
+        desc.device = opts.device
+        desc.rank = opts.rank
+        desc.world_size = opts.world_size
+        self._nccl_id = None
+        if opts.nccl_id is not None:
+            self._nccl_id = (C.c_uint8 * 128).from_buffer_copy(opts.nccl_id)
+            desc.nccl_id = C.cast(self._nccl_id, _lib.u8p)
+        desc.virtual_blocks = opts.virtual_blocks
+        desc.weighted_partition = int(opts.weighted_partition)
+        desc.memory_budget_bytes = opts.memory_budget_bytes
+        self._check(self._lib.detci_gpu_create(C.byref(desc), C.byref(self._h)), use_handle=False)
+        self.norbs = int(norbs)
+        self.alpha = _u64(alpha)
+        self.beta = _u64(beta)
+        self.n_alpha = len(self.alpha)
+        self.n_beta = len(self.beta)
+        self._check(self._lib.detci_gpu_set_strings(self._h, self.norbs, _ptr(self.alpha, C.c_uint64),
+                                                    self.n_alpha, _ptr(self.beta, C.c_uint64), self.n_beta))
+        h1 = _f64(h1).reshape(-1)
+        eri = _f64(eri).reshape(-1)
+        if h1.size != norbs ** 2 or eri.size != norbs ** 4:
+            raise InputError("integrals: expected norbs^2 one-electron and norbs^4 two-electron values")
+        self._check(self._lib.detci_gpu_set_integrals(self._h, float(core), _ptr(h1, C.c_double),
+                                                      _ptr(eri, C.c_double)))
+        self._check(self._lib.detci_gpu_build_basis(self._h))
+        b, e, nb = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        self._check(self._lib.detci_gpu_local_rows(self._h, C.byref(b), C.byref(e), C.byref(nb)))
+        self.row_begin, self.row_end = b.value, e.value
+        self.local_dim = (e.value - b.value) * nb.value
+
+    # -- plumbing -----------------------------------------------------------
+    def _check(self, code: int, use_handle: bool = True) -> None:
+        if code:
+            msg = self._lib.detci_gpu_last_error(self._h if use_handle and self._h else None)
+            raise_for(code, (msg or b"").decode())
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) and self._h.value:
+            self._lib.detci_gpu_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def dimension(self) -> int:
+        return self.n_alpha * self.n_beta
+
+    # -- reference Basis members -------------------------------------------
+    def table(self, channel: int, kind: int):
+        """(flat u32, offset u64[n], len u32[n]) -- FlatExcitationTable."""
+        n = self.n_alpha if channel == 0 else self.n_beta
+        nflat = C.c_uint64()
+        self._check(self._lib.detci_gpu_helper_size(self._h, channel, kind, C.byref(nflat)))
+        flat = np.zeros(nflat.value, dtype=np.uint32)
+        off = np.zeros(n, dtype=np.uint64)
+        ln = np.zeros(n, dtype=np.uint32)
+        self._check(self._lib.detci_gpu_get_helpers(self._h, channel, kind, _ptr(flat, C.c_uint32),
+                                                    _ptr(off, C.c_uint64), _ptr(ln, C.c_uint32)))
+        return flat, off, ln
+
+    @property
+    def singles_a(self):
+        return self.table(0, 0)
+
+    @property
+    def doubles_a(self):
+        return self.table(0, 1)
+
+    @property
+    def singles_b(self):
+        return self.table(1, 0)
+
+    @property
+    def doubles_b(self):
+        return self.table(1, 1)
+
+    def diag(self) -> np.ndarray:
+        out = np.zeros(self.local_dim, dtype=np.float64)
+        self._check(self._lib.detci_gpu_diag(self._h, _ptr(out, C.c_double)))
+        return out
+
+    def nnz(self) -> dict:
+        t, a, b, m = (C.c_uint64() for _ in range(4))
+        self._check(self._lib.detci_gpu_nnz(self._h, C.byref(t), C.byref(a), C.byref(b), C.byref(m)))
+        return {"total": t.value, "alpha": a.value, "beta": b.value, "mixed": m.value}
+
+    def linear_operator(self) -> Callable[[np.ndarray, np.ndarray], None]:
+        """LinearOperator (davidson.hpp:28): y = H x on host arrays."""
+        return lambda x, y: matvec(self, x, y)
+
+
+def build_basis(alpha: Sequence[int], beta: Sequence[int], integrals, opts: BasisOptions = BasisOptions()) -> GpuBasis:
+    """build_basis (basis.hpp:85-86).  `integrals` exposes norbs, core, h1 (n^2), eri (n^4)."""
+    return GpuBasis(integrals.norbs, alpha, beta, integrals.core, integrals.h1, integrals.eri, opts)
+
+
+def matvec(basis: GpuBasis, x: np.ndarray, y: Optional[np.ndarray] = None, timings: Optional[dict] = None) -> np.ndarray:
+    """y = H x (matvec.hpp:64-68); length mismatch -> InputError (matvec.cpp:128-130)."""
+    x = _f64(x)
+    if x.size != basis.local_dim or (y is not None and y.size != basis.local_dim):
+        raise InputError(f"matvec: vector length {x.size} does not match basis dimension {basis.local_dim}")
+    out = np.empty(basis.local_dim, dtype=np.float64) if y is None else y
+    if out.dtype != np.float64 or not out.flags["C_CONTIGUOUS"]:
+        raise InputError("matvec: y must be a contiguous float64 array")
+    tm = _lib.Timings()
+    basis._check(basis._lib.detci_gpu_sigma(basis.handle, x.ctypes.data, out.ctypes.data, C.byref(tm)))
+    if timings is not None:
+        timings.update(tm.as_dict())
+    return out
+
+
+def davidson_solve(basis: GpuBasis, opts: DavidsonOptions = DavidsonOptions(), want_vector: bool = True,
+                   callback: Optional[Callable[[IterationStats, int], None]] = None) -> DavidsonResult:
+    """davidson_solve (davidson.hpp:85-86) over the device sigma and device vector ops."""
+    o = _lib.DavOpts()
+    o.tol = opts.tol
+    o.max_iter = opts.max_iter
+    o.max_subspace = opts.max_subspace
+    guess = None
+    if opts.initial_guess is not None:
+        guess = _f64(opts.initial_guess)
+        if guess.size != basis.local_dim:
+            raise InputError("davidson_solve: initial guess length mismatch")
+        o.initial_guess = _ptr(guess, C.c_double)
+    r = _lib.DavResult()
+    vec = np.zeros(basis.local_dim, dtype=np.float64) if want_vector else None
+    if vec is not None:
+        r.eigenvector = _ptr(vec, C.c_double)
+    cap = max(1, opts.max_iter)
+    trace = (_lib.DavIter * cap)()
+    r.trace = C.cast(trace, C.POINTER(_lib.DavIter))
+    r.trace_cap = cap
+
+    def _cb(it_ptr, i, _user):
+        if callback is not None:
+            it = it_ptr.contents
+            callback(_iter_stats(it), i)
+
+    cb = _lib.TRACE_CB(_cb)
+    basis._check(basis._lib.detci_gpu_davidson(basis.handle, C.byref(o), C.byref(r), cb, None))
+    its = [_iter_stats(trace[i]) for i in range(r.iterations)]
+    return DavidsonResult(status=SOLVE_STATUS[r.status], converged=bool(r.converged), energy=r.energy,
+                          eigenvector=vec, iterations=its, seconds=r.seconds)
+
+
+def _iter_stats(it) -> IterationStats:
+    return IterationStats(it.ritz_value, it.residual_norm, it.matvec_seconds, it.orthogonalization_seconds,
+                          it.subspace_solve_seconds, it.max_gram_deviation, bool(it.restarted))
+
+
+def inner_product(basis: GpuBasis, x, y) -> float:
+    x, y = _f64(x), _f64(y)
+    if x.size != y.size:
+        raise InputError(f"inner_product: length mismatch ({x.size} vs {y.size})")
+    out = C.c_double()
+    basis._check(basis._lib.detci_gpu_inner_product(basis.handle, _ptr(x, C.c_double), _ptr(y, C.c_double),
+                                                    x.size, C.byref(out)))
+    return out.value
+
+
+def orthonormalize(basis: GpuBasis, vs: Sequence[np.ndarray], candidate) -> Optional[np.ndarray]:
+    cand = _f64(candidate)
+    k = len(vs)
+    mat = _f64(np.stack(vs)) if k else np.zeros(1)
+    out = np.zeros_like(cand)
+    acc = C.c_int()
+    basis._check(basis._lib.detci_gpu_orthonormalize(basis.handle, _ptr(mat, C.c_double), k, cand.size,
+                                                     _ptr(cand, C.c_double), _ptr(out, C.c_double), C.byref(acc)))
+    return out if acc.value else None
+
+
+def precondition(basis: GpuBasis, residual, diag, theta: float) -> np.ndarray:
+    r, d = _f64(residual), _f64(diag)
+    if r.size != d.size:
+        raise InputError("precondition: residual and diagonal lengths differ")
+    out = np.zeros_like(r)
+    basis._check(basis._lib.detci_gpu_precondition(basis.handle, _ptr(r, C.c_double), _ptr(d, C.c_double),
+                                                   r.size, float(theta), _ptr(out, C.c_double)))
+    return out
+
+
+def factorized_element(integrals, bra_a: int, bra_b: int, ket_a: int, ket_b: int) -> float:
+    """<bra|H|ket> from the kernels' factorized closed forms (host, no GPU)."""
+    lib = _lib.load()
+    h1 = _f64(integrals.h1).reshape(-1)
+    eri = _f64(integrals.eri).reshape(-1)
+    out = C.c_double()
+    code = lib.detci_gpu_factorized_element(integrals.norbs, float(integrals.core), _ptr(h1, C.c_double),
+                                            _ptr(eri, C.c_double), bra_a, bra_b, ket_a, ket_b, C.byref(out))
+    raise_for(code, (lib.detci_gpu_last_error(None) or b"").decode())
+    return out.value
+
+
+def plan_partition(n_alpha: int, n_beta: int, len_sa, len_da, len_sb, len_db, P: int, weighted: bool) -> np.ndarray:
+    """Alpha-block boundaries for P ranks (host only; see detci_gpu_plan_partition)."""
+    lib = _lib.load()
+    arrs = [np.ascontiguousarray(np.asarray(a, dtype=np.uint32)) for a in (len_sa, len_da, len_sb, len_db)]
+    blk = np.zeros(P + 1, dtype=np.uint64)
+    code = lib.detci_gpu_plan_partition(n_alpha, n_beta, *[_ptr(a, C.c_uint32) for a in arrs], P, int(weighted),
+                                        _ptr(blk, C.c_uint64))
+    raise_for(code, (lib.detci_gpu_last_error(None) or b"").decode())
+    return blk
