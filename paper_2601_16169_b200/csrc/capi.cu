@@ -500,10 +500,10 @@ int detci_gpu_factorized_element(int norbs, double core, const double* h1, const
         }
         // mixed alpha single x beta single
         const int pa = __builtin_ctzll(bra_a & ~ket_a), qa = __builtin_ctzll(ket_a & ~bra_a);
-        const uint32_t ent = make_mixed_entry(bra_b, ket_b, 0, norbs);
-        const int cd = static_cast<int>((ent >> 18) & 0xfffu);
+        const MixedMove mv = mixed_move(bra_b, ket_b, norbs);
+        const int cd = static_cast<int>(mv.cd);
         double w = mixed_weight(eri, norbs, pa, qa, ket_a, cd / norbs, cd % norbs);
-        if (ent >> 31) w = -w;
+        if (mv.sbit) w = -w;
         if (mixed_outer_parity(bra_a, bra_b, pa, qa)) w = -w;
         *out = w;
     });

@@ -90,13 +90,28 @@ DG_HD PairEntry make_pair_entry(int ch, int kind, uint64_t si, uint64_t sj, cons
 }
 
 // Packed beta-single entry for the mixed term (SELL-32 table):
-//   bits 0..17 jb relative to its column segment, bits 18..29 cd = pb*n+qb,
-//   bit 31 = parity of popc(B_ib & open(pb, qb)).
-DG_HD uint32_t make_mixed_entry(uint64_t b_bra, uint64_t b_ket, uint32_t jb_local, int n) {
+//   bits 0..16  byte offset of C[ja, jb] inside the staged row segment
+//               (jb relative to its segment, times 8; segments <= 16383 cols)
+//   bits 17..31 index into the +-W table: cd + sbit * n^2 with cd = pb*n+qb
+//               and sbit = parity of popc(B_ib & open(pb, qb))
+// so the kernel needs one AND and one shift to address both gathers and the
+// sign of the beta half is folded into which half of +-W is read.
+struct MixedMove {
+    uint32_t cd;
+    uint32_t sbit;
+};
+
+DG_HD MixedMove mixed_move(uint64_t b_bra, uint64_t b_ket, int n) {
     const uint64_t x = b_bra & ~b_ket, y = b_ket & ~b_bra;
     const int pb = ctz64(x), qb = ctz64(y);
-    const uint32_t sbit = static_cast<uint32_t>(popc64(b_bra & open_mask(pb, qb)) & 1);
-    return jb_local | (static_cast<uint32_t>(pb * n + qb) << 18) | (sbit << 31);
+    MixedMove m;
+    m.cd = static_cast<uint32_t>(pb * n + qb);
+    m.sbit = static_cast<uint32_t>(popc64(b_bra & open_mask(pb, qb)) & 1);
+    return m;
+}
+
+DG_HD uint32_t encode_mixed_entry(uint32_t jb_local, uint32_t w_index) {
+    return (jb_local * 8u) | (w_index << 17);
 }
 
 // W_ja[cd] of the mixed term: (pa qa | c d) * (-1)^{popc(A'_ja & Mbeta(c,d))}

@@ -83,6 +83,7 @@ struct Handle {
     DevBuf<uint32_t> sell;
     DevBuf<uint64_t> sell_off;         // [slice * nseg + seg]
     DevBuf<uint32_t> sell_len;         // [slice * nseg + seg]
+    DevBuf<uint32_t> sell_perm;        // slot -> beta string (degree-sorted)
     uint32_t seg_cols = 0, nseg = 1, nslices = 0;
 
     // alpha-block partition: P = world (NCCL) or vblocks (virtual)

@@ -70,8 +70,20 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t 
     return lo;
 }
 
+// (-1)^{popc(S & M)} applied to the high word of x: parity of a 64-bit AND
+// via one 32-bit POPC of (lo ^ hi).
+__device__ __forceinline__ double spectator_signed(double x, uint32_t slo, uint32_t shi, uint32_t mlo,
+                                                   uint32_t mhi) {
+    const uint32_t par = __popc((slo & mlo) ^ (shi & mhi));
+    return __hiloint2double(__double2hiint(x) ^ static_cast<int>(par << 31), __double2loint(x));
+}
+
+// kTail: the CTA's column chunk crosses ncols, so column indices are clamped
+// (loads stay in bounds, stores are masked); full chunks use one base
+// pointer per entry with immediate offsets.
+template <bool kTail>
 __global__ void __launch_bounds__(kSSBlock)
-k_samespin(const SameSpinArgs a) {
+k_samespin(const SameSpinArgs a, uint32_t chunk0) {
     __shared__ uint32_t s_ja[kStage];
     __shared__ double s_v[kStage];
     __shared__ uint64_t s_m[kStage];
@@ -79,18 +91,21 @@ k_samespin(const SameSpinArgs a) {
     __shared__ uint64_t s_range[4];
 
     const uint32_t r = blockIdx.x % a.nrows;
-    const uint32_t chunk = blockIdx.x / a.nrows;
+    const uint32_t chunk = chunk0 + blockIdx.x / a.nrows;
     const uint32_t row = a.row0 + r;
     const uint32_t tid = threadIdx.x;
+    const uint32_t col0 = chunk * (kSSBlock * kSSR) + tid;
 
     uint32_t col[kSSR];
-    uint64_t spec[kSSR];
+    uint32_t slo[kSSR], shi[kSSR];
     double acc[kSSR];
 #pragma unroll
     for (int q = 0; q < kSSR; ++q) {
-        const uint32_t c = chunk * (kSSBlock * kSSR) + q * kSSBlock + tid;
-        col[q] = min(c, a.ncols - 1);  // clamp: loads stay in bounds, store is masked
-        spec[q] = a.spec[col[q]];
+        const uint32_t c = col0 + q * kSSBlock;
+        col[q] = kTail ? min(c, a.ncols - 1) : c;
+        const uint64_t sp = a.spec[col[q]];
+        slo[q] = static_cast<uint32_t>(sp);
+        shi[q] = static_cast<uint32_t>(sp >> 32);
         acc[q] = 0.0;
     }
 
@@ -122,29 +137,34 @@ k_samespin(const SameSpinArgs a) {
             if (kind == 0) {
 #pragma unroll 2
                 for (int e = 0; e < cnt; ++e) {
-                    const double* crow = a.C + static_cast<size_t>(s_ja[e]) * a.ldc;
+                    const size_t rowoff = static_cast<size_t>(s_ja[e]) * a.ldc;
                     const uint32_t ab = s_ab[e];
                     const double* jrow = a.J + static_cast<size_t>(ab & 0x7fffffffu) * a.ldj;
                     const double v = s_v[e];
                     const uint64_t m = s_m[e];
+                    const uint32_t mlo = static_cast<uint32_t>(m), mhi = static_cast<uint32_t>(m >> 32);
+                    const uint32_t jsign = ab & 0x80000000u;
 #pragma unroll
                     for (int q = 0; q < kSSR; ++q) {
-                        const double c = __ldg(crow + col[q]);
-                        const double j = __ldg(jrow + col[q]);
-                        const double val = v + flip_sign(j, ab >> 31);
-                        acc[q] = fma(flip_sign(val, parity64(spec[q] & m)), c, acc[q]);
+                        const uint32_t cq = kTail ? col[q] : col0 + q * kSSBlock;
+                        const double c = __ldg(a.C + rowoff + cq);
+                        const double j = __ldg(jrow + cq);
+                        const double val =
+                            v + __hiloint2double(__double2hiint(j) ^ static_cast<int>(jsign), __double2loint(j));
+                        acc[q] = fma(val, spectator_signed(c, slo[q], shi[q], mlo, mhi), acc[q]);
                     }
                 }
             } else {
 #pragma unroll 4
                 for (int e = 0; e < cnt; ++e) {
-                    const double* crow = a.C + static_cast<size_t>(s_ja[e]) * a.ldc;
+                    const double* base = a.C + static_cast<size_t>(s_ja[e]) * a.ldc + (kTail ? 0 : col0);
                     const double v = s_v[e];
                     const uint64_t m = s_m[e];
+                    const uint32_t mlo = static_cast<uint32_t>(m), mhi = static_cast<uint32_t>(m >> 32);
 #pragma unroll
                     for (int q = 0; q < kSSR; ++q) {
-                        const double c = __ldg(crow + col[q]);
-                        acc[q] = fma(flip_sign(v, parity64(spec[q] & m)), c, acc[q]);
+                        const double c = __ldg(kTail ? base + col[q] : base + q * kSSBlock);
+                        acc[q] = fma(v, spectator_signed(c, slo[q], shi[q], mlo, mhi), acc[q]);
                     }
                 }
             }
@@ -153,8 +173,8 @@ k_samespin(const SameSpinArgs a) {
 
 #pragma unroll
     for (int q = 0; q < kSSR; ++q) {
-        const uint32_t c = chunk * (kSSBlock * kSSR) + q * kSSBlock + tid;
-        if (c >= a.ncols) continue;
+        const uint32_t c = col0 + q * kSSBlock;
+        if (kTail && c >= a.ncols) continue;
         const size_t yi = static_cast<size_t>(r) * a.ldy + c;
         if (a.accumulate) {
             a.Y[yi] += acc[q];
@@ -193,6 +213,7 @@ struct MixedArgs {
     const uint32_t* sell;
     const uint64_t* sell_off;
     const uint32_t* sell_len;
+    const uint32_t* perm;     // slot -> beta string
     uint32_t seg_cols, nseg, nslices;
     const double* eri;
     int norbs;
@@ -208,8 +229,11 @@ __global__ void __launch_bounds__(kMxBlock, 2)
 k_mixed(const MixedArgs a) {
     extern __shared__ double smem[];
     const int nn = a.norbs * a.norbs;
-    double* W = smem;
-    double* crow = smem + ((nn + 1) & ~1);
+    double* W2 = smem;                                  // [+W | -W], 2*nn doubles
+    const uint32_t crow_dbl = static_cast<uint32_t>((2 * nn + 1) & ~1);
+    double* crow = smem + crow_dbl;
+    const char* wbase = reinterpret_cast<const char*>(smem);
+    const char* cbase = reinterpret_cast<const char*>(crow);
 
     const uint32_t r = blockIdx.x / a.nparts;
     const uint32_t part = blockIdx.x % a.nparts;
@@ -223,9 +247,9 @@ k_mixed(const MixedArgs a) {
     double sig[kMxR];
 #pragma unroll
     for (int q = 0; q < kMxR; ++q) {
-        const uint32_t ib = part * (kMxBlock * kMxR) + q * kMxBlock + tid;
-        B[q] = a.beta[min(ib, a.nb - 1)];
-        slice[q] = ib / kWarp;
+        const uint32_t slot = part * (kMxBlock * kMxR) + q * kMxBlock + tid;
+        B[q] = a.beta[a.perm[min(slot, a.nb - 1)]];
+        slice[q] = slot / kWarp;
         sig[q] = 0.0;
     }
 
@@ -249,10 +273,10 @@ k_mixed(const MixedArgs a) {
 
 #pragma unroll 1
         for (uint32_t g = 0; g < a.nseg; ++g) {
-            const uint32_t cbase = g * a.seg_cols;
-            const uint32_t segw = min(a.seg_cols, a.nb - cbase);
-            __syncthreads();  // previous users of W / crow are done
-            for (uint32_t c = tid; c < segw; c += kMxBlock) cp_async8(crow + c, src + cbase + c);
+            const uint32_t cbase_col = g * a.seg_cols;
+            const uint32_t segw = min(a.seg_cols, a.nb - cbase_col);
+            __syncthreads();  // previous users of W2 / crow are done
+            for (uint32_t c = tid; c < segw; c += kMxBlock) cp_async8(crow + c, src + cbase_col + c);
             if (g == 0) {
                 const double* erow = a.eri + static_cast<size_t>(pa * a.norbs + qa) * nn;
                 for (int cd = tid; cd < nn; cd += kMxBlock) {
@@ -262,7 +286,8 @@ k_mixed(const MixedArgs a) {
                         v = erow[cd];
                         if (__popcll(Ak & spectator_mask(1, c, d)) & 1) v = -v;
                     }
-                    W[cd] = v;
+                    W2[cd] = v;
+                    W2[nn + cd] = -v;
                 }
             }
             cp_async_wait_all();
@@ -272,15 +297,31 @@ k_mixed(const MixedArgs a) {
                 if (slice[q] >= a.nslices) continue;
                 const uint32_t L = a.sell_len[slice[q] * a.nseg + g];
                 const uint32_t* ent = a.sell + a.sell_off[slice[q] * a.nseg + g] + lane;
-                double s = 0.0;
-#pragma unroll 4
-                for (uint32_t t = 0; t < L; ++t) {
-                    const uint32_t e = __ldg(ent + static_cast<size_t>(t) * kWarp);
-                    const uint32_t jb = e & 0x3ffffu;
-                    const uint32_t cd = (e >> 18) & 0xfffu;
-                    s = fma(flip_sign_hi(W[cd], e), crow[jb], s);
+                double s0 = 0.0, s1 = 0.0;
+                uint32_t t = 0;
+#pragma unroll 1
+                for (; t + 8 <= L; t += 8) {
+                    uint32_t e[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) e[u] = __ldg(ent + static_cast<size_t>(t + u) * kWarp);
+#pragma unroll
+                    for (int u = 0; u < 8; u += 2) {
+                        const double w0 = *reinterpret_cast<const double*>(wbase + ((e[u] >> 17) << 3));
+                        const double c0 = *reinterpret_cast<const double*>(cbase + (e[u] & 0x1ffffu));
+                        const double w1 = *reinterpret_cast<const double*>(wbase + ((e[u + 1] >> 17) << 3));
+                        const double c1 = *reinterpret_cast<const double*>(cbase + (e[u + 1] & 0x1ffffu));
+                        s0 = fma(w0, c0, s0);
+                        s1 = fma(w1, c1, s1);
+                    }
                 }
-                acc[q] += s;
+#pragma unroll 1
+                for (; t < L; ++t) {
+                    const uint32_t e0 = __ldg(ent + static_cast<size_t>(t) * kWarp);
+                    const double w0 = *reinterpret_cast<const double*>(wbase + ((e0 >> 17) << 3));
+                    const double c0 = *reinterpret_cast<const double*>(cbase + (e0 & 0x1ffffu));
+                    s0 = fma(w0, c0, s0);
+                }
+                acc[q] += s0 + s1;
             }
         }
         const int sA = __popcll(A & open_mask(pa, qa)) & 1;
@@ -292,8 +333,8 @@ k_mixed(const MixedArgs a) {
 
 #pragma unroll
     for (int q = 0; q < kMxR; ++q) {
-        const uint32_t ib = part * (kMxBlock * kMxR) + q * kMxBlock + tid;
-        if (ib < a.nb) a.Y[static_cast<size_t>(r) * a.ldy + ib] += sig[q];
+        const uint32_t slot = part * (kMxBlock * kMxR) + q * kMxBlock + tid;
+        if (slot < a.nb) a.Y[static_cast<size_t>(r) * a.ldy + a.perm[slot]] += sig[q];
     }
 }
 
@@ -409,15 +450,22 @@ SameSpinArgs alpha_args(const Handle& h, const double* Cb, uint32_t b0, uint32_t
 
 void launch_samespin(const SameSpinArgs& s, cudaStream_t st) {
     if (s.nrows == 0 || s.ncols == 0) return;
-    const uint64_t chunks = (s.ncols + kSSBlock * kSSR - 1) / (kSSBlock * kSSR);
-    const uint64_t grid = chunks * s.nrows;
-    k_samespin<<<static_cast<unsigned>(grid), kSSBlock, 0, st>>>(s);
-    CUDA_LAUNCH_CHECK();
+    constexpr uint32_t kChunk = kSSBlock * kSSR;
+    const uint64_t full = s.ncols / kChunk;
+    const bool tail = s.ncols % kChunk != 0;
+    if (full) {
+        k_samespin<false><<<static_cast<unsigned>(full * s.nrows), kSSBlock, 0, st>>>(s, 0);
+        CUDA_LAUNCH_CHECK();
+    }
+    if (tail) {
+        k_samespin<true><<<s.nrows, kSSBlock, 0, st>>>(s, static_cast<uint32_t>(full));
+        CUDA_LAUNCH_CHECK();
+    }
 }
 
 size_t mixed_smem(const Handle& h) {
     const size_t nn = static_cast<size_t>(h.norbs) * h.norbs;
-    return (((nn + 1) & ~size_t{1}) + h.seg_cols) * sizeof(double);
+    return (((2 * nn + 1) & ~size_t{1}) + h.seg_cols) * sizeof(double);
 }
 
 void launch_mixed(const Handle& h, const double* Cb, uint32_t b0, uint32_t b1, double* y_loc,
@@ -442,6 +490,7 @@ void launch_mixed(const Handle& h, const double* Cb, uint32_t b0, uint32_t b1, d
     m.sell = h.sell.p;
     m.sell_off = h.sell_off.p;
     m.sell_len = h.sell_len.p;
+    m.perm = h.sell_perm.p;
     m.seg_cols = h.seg_cols;
     m.nseg = h.nseg;
     m.nslices = h.nslices;
@@ -513,9 +562,13 @@ template <class Fetch>
 void sigma_ring(Handle& h, int g, int P, const double* x_loc, double* y_loc, PhaseTimer& tm,
                 Fetch&& fetch) {
     const uint64_t a0 = h.blk[g], a1 = h.blk[g + 1];
-    beta_term(h, x_loc, a0, a1, tm);
     cudaEvent_t* done_compute = h.ev;      // [0..1]
     cudaEvent_t* done_comm = h.ev + 2;     // [2..3]
+    // x and the ring buffers are produced / last read on the compute stream:
+    // the comm stream must not send or overwrite them before that work ends.
+    CUDA_CHECK(cudaEventRecord(h.ev[4], h.stream));
+    CUDA_CHECK(cudaStreamWaitEvent(h.comm_stream, h.ev[4], 0));
+    beta_term(h, x_loc, a0, a1, tm);
     const double* held = x_loc;
     for (int s = 0; s < P; ++s) {
         const int b = (g + s) % P;
