@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""Benchmark of the Davidson sigma build (H*C) -- the BASELINE.json metric.
+
+    python bench.py [--gpus N --steps K --warmup W] [--config C2] [--impl reference]
+
+One "step" is one sigma = H*C over the whole selected determinant space of
+the configuration (default C2 = BASELINE configs[1]: 26 orbitals, 14 e,
+1e8 alpha x beta determinants, single B200).  `value` is determinants per
+second over all ranks (dim / device time of one sigma, max over ranks),
+inputs resident in HBM; `e2e` is the same through the public C-ABI call with
+host buffers (H2D of x and D2H of y inside the timed region).  Inputs are
+larger than L2 (0.8 GB per vector at C2), so no L2 flush is needed.
+
+--impl reference times the reference's own CPU sigma (the unmodified detci
+library compiled into oracle/_ref) on this host's cores, row-sampled
+(SURVEY.md 8(d)): whole alpha rows through the reference kernels in the
+reference contribution order, extrapolated by the exact per-row element
+count.  Only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = json.loads((ROOT / "BASELINE.json").read_text())["metric"]
+WORKLOADS = {
+    "C1": "C1: N2-like synthetic, 16 orbitals 10e, 1e6 alpha x beta dets",
+    "C2": "C2: N2 cc-pVDZ-sized synthetic, 26 orbitals 14e, 1e8 alpha x beta dets, single B200",
+    "C3": "C3: [2Fe-2S]-sized synthetic, 36 orbitals 30e, 3e8 alpha x beta dets",
+    "C4": "C4: [4Fe-4S]-sized synthetic, 36 orbitals 54e, 1e9 alpha x beta dets",
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+            time.sleep(0.3)
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.2)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+def row_work(la_s, la_d, lb_s, lb_d, nb):
+    """Exact element count per alpha row (matvec.cpp loop counts)."""
+    return (la_s + la_d).astype(np.float64) * nb + float((lb_s + lb_d).sum()) + la_s.astype(np.float64) * float(lb_s.sum())
+
+
+def reference_cpu(cfg: str, target_seconds: float, steps: int = 1, warmup: int = 0, threads: int = 0):
+    """Row-sampled reference sigma: returns (dets/s, per-step seconds, info)."""
+    from oracle.bindings import RefLib
+    from paper_2601_16169_b200 import synth
+
+    ref = RefLib()
+    threads = threads or ref.max_threads()
+    ints, a, b = synth.synthetic_system(cfg)
+    t0 = time.time()
+    rt = ref.table_from_integrals(ints)
+    rb = rt.basis(a, b, budget=64 << 30, workers=threads)       # reference defaults: det cache on
+    build_s = time.time() - t0
+    la = [rb.table(0, k)[2] for k in (0, 1)]
+    lb = [rb.table(1, k)[2] for k in (0, 1)]
+    work = row_work(la[0], la[1], lb[0], lb[1], len(b))
+    total = float(work.sum())
+    x = synth.random_vector(len(a) * len(b), 11)
+    rng = np.random.default_rng(7)
+    # calibrate: one row per thread
+    probe = rng.choice(len(a), size=min(len(a), threads), replace=False).astype(np.uint64)
+    t0 = time.time()
+    rb.matvec_rows(probe, x, workers=threads)
+    per_elem = (time.time() - t0) / float(work[probe.astype(np.int64)].sum())
+    nrows = int(np.clip(target_seconds / (per_elem * total / len(a)), threads, len(a)))
+    nrows = max(threads, (nrows // threads) * threads)
+    rates, secs = [], []
+    for i in range(warmup + steps):
+        rows = rng.choice(len(a), size=min(nrows, len(a)), replace=False).astype(np.uint64)
+        t0 = time.time()
+        rb.matvec_rows(rows, x, workers=threads)
+        dt = time.time() - t0
+        frac = float(work[rows.astype(np.int64)].sum()) / total
+        if i >= warmup:
+            secs.append(dt)
+            rates.append(len(a) * len(b) / (dt / frac))
+    info = {"rows_per_step": int(nrows), "n_alpha": len(a), "sample_fraction": float(nrows) / len(a),
+            "build_seconds": build_s, "threads": threads}
+    return float(np.median(rates)), secs, info
+
+
+# ---------------------------------------------------------------------------
+def run_reference_arm(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    value, secs, info = reference_cpu(args.config, args.ref_seconds, steps=args.steps, warmup=args.warmup)
+    cores = info["threads"]
+    sample = (f"{info['rows_per_step']} of {info['n_alpha']} alpha rows x all beta per step "
+              f"({100 * info['sample_fraction']:.2f}%), reference hij_words in matvec.cpp order, "
+              f"extrapolated by exact per-row element counts")
+    line = {
+        "metric": METRIC, "value": value, "unit": "dets/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(secs) if secs else None,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": WORKLOADS.get(args.config, args.config), "config": args.config,
+                   "reference": "unmodified detci (proj/core) built from /root/reference into oracle/_ref",
+                   "ms_per_step_is": "wall time of one row-sampled step (the sample, not a full sigma)"},
+        "cpu_baseline": {"value": value, "unit": "dets/s", "cores": cores, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": "dets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def run_gpu_arm(args):
+    import torch
+
+    from paper_2601_16169_b200 import _lib, detci, synth
+
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    lib = _lib.load()
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        obj = [None]
+        if rank == 0:
+            buf = (C.c_uint8 * 128)()
+            assert lib.detci_gpu_nccl_unique_id(buf) == 0
+            obj = [bytes(buf)]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    t_build = time.time()
+    ints, a, b = synth.synthetic_system(args.config)
+    opts = detci.BasisOptions(device=local_rank, rank=rank, world_size=world, nccl_id=nccl_id,
+                              weighted_partition=world > 1)
+    basis = detci.GpuBasis(ints.norbs, a, b, ints.core, ints.h1, ints.eri, opts)
+    build_s = time.time() - t_build
+    na, nb = len(a), len(b)
+    dim = na * nb
+    nnz = basis.nnz()
+    r0, r1 = basis.row_begin, basis.row_end
+    x_full = synth.random_vector(dim, 11)
+    x_loc = np.ascontiguousarray(x_full.reshape(na, nb)[r0:r1].ravel())
+    del x_full
+    dx = torch.from_numpy(x_loc).cuda()
+    dy = torch.empty_like(dx)
+    sp = C.c_void_p()
+    assert lib.detci_gpu_stream(basis.handle, C.byref(sp)) == 0
+    ext = torch.cuda.ExternalStream(sp.value, device=torch.device("cuda", local_rank))
+
+    def sigma_async():
+        code = lib.detci_gpu_sigma_async(basis.handle, dx.data_ptr(), dy.data_ptr())
+        if code:
+            raise RuntimeError(lib.detci_gpu_last_error(basis.handle).decode())
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        import torch.distributed as dist
+
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        sigma_async()
+    ext.synchronize()
+
+    # ---- timed region: K sigma steps, device events on the kernels' stream
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    barrier()
+    cnt0 = C.c_uint64()
+    lib.detci_gpu_launch_count(C.byref(cnt0))
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(ext)
+    for _ in range(args.steps):
+        sigma_async()
+    end.record(ext)
+    end.synchronize()
+    cnt1 = C.c_uint64()
+    lib.detci_gpu_launch_count(C.byref(cnt1))
+    barrier()
+    clocks = sampler.stop()
+    dev_s = max_over_ranks(start.elapsed_time(end) * 1e-3)
+    per_step = dev_s / args.steps
+    value = dim / per_step
+
+    # ---- per-kernel split (CUDA events around each phase on the same stream)
+    parts = {"alpha_seconds": [], "beta_seconds": [], "mixed_seconds": [], "combine_seconds": [], "total_seconds": []}
+    for _ in range(min(3, args.steps)):
+        tm = _lib.Timings()
+        assert lib.detci_gpu_sigma_device(basis.handle, dx.data_ptr(), dy.data_ptr(), C.byref(tm)) == 0
+        for k in parts:
+            parts[k].append(getattr(tm, k))
+    split = {k: max_over_ranks(float(np.mean(v))) for k, v in parts.items()}
+
+    # ---- parity spot check against the committed reference rows
+    parity = None
+    golden = ROOT / "tests" / "golden" / f"rows_{args.config}.npz"
+    if golden.exists():
+        g = np.load(golden)
+        y = dy.cpu().numpy().reshape(r1 - r0, nb)
+        errs = [float(np.max(np.abs(y[int(r) - r0] - g["sigma_rows"][i]) /
+                             np.maximum(1.0, np.maximum(np.abs(y[int(r) - r0]), np.abs(g["sigma_rows"][i])))))
+                for i, r in enumerate(g["rows"]) if r0 <= int(r) < r1]
+        parity = max(errs) if errs else None
+
+    # ---- end to end: public C-ABI call with pinned host buffers
+    hx = torch.from_numpy(x_loc).pin_memory()
+    hy = torch.empty_like(hx).pin_memory()
+    tmh = _lib.Timings()
+    assert lib.detci_gpu_sigma(basis.handle, hx.data_ptr(), hy.data_ptr(), C.byref(tmh)) == 0   # warm
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(ext)
+    for _ in range(args.steps):
+        assert lib.detci_gpu_sigma(basis.handle, hx.data_ptr(), hy.data_ptr(), None) == 0
+    e1.record(ext)
+    e1.synchronize()
+    e2e_s = max_over_ranks(e0.elapsed_time(e1) * 1e-3) / args.steps
+    barrier()
+
+    # ---- roofline (dominant kernel: the mixed alpha-beta term)
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s (B200_PROFILING.md)"
+    dim_loc = (r1 - r0) * nb
+    mixed_bytes = 8.0 * nnz["mixed"] * dim_loc / dim + 16.0 * dim_loc      # per rank per sigma
+    sigma_bytes = 8.0 * nnz["total"] + 24.0 * dim                             # SURVEY.md 8(d) gather model
+    ncu = {}
+    ncu_path = ROOT / "profiles" / "ncu_summary.json"
+    if ncu_path.exists():
+        ncu = json.loads(ncu_path.read_text()).get(args.config, {})
+    traffic = ncu.get("k_mixed", {}).get("dram_bytes") if world == 1 else None
+    achieved = mixed_bytes / split["mixed_seconds"] / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": "k_mixed",
+                "algorithmic_bytes": mixed_bytes, "peak_source": peak_src}
+    sigma_achieved = sigma_bytes / per_step / 1e9
+    roofline_sigma = {"bytes_per_sigma": sigma_bytes, "achieved": sigma_achieved, "unit": "GB/s",
+                      "frac_of_measured": sigma_achieved / peak, "frac_of_8TBs": sigma_achieved / 8000.0}
+
+    # ---- full Davidson (s/iter of the whole solver) on the same basis
+    dav = None
+    if args.davidson:
+        res = detci.davidson_solve(basis, detci.DavidsonOptions(max_iter=args.davidson_iters), want_vector=False)
+        dav = {"status": res.status, "iterations": len(res.iterations), "seconds": res.seconds,
+               "s_per_iter": res.seconds / max(1, len(res.iterations)), "energy": res.energy,
+               "sigma_share": sum(i.matvec_seconds for i in res.iterations) / res.seconds}
+
+    # ---- CPU baseline (reference on this host), rank 0 at N=1 only
+    cpu = None
+    if rank == 0 and world == 1 and args.cpu_baseline:
+        try:
+            v, secs, info = reference_cpu(args.config, args.ref_seconds, steps=1)
+            cpu = {"value": v, "unit": "dets/s", "cores": info["threads"], "kind": "reference",
+                   "sample": f"{info['rows_per_step']} of {info['n_alpha']} alpha rows x all beta "
+                             f"({100 * info['sample_fraction']:.2f}%) through the unmodified reference "
+                             f"kernels, extrapolated by exact element counts; {secs[0]:.1f} s"}
+        except Exception as exc:   # reference library missing on this box
+            cpu = {"value": None, "unit": "dets/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    launches = int(cnt1.value - cnt0.value)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "dets/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS.get(args.config, args.config), "config": args.config,
+                       "norbs": ints.norbs, "n_electrons": ints.nelec, "n_alpha": na, "n_beta": nb, "dim": dim,
+                       "nnz_offdiag": nnz["total"], "nnz_alpha": nnz["alpha"], "nnz_beta": nnz["beta"],
+                       "nnz_mixed": nnz["mixed"], "l2": "inputs larger than L2 (x, y = 8*dim bytes each)",
+                       "parallelism": f"alpha-block ring x{world} (NCCL send/recv)" if world > 1 else "single GPU",
+                       "build_seconds": build_s, "sigma_s_per_iter": per_step,
+                       "phase_seconds": split, "parity_rows_max_rel_err": parity},
+            "roofline": roofline,
+            "roofline_sigma": roofline_sigma,
+            "cpu_baseline": cpu,
+            "e2e": {"value": dim / e2e_s, "unit": "dets/s", "h2d_bytes_per_step": 8 * dim_loc,
+                    "d2h_bytes_per_step": 8 * dim_loc, "ms_per_step": e2e_s * 1e3},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "davidson": dav,
+        }
+        print(json.dumps(line), flush=True)
+    basis.close()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-seconds", type=float, default=8.0, help="target CPU seconds per reference sample")
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-davidson", dest="davidson", action="store_false")
+    ap.add_argument("--davidson-iters", type=int, default=30,
+                    help="Davidson iterations timed for s/iter (reference defaults otherwise)")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        log("bench: warmup raised to 3 (timing rules)")
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -177,6 +177,14 @@ int detci_gpu_sigma(detci_gpu_handle* h, const double* x_local, double* y_local,
  * synchronised before return.  x and y must not alias. */
 int detci_gpu_sigma_device(detci_gpu_handle* h, const double* dx, double* dy,
                            detci_gpu_timings* timings);
+/* Enqueue sigma on the handle's stream without a host synchronisation
+ * (back-to-back benchmark steps); pair with detci_gpu_stream + events. */
+int detci_gpu_sigma_async(detci_gpu_handle* h, const double* dx, double* dy);
+/* The handle's compute stream (a cudaStream_t) so callers can record events
+ * on the stream the kernels run on. */
+int detci_gpu_stream(const detci_gpu_handle* h, void** stream);
+/* Kernels this library has launched in the process so far (all handles). */
+int detci_gpu_launch_count(uint64_t* count);
 /* Device scratch sized for one local vector (for benchmarks/tests). */
 int detci_gpu_alloc_vector(detci_gpu_handle* h, double** dptr);
 int detci_gpu_free_vector(detci_gpu_handle* h, double* dptr);

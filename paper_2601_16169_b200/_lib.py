@@ -100,6 +100,9 @@ SIGNATURES = {
     "detci_gpu_diag": (C.c_int, [vp, dp]),
     "detci_gpu_sigma": (C.c_int, [vp, vp, vp, C.POINTER(Timings)]),
     "detci_gpu_sigma_device": (C.c_int, [vp, vp, vp, C.POINTER(Timings)]),
+    "detci_gpu_sigma_async": (C.c_int, [vp, vp, vp]),
+    "detci_gpu_stream": (C.c_int, [vp, C.POINTER(vp)]),
+    "detci_gpu_launch_count": (C.c_int, [u64p]),
     "detci_gpu_alloc_vector": (C.c_int, [vp, C.POINTER(vp)]),
     "detci_gpu_free_vector": (C.c_int, [vp, vp]),
     "detci_gpu_copy_vector": (C.c_int, [vp, vp, vp, C.c_int]),

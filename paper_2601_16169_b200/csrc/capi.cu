@@ -2,6 +2,7 @@
 // point converts internal failures to a status code (no exception crosses
 // the ABI) and records the message for detci_gpu_last_error.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -12,6 +13,11 @@
 #include "handle.hpp"
 
 using namespace detci_gpu;
+
+namespace detci_gpu {
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+} // namespace detci_gpu
 
 struct detci_gpu_handle {
     Handle h;
@@ -308,6 +314,29 @@ int detci_gpu_sigma_device(detci_gpu_handle* hh, const double* dx, double* dy, d
         activate(hh->h);
         if (tm) *tm = detci_gpu_timings{};
         sigma_device(hh->h, dx, dy, tm);
+    });
+}
+
+int detci_gpu_sigma_async(detci_gpu_handle* hh, const double* dx, double* dy) {
+    return guarded(hh, [&] {
+        require(hh != nullptr && dx && dy, DETCI_GPU_E_INPUT, "sigma: null argument");
+        require(dx != dy, DETCI_GPU_E_INPUT, "sigma: x and y must not alias");
+        activate(hh->h);
+        sigma_enqueue(hh->h, dx, dy);
+    });
+}
+
+int detci_gpu_stream(const detci_gpu_handle* hh, void** stream) {
+    return guarded(const_cast<detci_gpu_handle*>(hh), [&] {
+        require(hh && stream, DETCI_GPU_E_INPUT, "stream: null argument");
+        *stream = reinterpret_cast<void*>(hh->h.stream);
+    });
+}
+
+int detci_gpu_launch_count(uint64_t* count) {
+    return guarded(nullptr, [&] {
+        require(count != nullptr, DETCI_GPU_E_INPUT, "launch_count: null argument");
+        *count = g_launches.load();
     });
 }
 

@@ -34,7 +34,14 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 }
 
 #define CUDA_CHECK(expr) ::detci_gpu::cuda_check((expr), #expr, __FILE__, __LINE__)
-#define CUDA_LAUNCH_CHECK() ::detci_gpu::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+// Every kernel launch site ends with CUDA_LAUNCH_CHECK(), which also counts
+// the launch (detci_gpu_launch_count; bench.py reports it as gpu_launches).
+void count_launch();
+#define CUDA_LAUNCH_CHECK()                                                                  \
+    do {                                                                                     \
+        ::detci_gpu::count_launch();                                                         \
+        ::detci_gpu::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__);    \
+    } while (0)
 
 // Bits [lo, hi] inclusive of a 64-bit word (empty when lo > hi).
 __host__ __device__ __forceinline__ uint64_t bit_range(int lo, int hi) {

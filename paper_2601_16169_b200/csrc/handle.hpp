@@ -120,6 +120,7 @@ void release_basis(Handle& h);
 
 // sigma.cu
 void sigma_device(Handle& h, const double* dx, double* dy, detci_gpu_timings* tm);
+void sigma_enqueue(Handle& h, const double* dx, double* dy);  // no host sync
 
 // davidson.cu
 struct DavidsonOutcome {

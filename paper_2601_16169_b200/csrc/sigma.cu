@@ -596,15 +596,9 @@ void sigma_ring(Handle& h, int g, int P, const double* x_loc, double* y_loc, Pha
 
 } // namespace
 
-void sigma_device(Handle& h, const double* dx, double* dy, detci_gpu_timings* out) {
-    if (!h.built) fail(DETCI_GPU_E_INPUT, "sigma: basis not built");
-    PhaseTimer tm(h, out != nullptr);
-    cudaEvent_t t0 = nullptr, t1 = nullptr;
-    if (out) {
-        CUDA_CHECK(cudaEventCreate(&t0));
-        CUDA_CHECK(cudaEventCreate(&t1));
-        CUDA_CHECK(cudaEventRecord(t0, h.stream));
-    }
+namespace {
+
+void sigma_schedule(Handle& h, const double* dx, double* dy, PhaseTimer& tm) {
     const size_t nb = h.nb();
     const int P = std::max(h.world, h.vblocks);
     if (h.world > 1) {
@@ -633,6 +627,26 @@ void sigma_device(Handle& h, const double* dx, double* dy, detci_gpu_timings* ou
     } else {
         sigma_ring(h, 0, 1, dx, dy, tm, [](int, const double*, double*, int) {});
     }
+}
+
+} // namespace
+
+void sigma_enqueue(Handle& h, const double* dx, double* dy) {
+    if (!h.built) fail(DETCI_GPU_E_INPUT, "sigma: basis not built");
+    PhaseTimer tm(h, false);
+    sigma_schedule(h, dx, dy, tm);
+}
+
+void sigma_device(Handle& h, const double* dx, double* dy, detci_gpu_timings* out) {
+    if (!h.built) fail(DETCI_GPU_E_INPUT, "sigma: basis not built");
+    PhaseTimer tm(h, out != nullptr);
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (out) {
+        CUDA_CHECK(cudaEventCreate(&t0));
+        CUDA_CHECK(cudaEventCreate(&t1));
+        CUDA_CHECK(cudaEventRecord(t0, h.stream));
+    }
+    sigma_schedule(h, dx, dy, tm);
     if (out) {
         CUDA_CHECK(cudaEventRecord(t1, h.stream));
         CUDA_CHECK(cudaEventSynchronize(t1));

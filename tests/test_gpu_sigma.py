@@ -1,0 +1,134 @@
+"""sigma = H C on the B200 against the reference (test_matvec.cpp:109-189,
+acceptance.cpp:330-368) and the row-sampled reference at the BASELINE
+configs.  Tolerance: rel_diff = |a-b| / max(1,|a|,|b|) <= 1e-12."""
+import numpy as np
+import pytest
+
+from paper_2601_16169_b200 import detci, errors, synth
+from util import FIXTURES, GOLDEN, load_fixture, rel_diff
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_basis(ints, a, b, **kw):
+    return detci.GpuBasis(ints.norbs, a, b, ints.core, ints.h1, ints.eri, detci.BasisOptions(**kw))
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_fixture_sigma(name):
+    ints, d = load_fixture(name)
+    with gpu_basis(ints, d["alpha"], d["beta"]) as b:
+        assert rel_diff(detci.matvec(b, d["x11"]), d["sigma11"]) <= 1e-12
+
+
+def test_unit_vectors_reproduce_dense_columns():
+    ints, d = load_fixture("h4_chain")
+    dense = d["dense"]
+    with gpu_basis(ints, d["alpha"], d["beta"]) as b:
+        dim = b.dimension()
+        for j in range(dim):
+            e = np.zeros(dim)
+            e[j] = 1.0
+            assert np.max(np.abs(detci.matvec(b, e) - dense[:, j])) <= 1e-12
+
+
+def test_diagonal_only_system_multiplies_by_diag_exactly():
+    """test_matvec.cpp:123-135: y == diag * x bitwise."""
+    h1 = np.zeros((3, 3))
+    eri = np.zeros((3, 3, 3, 3))
+    for p in range(3):
+        h1[p, p] = -1.0 + 0.3 * p
+        eri[p, p, p, p] = 0.5
+    ints = synth.Integrals(3, 2, 0, 0.0, h1, eri)
+    s = synth.full_channel_strings(3, 1)
+    with gpu_basis(ints, s, s) as b:
+        x = synth.random_vector(b.dimension(), 5)
+        y = detci.matvec(b, x)
+        assert np.array_equal(y, b.diag() * x)
+
+
+def test_linearity():
+    ints, d = load_fixture("h4_chain")
+    with gpu_basis(ints, d["alpha"], d["beta"]) as b:
+        x = synth.random_vector(b.dimension(), 7)
+        z = synth.random_vector(b.dimension(), 9)
+        assert rel_diff(detci.matvec(b, x + z), detci.matvec(b, x) + detci.matvec(b, z)) <= 1e-12
+
+
+def test_symmetry():
+    ints, d = load_fixture("chain8")
+    with gpu_basis(ints, d["alpha"], d["beta"]) as b:
+        for rep in range(10):
+            x = synth.random_vector(b.dimension(), 100 + rep)
+            y = synth.random_vector(b.dimension(), 200 + rep)
+            assert rel_diff(x @ detci.matvec(b, y), detci.matvec(b, x) @ y) <= 1e-10
+
+
+def test_deterministic_bitwise():
+    ints, d = load_fixture("h6_ring")
+    with gpu_basis(ints, d["alpha"], d["beta"]) as b:
+        x = d["x11"]
+        assert np.array_equal(detci.matvec(b, x), detci.matvec(b, x))
+
+
+def test_dimension_mismatch_is_input_error():
+    ints, d = load_fixture("h2_minimal")
+    with gpu_basis(ints, d["alpha"], d["beta"]) as b:
+        with pytest.raises(errors.InputError):
+            detci.matvec(b, np.zeros(b.dimension() - 1))
+
+
+@pytest.mark.parametrize("blocks,weighted", [(2, False), (3, True), (7, False), (7, True)])
+def test_virtual_alpha_blocks_ring_equals_single(blocks, weighted):
+    """The multi-GPU schedule (alpha blocks + C ring) emulated on one GPU."""
+    ints = synth.synthetic_integrals(12, 8)
+    s = synth.synthetic_strings(12, 4, 200)
+    x = synth.random_vector(len(s) ** 2, 3)
+    with gpu_basis(ints, s, s) as b1:
+        y1 = detci.matvec(b1, x)
+    with gpu_basis(ints, s, s, virtual_blocks=blocks, weighted_partition=weighted) as bp:
+        yp = detci.matvec(bp, x)
+    assert rel_diff(yp, y1) <= 1e-12
+
+
+def test_synthetic_s12_sigma():
+    d = np.load(GOLDEN / "synthetic_s12.npz")
+    ints = synth.synthetic_integrals(12, 8)
+    with gpu_basis(ints, d["alpha"], d["beta"]) as b:
+        x = synth.random_vector(b.dimension(), 11)
+        assert rel_diff(detci.matvec(b, x), d["sigma11"]) <= 1e-12
+
+
+def test_asymmetric_alpha_beta_lists():
+    """Different alpha and beta string lists (n_alpha != n_beta, shuffled order)."""
+    from oracle.bindings import Oracle
+
+    ints = synth.synthetic_integrals(10, 7)
+    a = synth.synthetic_strings(10, 4, 90)
+    bb = synth.synthetic_strings(10, 3, 70)[::-1].copy()
+    o = Oracle().system(ints, a, bb, threads=4)
+    with gpu_basis(ints, a, bb) as b:
+        for ch in (0, 1):
+            for kind in (0, 1):
+                assert all(g.tobytes() == w.tobytes() for g, w in zip(b.table(ch, kind), o.tables[(ch, kind)]))
+        x = synth.random_vector(b.dimension(), 4)
+        assert rel_diff(detci.matvec(b, x), o.matvec(x)) <= 1e-12
+        assert rel_diff(b.diag(), o.diag) <= 1e-12
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3"])
+def test_config_sigma_rows_vs_reference(cfg):
+    """Row-sampled reference sigma (exact reference rows) at the
+    BASELINE configs, plus size-independent properties of the full vector."""
+    rows = np.load(GOLDEN / f"rows_{cfg}.npz")
+    ints, a, bb = synth.synthetic_system(cfg)
+    with gpu_basis(ints, a, bb) as b:
+        x = synth.random_vector(b.dimension(), 11)
+        y = detci.matvec(b, x)
+        r = rows["rows"].astype(np.int64)
+        assert rel_diff(y.reshape(len(a), -1)[r], rows["sigma_rows"]) <= 1e-12
+        # linearity and symmetry at full size
+        z = synth.random_vector(b.dimension(), 12)
+        hz = detci.matvec(b, z)
+        assert rel_diff(detci.matvec(b, x + z), y + hz) <= 1e-12
+        assert abs(x @ hz - y @ z) <= 1e-10 * max(1.0, abs(x @ hz))

@@ -1,0 +1,154 @@
+"""The C restatement oracle (oracle/detci_oracle.c) pinned against the
+reference: committed golden vectors generated from the unmodified reference
+library, the shipped chain8 golden (proj/test_output.txt:33), and -- when
+oracle/_ref/libdetci_ref.so is present -- live comparisons with it.
+CPU only."""
+import numpy as np
+import pytest
+
+from oracle.bindings import REF_SO, Oracle
+from paper_2601_16169_b200 import synth
+from util import FIXTURES, golden_meta, load_fixture, rel_diff, table_digest, tables_of
+
+orc = Oracle()
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_fixture_tables_diag_sigma_bitwise(name):
+    ints, d = load_fixture(name)
+    s = orc.system(ints, d["alpha"], d["beta"], threads=4)
+    for key, want in tables_of(d).items():
+        got = s.tables[key]
+        for g, w in zip(got, want):
+            assert g.dtype == w.dtype and np.array_equal(g, w), (name, key)
+    assert np.array_equal(s.diag, d["diag"])          # same arithmetic order -> bitwise
+    assert np.array_equal(s.matvec(d["x11"]), d["sigma11"])
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_fixture_davidson_energy(name):
+    ints, d = load_fixture(name)
+    s = orc.system(ints, d["alpha"], d["beta"], threads=4)
+    res = s.davidson()
+    assert res["status"] == 0
+    assert abs(res["energy"] - float(d["energy"])) <= 1e-10 * max(1.0, abs(float(d["energy"])))
+    if "dense_ground" in d:
+        assert abs(res["energy"] - float(d["dense_ground"])) <= 1e-10 * abs(float(d["dense_ground"]))
+
+
+def test_chain8_shipped_golden():
+    ints, d = load_fixture("chain8")
+    res = orc.system(ints, d["alpha"], d["beta"], threads=4).davidson()
+    assert f"{res['energy']:.12e}" == "-2.420193979007e+00"       # proj/test_output.txt:33
+
+
+def test_dense_columns_h4():
+    """test_matvec.cpp:109-121 on the oracle."""
+    ints, d = load_fixture("h4_chain")
+    s = orc.system(ints, d["alpha"], d["beta"], threads=2)
+    dim = len(d["alpha"]) * len(d["beta"])
+    for j in range(dim):
+        e = np.zeros(dim)
+        e[j] = 1.0
+        assert np.max(np.abs(s.matvec(e) - d["dense"][:, j])) <= 1e-12
+
+
+def test_connectivity_goldens():
+    """test_connectivity.cpp:48-75,132-139."""
+    strs = np.array([0b011, 0b101, 0b110], dtype=np.uint64)
+    f, o, l = orc.generate_table(strs, 3, 0)
+    assert list(l) == [2, 2, 2] and len(f) == 6
+    dump = "".join(" ".join(str(j) for j in f[o[i]:o[i] + l[i]]) + "\n" for i in range(3))
+    assert dump == "1 2\n0 2\n0 1\n"
+    f, o, l = orc.generate_table(strs, 3, 1)
+    assert list(l) == [0, 0, 0]
+    f, o, l = orc.generate_table(np.array([0b0011, 0b1100], dtype=np.uint64), 4, 1)
+    assert list(l) == [1, 1] and list(f) == [1, 0]
+    with pytest.raises(Exception):
+        orc.generate_table(np.array([0b0011, 0b0011], dtype=np.uint64), 4, 0)
+
+
+def test_pairwise_degree_oracle():
+    """test_connectivity.cpp:106-130: random subsets of C(6,3)."""
+    allc = synth.full_channel_strings(6, 3)
+    rng = synth.SplitMix64(41)
+    for _ in range(10):
+        sub = np.array([s for s in allc if rng.next() % 3 != 0], dtype=np.uint64)
+        for kind, deg in ((0, 1), (1, 2)):
+            f, o, l = orc.generate_table(sub, 6, kind)
+            got = {(i, int(j)) for i in range(len(sub)) for j in f[o[i]:o[i] + l[i]]}
+            want = {(i, j) for i in range(len(sub)) for j in range(len(sub))
+                    if i != j and bin(int(sub[i]) ^ int(sub[j])).count("1") // 2 == deg}
+            assert got == want
+
+
+def test_phase_probe_against_reference_values():
+    meta = golden_meta()["elements"]["phase_probe"]
+    probe = synth.Integrals(3, 2, 0, 0.0, np.zeros((3, 3)), np.zeros((3, 3, 3, 3)))
+    probe.h1[0, 1] = probe.h1[1, 0] = 0.25
+    s = orc.system(probe, np.array([1], dtype=np.uint64), np.array([1], dtype=np.uint64), threads=1)
+    assert s.hij(0b001, 0b001, 0b010, 0b001) == meta["a01_beta0"] == -0.25
+    assert s.hij(0b001, 0b100, 0b010, 0b100) == meta["a01_beta2"] == 0.25
+    assert s.hij(0b010, 0b001, 0b010, 0b010) == meta["b01_alpha1"]
+    assert s.hij(0b001, 0b001, 0b001, 0b010) == meta["b01_alpha0"]
+
+
+def test_elements_n36_against_reference_hij():
+    """Oracle hij vs the reference hij at 36 orbitals, bit_length 20 (4-word dets)."""
+    g = np.load(__import__("util").GOLDEN / "elements_n36.npz")
+    ints = synth.synthetic_integrals(36, 30)
+    assert __import__("util").golden_meta()["elements"]["eri_sha256_n36"] == _eri_sha(ints)
+    s = orc.system(ints, np.array([1], dtype=np.uint64), np.array([1], dtype=np.uint64), threads=1)
+    got = np.array([s.hij(*map(int, row)) for row in g["dets"]])
+    assert np.array_equal(got, g["values"])
+
+
+def _eri_sha(ints):
+    import hashlib
+
+    return hashlib.sha256(np.ascontiguousarray(ints.eri).tobytes() + np.ascontiguousarray(ints.h1).tobytes()).hexdigest()
+
+
+def test_synthetic_s12_bitwise():
+    d = np.load(__import__("util").GOLDEN / "synthetic_s12.npz")
+    ints = synth.synthetic_integrals(12, 8)
+    s = orc.system(ints, d["alpha"], d["beta"], threads=4)
+    for key, want in tables_of(d).items():
+        assert all(np.array_equal(g, w) for g, w in zip(s.tables[key], want))
+    assert np.array_equal(s.diag, d["diag"])
+    x = synth.random_vector(len(d["alpha"]) ** 2, 11)
+    assert np.array_equal(s.matvec(x), d["sigma11"])
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_config_tables_and_rows(cfg):
+    meta = golden_meta()[cfg]
+    ints, a, b = synth.synthetic_system(cfg)
+    assert _eri_sha(ints) == meta["eri_sha256"]
+    s = orc.system(ints, a, b)
+    for ch in (0, 1):
+        for kind in (0, 1):
+            assert table_digest(*s.tables[(ch, kind)]) == meta["tables_sha256"][f"{ch}{kind}"]
+    rows = np.load(__import__("util").GOLDEN / f"rows_{cfg}.npz")
+    x = synth.random_vector(len(a) * len(b), 11)
+    got = s.matvec_rows(rows["rows"][:2], x)
+    assert np.array_equal(got, rows["sigma_rows"][:2])     # exact oracle rows
+
+
+@pytest.mark.skipif(not REF_SO.exists(), reason="reference library not built here")
+def test_live_against_reference_random_sets():
+    from oracle.bindings import RefLib
+
+    ref = RefLib()
+    for seed in range(3):
+        ints = synth.synthetic_integrals(10, 6, seed=seed + 5)
+        strs = synth.synthetic_strings(10, 3, 60, seed=seed + 1)
+        perm = ref.shuffle(strs, 10, seed)
+        rb = ref.table_from_integrals(ints).basis(perm, strs)
+        s = orc.system(ints, perm, strs, threads=2)
+        for ch in (0, 1):
+            for kind in (0, 1):
+                assert all(np.array_equal(g, w) for g, w in zip(s.tables[(ch, kind)], rb.table(ch, kind)))
+        x = synth.random_vector(rb.dim(), seed)
+        assert np.array_equal(s.matvec(x), rb.matvec(x, a=3, b=2, t=2, workers=3))
+        assert rel_diff(s.davidson()["energy"], rb.davidson()["energy"]) <= 1e-10
