@@ -1,0 +1,162 @@
+// detci_gpu_shim.hpp -- the drop-in for code inside the reference tree
+// (proj/core).  Converts the reference's value types to the C-ABI
+// (include/detci_gpu.h) and rethrows status codes as detci::Error subclasses,
+// keeping the reference signatures:
+//
+//   build_basis_gpu(const detci::Basis&)          device copy of a host Basis
+//   matvec(DeviceBasis, x, y, MatvecTimings*)     matvec.hpp:64-65 (plan and
+//                                                 workers are scheduling-only
+//                                                 in the reference and have no
+//                                                 device meaning)
+//   linear_operator(DeviceBasis) -> detci::LinearOperator   davidson.hpp:28
+//   davidson_solve(DeviceBasis, DavidsonOptions) -> detci::DavidsonResult
+//
+// INTEGRATION.md shows the run.cpp hook (Method::Gpu) that uses these.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <span>
+#include <string>
+#include <vector>
+
+#include <detci/basis.hpp>
+#include <detci/davidson.hpp>
+#include <detci/error.hpp>
+#include <detci/matvec.hpp>
+
+#include "../include/detci_gpu.h"
+
+namespace detci::gpu {
+
+inline void rethrow(int code, const detci_gpu_handle* h) {
+    if (code == DETCI_GPU_OK) return;
+    const std::string msg = detci_gpu_last_error(h);
+    switch (code) {
+        case DETCI_GPU_E_INPUT: throw InputError(msg);
+        case DETCI_GPU_E_FORMAT: throw FormatError(msg);
+        case DETCI_GPU_E_CONFIG: throw ConfigError(msg);
+        case DETCI_GPU_E_CAPACITY: throw CapacityError(msg);
+        case DETCI_GPU_E_UNSUPPORTED: throw UnsupportedError(msg);
+        default: throw Error(msg);
+    }
+}
+
+/// One uint64 mask per channel string; the device path holds norbs <= 64.
+inline std::vector<std::uint64_t> channel_masks(const std::vector<BitString>& strings, int norbs) {
+    if (norbs > 64) throw UnsupportedError("gpu: norbs > 64 is not supported on the device path");
+    std::vector<std::uint64_t> out;
+    out.reserve(strings.size());
+    for (const BitString& s : strings) {
+        std::uint64_t m = 0;
+        for (int i : occupied_list(s)) m |= std::uint64_t{1} << i;
+        out.push_back(m);
+    }
+    return out;
+}
+
+struct DeviceOptions {
+    int device = 0, rank = 0, world_size = 1, virtual_blocks = 1;
+    bool weighted_partition = true;
+    const std::uint8_t* nccl_id = nullptr;
+    std::uint64_t memory_budget_bytes = 0;
+};
+
+class DeviceBasis {
+public:
+    explicit DeviceBasis(const Basis& basis, const DeviceOptions& o = {}) {
+        detci_gpu_desc d{o.device, o.rank, o.world_size, o.nccl_id, o.virtual_blocks,
+                         o.weighted_partition ? 1 : 0, o.memory_budget_bytes};
+        rethrow(detci_gpu_create(&d, &h_), nullptr);
+        try {
+            const int n = basis.norbs;
+            const auto a = channel_masks(basis.alpha_strings, n);
+            const auto b = channel_masks(basis.beta_strings, n);
+            rethrow(detci_gpu_set_strings(h_, n, a.data(), a.size(), b.data(), b.size()), h_);
+            const std::size_t nn = static_cast<std::size_t>(n);
+            std::vector<double> h1(nn * nn), eri(nn * nn * nn * nn);
+            for (int p = 0; p < n; ++p)
+                for (int q = 0; q < n; ++q) h1[p * nn + q] = basis.integrals.one_electron(p, q);
+            for (int p = 0; p < n; ++p)
+                for (int q = 0; q < n; ++q)
+                    for (int r = 0; r < n; ++r)
+                        for (int s = 0; s < n; ++s)
+                            eri[((p * nn + q) * nn + r) * nn + s] = basis.integrals.two_electron(p, q, r, s);
+            rethrow(detci_gpu_set_integrals(h_, basis.integrals.core_energy(), h1.data(), eri.data()), h_);
+            rethrow(detci_gpu_build_basis(h_), h_);
+            std::uint64_t nb = 0;
+            rethrow(detci_gpu_local_rows(h_, &row_begin_, &row_end_, &nb), h_);
+            local_dim_ = (row_end_ - row_begin_) * nb;
+        } catch (...) {
+            detci_gpu_destroy(h_);
+            throw;
+        }
+    }
+    DeviceBasis(const DeviceBasis&) = delete;
+    DeviceBasis& operator=(const DeviceBasis&) = delete;
+    ~DeviceBasis() { detci_gpu_destroy(h_); }
+
+    detci_gpu_handle* handle() const { return h_; }
+    std::size_t local_dimension() const { return local_dim_; }
+
+private:
+    detci_gpu_handle* h_ = nullptr;
+    std::uint64_t row_begin_ = 0, row_end_ = 0;
+    std::size_t local_dim_ = 0;
+};
+
+inline std::unique_ptr<DeviceBasis> build_basis_gpu(const Basis& basis, const DeviceOptions& o = {}) {
+    return std::make_unique<DeviceBasis>(basis, o);
+}
+
+inline void matvec(const DeviceBasis& db, std::span<const double> x, std::span<double> y,
+                   MatvecTimings* timings = nullptr) {
+    if (x.size() != db.local_dimension() || y.size() != db.local_dimension())
+        throw InputError("matvec: vector length " + std::to_string(x.size()) +
+                         " does not match basis dimension " + std::to_string(db.local_dimension()));
+    detci_gpu_timings t{};
+    rethrow(detci_gpu_sigma(db.handle(), x.data(), y.data(), timings ? &t : nullptr), db.handle());
+    if (timings) {
+        timings->alpha_seconds = t.alpha_seconds;
+        timings->beta_seconds = t.beta_seconds;
+        timings->mixed_seconds = t.mixed_seconds;
+        timings->combine_seconds = t.combine_seconds;
+    }
+}
+
+inline LinearOperator linear_operator(const DeviceBasis& db) {
+    return [&db](std::span<const double> x, std::span<double> y) { matvec(db, x, y); };
+}
+
+inline DavidsonResult davidson_solve(const DeviceBasis& db, const DavidsonOptions& o = {}) {
+    if (!o.initial_guess.empty() && o.initial_guess.size() != db.local_dimension())
+        throw InputError("davidson_solve: initial guess length mismatch");
+    detci_dav_opts opts{o.tol, o.max_iter, o.max_subspace,
+                        o.initial_guess.empty() ? nullptr : o.initial_guess.data()};
+    std::vector<detci_dav_iter> trace(static_cast<std::size_t>(o.max_iter > 0 ? o.max_iter : 1));
+    DavidsonResult r;
+    r.eigenvector.resize(db.local_dimension());
+    detci_dav_result res{};
+    res.eigenvector = r.eigenvector.data();
+    res.trace = trace.data();
+    res.trace_cap = static_cast<int>(trace.size());
+    rethrow(detci_gpu_davidson(db.handle(), &opts, &res, nullptr, nullptr), db.handle());
+    r.status = res.status == 0 ? SolveStatus::Converged
+                               : (res.status == 1 ? SolveStatus::MaxIterationsReached : SolveStatus::Stagnated);
+    r.converged = res.converged != 0;
+    r.energy = res.energy;
+    for (int i = 0; i < res.iterations; ++i) {
+        IterationStats s;
+        s.ritz_value = trace[i].ritz_value;
+        s.residual_norm = trace[i].residual_norm;
+        s.matvec_seconds = trace[i].matvec_seconds;
+        s.orthogonalization_seconds = trace[i].orthogonalization_seconds;
+        s.subspace_solve_seconds = trace[i].subspace_solve_seconds;
+        s.max_gram_deviation = trace[i].max_gram_deviation;
+        s.restarted = trace[i].restarted != 0;
+        r.trace.iterations.push_back(s);
+    }
+    return r;
+}
+
+} // namespace detci::gpu
