@@ -312,7 +312,9 @@ void build_mixed_sell(Handle& h) {
     const uint32_t nb = static_cast<uint32_t>(b.n);
     const int n = h.norbs;
     const uint32_t nn = static_cast<uint32_t>(n * n);
-    const uint32_t max_seg = 12288;
+    // two stage buffers of [+-W | C segment] must fit in 220 KB of smem
+    const uint32_t wdbl = (2 * nn + 1) & ~1u;
+    const uint32_t max_seg = std::min<uint32_t>(16000, (220u * 1024 / 8 / 2 - wdbl) & ~1u);
     h.nseg = (nb + max_seg - 1) / max_seg;
     if (h.nseg > 16) fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: more than 16 column segments");
     h.seg_cols = (nb + h.nseg - 1) / h.nseg;
@@ -351,6 +353,7 @@ void build_mixed_sell(Handle& h) {
     #pragma omp parallel for schedule(dynamic, 4)
     for (int64_t sl = 0; sl < static_cast<int64_t>(nslices); ++sl) {
         std::vector<std::pair<uint32_t, uint32_t>> lanes[kWarp];  // (jb_local, w_index)
+        uint64_t rng = 0x9e3779b97f4a7c15ull ^ static_cast<uint64_t>(sl);  // deterministic per slice
         for (uint32_t g = 0; g < nseg; ++g) {
             for (int l = 0; l < kWarp; ++l) {
                 lanes[l].clear();
@@ -369,30 +372,57 @@ void build_mixed_sell(Handle& h) {
             for (uint32_t k = 0; k < L; ++k) {
                 for (int half = 0; half < 2; ++half) {
                     int64_t used_w[16], used_c[16];
-                    for (int i = 0; i < 16; ++i) used_w[i] = used_c[i] = -1;
                     auto cost = [&](uint32_t jbl, uint32_t wi) {
                         const int64_t uw = used_w[wi % 16], uc = used_c[jbl % 16];
                         return (uw >= 0 && uw != wi) + (uc >= 0 && uc != jbl);
                     };
+                    // greedy first-fit over the 16 lanes, best of a few lane orders
+                    int order[16], best_order[16], best_total = 1 << 30;
+                    size_t pick[16], best_pick[16];
+                    for (int i = 0; i < 16; ++i) order[i] = half * 16 + i;
+                    for (int attempt = 0; attempt < 8 && best_total > 0; ++attempt) {
+                        if (attempt > 0)
+                            for (int i = 15; i > 0; --i) {
+                                rng = rng * 6364136223846793005ull + 1442695040888963407ull;
+                                std::swap(order[i], order[(rng >> 33) % (i + 1)]);
+                            }
+                        for (int i = 0; i < 16; ++i) used_w[i] = used_c[i] = -1;
+                        int total = 0;
+                        for (int oi = 0; oi < 16; ++oi) {
+                            const auto& r = lanes[order[oi]];
+                            if (r.empty()) continue;
+                            size_t best = 0;
+                            int best_cost = 3;
+                            for (size_t i = 0; i < r.size(); ++i) {
+                                const int c = cost(r[i].first, r[i].second);
+                                if (c < best_cost) {
+                                    best_cost = c;
+                                    best = i;
+                                    if (c == 0) break;
+                                }
+                            }
+                            pick[oi] = best;
+                            total += best_cost;
+                            if (used_w[r[best].second % 16] < 0) used_w[r[best].second % 16] = r[best].second;
+                            if (used_c[r[best].first % 16] < 0) used_c[r[best].first % 16] = r[best].first;
+                        }
+                        if (total < best_total) {
+                            best_total = total;
+                            std::copy(order, order + 16, best_order);
+                            std::copy(pick, pick + 16, best_pick);
+                        }
+                    }
+                    for (int i = 0; i < 16; ++i) used_w[i] = used_c[i] = -1;
                     int pads[16], npad = 0;
-                    for (int l = half * 16; l < half * 16 + 16; ++l) {
+                    for (int oi = 0; oi < 16; ++oi) {
+                        const int l = best_order[oi];
                         auto& r = lanes[l];
                         if (r.empty()) {
                             pads[npad++] = l;
                             continue;
                         }
-                        size_t best = 0;
-                        int best_cost = 3;
-                        for (size_t i = 0; i < r.size(); ++i) {
-                            const int c = cost(r[i].first, r[i].second);
-                            if (c < best_cost) {
-                                best_cost = c;
-                                best = i;
-                                if (c == 0) break;
-                            }
-                        }
-                        const auto e = r[best];
-                        r[best] = r.back();
+                        const auto e = r[best_pick[oi]];
+                        r[best_pick[oi]] = r.back();
                         r.pop_back();
                         if (used_w[e.second % 16] < 0) used_w[e.second % 16] = e.second;
                         if (used_c[e.first % 16] < 0) used_c[e.first % 16] = e.first;

@@ -195,8 +195,8 @@ k_samespin(const SameSpinArgs a, uint32_t chunk0) {
 // (one coalesced 4 B entry per element) gathering W[cd] and C[ja, jb] from
 // smem.  The ib-dependent alpha sign is applied once per (ja, ib).
 // ---------------------------------------------------------------------------
-constexpr int kMxBlock = 256;
-constexpr int kMxR = 8;
+constexpr int kMxBlock = 1024;   // one CTA per SM, 32 warps
+constexpr int kMxR = 2;          // beta slots per thread -> 2048 slots per CTA
 
 struct MixedArgs {
     const double* C;
@@ -223,17 +223,19 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
-__global__ void __launch_bounds__(kMxBlock, 2)
+// Stage = (alpha single ja, column segment g).  Two stage buffers, each
+// [ +W | -W | C[ja, segment] ]; the next stage's row segment streams in with
+// cp.async (and its W is built) while the current one is consumed.
+__global__ void __launch_bounds__(kMxBlock, 1)
 k_mixed(const MixedArgs a) {
     extern __shared__ double smem[];
     const int nn = a.norbs * a.norbs;
-    double* W2 = smem;                                  // [+W | -W], 2*nn doubles
-    const uint32_t crow_dbl = static_cast<uint32_t>((2 * nn + 1) & ~1);
-    double* crow = smem + crow_dbl;
-    const char* wbase = reinterpret_cast<const char*>(smem);
-    const char* cbase = reinterpret_cast<const char*>(crow);
+    const uint32_t wdbl = static_cast<uint32_t>((2 * nn + 1) & ~1);
+    const uint32_t stage_dbl = wdbl + ((a.seg_cols + 1) & ~1u);
 
     const uint32_t r = blockIdx.x / a.nparts;
     const uint32_t part = blockIdx.x % a.nparts;
@@ -244,13 +246,14 @@ k_mixed(const MixedArgs a) {
 
     uint64_t B[kMxR];
     uint32_t slice[kMxR];
-    double sig[kMxR];
+    double sig[kMxR], acc[kMxR];
 #pragma unroll
     for (int q = 0; q < kMxR; ++q) {
         const uint32_t slot = part * (kMxBlock * kMxR) + q * kMxBlock + tid;
         B[q] = a.beta[a.perm[min(slot, a.nb - 1)]];
         slice[q] = slot / kWarp;
         sig[q] = 0.0;
+        acc[q] = 0.0;
     }
 
     const uint64_t o = a.sa_off[ia];
@@ -258,77 +261,92 @@ k_mixed(const MixedArgs a) {
     const uint32_t* f = a.sa_flat + o;
     const uint32_t kb = a.j0 == 0 ? 0 : lower_bound_u32(f, n, a.j0);
     const uint32_t ke = lower_bound_u32(f, n, a.j1);
+    const uint32_t nstages = (ke - kb) * a.nseg;
 
-#pragma unroll 1
-    for (uint32_t k = kb; k < ke; ++k) {
+    // issue stage i into buffer i & 1: C row segment (async) + +-W (threads)
+    auto issue = [&](uint32_t i) {
+        double* buf = smem + (i & 1) * stage_dbl;
+        const uint32_t k = kb + i / a.nseg, g = i % a.nseg;
         const uint32_t ja = f[k];
+        const double* src = a.C + static_cast<size_t>(ja - a.c_row0) * a.ldc + g * a.seg_cols;
+        const uint32_t segw = min(a.seg_cols, a.nb - g * a.seg_cols);
+        double* crow = buf + wdbl;
+        for (uint32_t c = tid; c < segw; c += kMxBlock) cp_async8(crow + c, src + c);
+        cp_async_commit();
         const uint64_t Ak = a.alpha[ja];
         const int pa = __ffsll(static_cast<long long>(A & ~Ak)) - 1;
         const int qa = __ffsll(static_cast<long long>(Ak & ~A)) - 1;
-        const double* src = a.C + static_cast<size_t>(ja - a.c_row0) * a.ldc;
+        const double* erow = a.eri + static_cast<size_t>(pa * a.norbs + qa) * nn;
+        for (int cd = tid; cd < nn; cd += kMxBlock) {
+            const int c = cd / a.norbs, d = cd - c * a.norbs;
+            double v = 0.0;
+            if (c != d) {
+                v = erow[cd];
+                if (__popcll(Ak & spectator_mask(1, c, d)) & 1) v = -v;
+            }
+            buf[cd] = v;
+            buf[nn + cd] = -v;
+        }
+    };
 
-        double acc[kMxR];
-#pragma unroll
-        for (int q = 0; q < kMxR; ++q) acc[q] = 0.0;
-
+    if (nstages > 0) issue(0);
 #pragma unroll 1
-        for (uint32_t g = 0; g < a.nseg; ++g) {
-            const uint32_t cbase_col = g * a.seg_cols;
-            const uint32_t segw = min(a.seg_cols, a.nb - cbase_col);
-            __syncthreads();  // previous users of W2 / crow are done
-            for (uint32_t c = tid; c < segw; c += kMxBlock) cp_async8(crow + c, src + cbase_col + c);
-            if (g == 0) {
-                const double* erow = a.eri + static_cast<size_t>(pa * a.norbs + qa) * nn;
-                for (int cd = tid; cd < nn; cd += kMxBlock) {
-                    const int c = cd / a.norbs, d = cd - c * a.norbs;
-                    double v = 0.0;
-                    if (c != d) {
-                        v = erow[cd];
-                        if (__popcll(Ak & spectator_mask(1, c, d)) & 1) v = -v;
-                    }
-                    W2[cd] = v;
-                    W2[nn + cd] = -v;
+    for (uint32_t i = 0; i < nstages; ++i) {
+        if (i + 1 < nstages) {
+            issue(i + 1);          // buffer (i+1)&1 was released by the barrier ending stage i-1
+            cp_async_wait_prev();  // stage i's row has landed
+        } else {
+            cp_async_wait_all();
+        }
+        __syncthreads();
+        const char* wbase = reinterpret_cast<const char*>(smem + (i & 1) * stage_dbl);
+        const char* cbase = reinterpret_cast<const char*>(smem + (i & 1) * stage_dbl + wdbl);
+        const uint32_t g = i % a.nseg;
+#pragma unroll
+        for (int q = 0; q < kMxR; ++q) {
+            if (slice[q] >= a.nslices) continue;
+            const uint32_t L = a.sell_len[slice[q] * a.nseg + g];
+            const uint32_t* ent = a.sell + a.sell_off[slice[q] * a.nseg + g] + lane;
+            double s0 = 0.0, s1 = 0.0;
+            uint32_t t = 0;
+#pragma unroll 1
+            for (; t + 8 <= L; t += 8) {
+                uint32_t e[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) e[u] = __ldg(ent + static_cast<size_t>(t + u) * kWarp);
+#pragma unroll
+                for (int u = 0; u < 8; u += 2) {
+                    const double w0 = *reinterpret_cast<const double*>(wbase + ((e[u] >> 17) << 3));
+                    const double c0 = *reinterpret_cast<const double*>(cbase + (e[u] & 0x1ffffu));
+                    const double w1 = *reinterpret_cast<const double*>(wbase + ((e[u + 1] >> 17) << 3));
+                    const double c1 = *reinterpret_cast<const double*>(cbase + (e[u + 1] & 0x1ffffu));
+                    s0 = fma(w0, c0, s0);
+                    s1 = fma(w1, c1, s1);
                 }
             }
-            cp_async_wait_all();
-            __syncthreads();
+#pragma unroll 1
+            for (; t < L; ++t) {
+                const uint32_t e0 = __ldg(ent + static_cast<size_t>(t) * kWarp);
+                const double w0 = *reinterpret_cast<const double*>(wbase + ((e0 >> 17) << 3));
+                const double c0 = *reinterpret_cast<const double*>(cbase + (e0 & 0x1ffffu));
+                s0 = fma(w0, c0, s0);
+            }
+            acc[q] += s0 + s1;
+        }
+        if (g + 1 == a.nseg) {  // last segment of this ja: apply the alpha sign
+            const uint32_t ja = f[kb + i / a.nseg];
+            const uint64_t Ak = a.alpha[ja];
+            const int pa = __ffsll(static_cast<long long>(A & ~Ak)) - 1;
+            const int qa = __ffsll(static_cast<long long>(Ak & ~A)) - 1;
+            const int sA = __popcll(A & open_mask(pa, qa)) & 1;
+            const uint64_t ma = spectator_mask(0, pa, qa);
 #pragma unroll
             for (int q = 0; q < kMxR; ++q) {
-                if (slice[q] >= a.nslices) continue;
-                const uint32_t L = a.sell_len[slice[q] * a.nseg + g];
-                const uint32_t* ent = a.sell + a.sell_off[slice[q] * a.nseg + g] + lane;
-                double s0 = 0.0, s1 = 0.0;
-                uint32_t t = 0;
-#pragma unroll 1
-                for (; t + 8 <= L; t += 8) {
-                    uint32_t e[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) e[u] = __ldg(ent + static_cast<size_t>(t + u) * kWarp);
-#pragma unroll
-                    for (int u = 0; u < 8; u += 2) {
-                        const double w0 = *reinterpret_cast<const double*>(wbase + ((e[u] >> 17) << 3));
-                        const double c0 = *reinterpret_cast<const double*>(cbase + (e[u] & 0x1ffffu));
-                        const double w1 = *reinterpret_cast<const double*>(wbase + ((e[u + 1] >> 17) << 3));
-                        const double c1 = *reinterpret_cast<const double*>(cbase + (e[u + 1] & 0x1ffffu));
-                        s0 = fma(w0, c0, s0);
-                        s1 = fma(w1, c1, s1);
-                    }
-                }
-#pragma unroll 1
-                for (; t < L; ++t) {
-                    const uint32_t e0 = __ldg(ent + static_cast<size_t>(t) * kWarp);
-                    const double w0 = *reinterpret_cast<const double*>(wbase + ((e0 >> 17) << 3));
-                    const double c0 = *reinterpret_cast<const double*>(cbase + (e0 & 0x1ffffu));
-                    s0 = fma(w0, c0, s0);
-                }
-                acc[q] += s0 + s1;
+                sig[q] += flip_sign(acc[q], static_cast<uint32_t>(sA ^ (__popcll(B[q] & ma) & 1)));
+                acc[q] = 0.0;
             }
         }
-        const int sA = __popcll(A & open_mask(pa, qa)) & 1;
-        const uint64_t ma = spectator_mask(0, pa, qa);
-#pragma unroll
-        for (int q = 0; q < kMxR; ++q)
-            sig[q] += flip_sign(acc[q], static_cast<uint32_t>(sA ^ (__popcll(B[q] & ma) & 1)));
+        __syncthreads();  // buffer i&1 free for stage i+2
     }
 
 #pragma unroll
@@ -465,7 +483,7 @@ void launch_samespin(const SameSpinArgs& s, cudaStream_t st) {
 
 size_t mixed_smem(const Handle& h) {
     const size_t nn = static_cast<size_t>(h.norbs) * h.norbs;
-    return (((2 * nn + 1) & ~size_t{1}) + h.seg_cols) * sizeof(double);
+    return 2 * (((2 * nn + 1) & ~size_t{1}) + ((h.seg_cols + 1) & ~size_t{1})) * sizeof(double);
 }
 
 void launch_mixed(const Handle& h, const double* Cb, uint32_t b0, uint32_t b1, double* y_loc,
