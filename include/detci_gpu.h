@@ -110,6 +110,28 @@ typedef struct {
     int trace_cap;
 } detci_dav_result;
 
+/* Multi-root block Davidson (BASELINE config C5).  A
+ * capability beyond the reference's single-root davidson_solve
+ * (davidson.hpp:83-86), built from the same rules. */
+typedef struct {
+    double tol;         /* max over roots of the residual 2-norm */
+    int max_iter;
+    int max_subspace;   /* >= 2 * nroots */
+    int nroots;
+} detci_dav_block_opts;
+
+typedef struct {
+    int status;             /* as detci_dav_result */
+    int converged;
+    int iterations;
+    double seconds;
+    double* energies;       /* nroots, ascending, or NULL */
+    double* residuals;      /* nroots, or NULL */
+    double* eigenvectors;   /* nroots * local length (root-major), or NULL */
+    detci_dav_iter* trace;  /* ritz_value = lowest root, residual_norm = max over roots */
+    int trace_cap;
+} detci_dav_block_result;
+
 /* Called once per Davidson iteration (after the trace entry is final). */
 typedef void (*detci_trace_cb)(const detci_dav_iter* it, int iteration, void* user);
 
@@ -193,6 +215,13 @@ int detci_gpu_copy_vector(detci_gpu_handle* h, double* dst, const double* src, i
 /* ---- Davidson -------------------------------------------------------------- */
 int detci_gpu_davidson(detci_gpu_handle* h, const detci_dav_opts* opts, detci_dav_result* res,
                        detci_trace_cb cb, void* user);
+
+int detci_gpu_davidson_roots(detci_gpu_handle* h, const detci_dav_block_opts* opts,
+                             detci_dav_block_result* res);
+
+/* m vectors through one blocked sigma: dx[i], dy[i] device pointers of the
+ * local length (the multi-root Davidson's new block). */
+int detci_gpu_sigma_block(detci_gpu_handle* h, const double* const* dx, double* const* dy, int m);
 
 /* davidson.hpp:67-81 helpers on host arrays of length n (single GPU). */
 int detci_gpu_inner_product(detci_gpu_handle* h, const double* x, const double* y, uint64_t n,

@@ -81,6 +81,24 @@ class DavResult(C.Structure):
     ]
 
 
+class DavBlockOpts(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_iter", C.c_int), ("max_subspace", C.c_int), ("nroots", C.c_int)]
+
+
+class DavBlockResult(C.Structure):
+    _fields_ = [
+        ("status", C.c_int),
+        ("converged", C.c_int),
+        ("iterations", C.c_int),
+        ("seconds", C.c_double),
+        ("energies", dp),
+        ("residuals", dp),
+        ("eigenvectors", dp),
+        ("trace", C.POINTER(DavIter)),
+        ("trace_cap", C.c_int),
+    ]
+
+
 TRACE_CB = C.CFUNCTYPE(None, C.POINTER(DavIter), C.c_int, vp)
 
 # name -> (restype, argtypes); mirrors include/detci_gpu.h exactly
@@ -107,6 +125,8 @@ SIGNATURES = {
     "detci_gpu_free_vector": (C.c_int, [vp, vp]),
     "detci_gpu_copy_vector": (C.c_int, [vp, vp, vp, C.c_int]),
     "detci_gpu_davidson": (C.c_int, [vp, C.POINTER(DavOpts), C.POINTER(DavResult), TRACE_CB, vp]),
+    "detci_gpu_davidson_roots": (C.c_int, [vp, C.POINTER(DavBlockOpts), C.POINTER(DavBlockResult)]),
+    "detci_gpu_sigma_block": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.c_int]),
     "detci_gpu_inner_product": (C.c_int, [vp, dp, dp, C.c_uint64, dp]),
     "detci_gpu_orthonormalize": (C.c_int, [vp, dp, C.c_int, C.c_uint64, dp, dp, C.POINTER(C.c_int)]),
     "detci_gpu_precondition": (C.c_int, [vp, dp, dp, C.c_uint64, C.c_double, dp]),

@@ -307,19 +307,19 @@ void build_pair_tables(Handle& h, int c) {
 //    C[ja, jb]); padding entries point at a zero of W and reuse a
 //    C address already read in that step (broadcast).  Simulated on C2 this
 //    cuts shared-memory wavefronts per element step from 9.2 to 5.6.
-void build_mixed_sell(Handle& h) {
+void build_mixed_sell(Handle& h, SellTable& st, int M) {
     ChannelTables& b = h.ch[1];
     const uint32_t nb = static_cast<uint32_t>(b.n);
     const int n = h.norbs;
     const uint32_t nn = static_cast<uint32_t>(n * n);
-    // two stage buffers of [+-W | C segment] must fit in 220 KB of smem
+    // two stage buffers of [+-W | M C-row segments] must fit in 220 KB of smem
     const uint32_t wdbl = (2 * nn + 1) & ~1u;
-    const uint32_t max_seg = std::min<uint32_t>(16000, (220u * 1024 / 8 / 2 - wdbl) & ~1u);
-    h.nseg = (nb + max_seg - 1) / max_seg;
-    if (h.nseg > 16) fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: more than 16 column segments");
-    h.seg_cols = (nb + h.nseg - 1) / h.nseg;
+    const uint32_t max_seg = std::min<uint32_t>(16000, ((220u * 1024 / 8 / 2 - wdbl) / M) & ~1u);
+    st.nseg = (nb + max_seg - 1) / max_seg;
+    if (st.nseg > 16) fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: more than 16 column segments");
+    st.seg_cols = (nb + st.nseg - 1) / st.nseg;
     h.nslices = (nb + kWarp - 1) / kWarp;
-    const uint32_t nseg = h.nseg, seg_cols = h.seg_cols, nslices = h.nslices;
+    const uint32_t nseg = st.nseg, seg_cols = st.seg_cols, nslices = h.nslices;
 
     std::vector<uint32_t> flat(std::max<uint64_t>(b.nflat[0], 1));
     std::vector<uint64_t> off(nb);
@@ -451,11 +451,12 @@ void build_mixed_sell(Handle& h) {
             }
         }
     }
-    upload(h.sell_perm, perm, h.stream);
-    upload(h.sell_len, slen, h.stream);
-    upload(h.sell_off, soff, h.stream);
-    upload(h.sell, sell, h.stream);
+    if (!h.sell_perm.p) upload(h.sell_perm, perm, h.stream);
+    upload(st.len, slen, h.stream);
+    upload(st.off, soff, h.stream);
+    upload(st.sell, sell, h.stream);
     CUDA_CHECK(cudaStreamSynchronize(h.stream));
+    st.built = true;
 }
 
 void build_partition(Handle& h) {
@@ -534,6 +535,13 @@ size_t estimate_bytes(const Handle& h) {
 
 } // namespace
 
+const SellTable& mixed_table(Handle& h, int M) {
+    const int idx = M == 1 ? 0 : (M == 2 ? 1 : 2);
+    SellTable& t = h.sell_m[idx];
+    if (!t.built) build_mixed_sell(h, t, M);
+    return t;
+}
+
 void release_basis(Handle& h) {
     for (auto& t : h.ch) {
         for (int k = 0; k < 2; ++k) {
@@ -546,9 +554,12 @@ void release_basis(Handle& h) {
         t.pab.reset();
         t.J.reset();
     }
-    h.sell.reset();
-    h.sell_off.reset();
-    h.sell_len.reset();
+    for (auto& t : h.sell_m) {
+        t.sell.reset();
+        t.off.reset();
+        t.len.reset();
+        t.built = false;
+    }
     h.sell_perm.reset();
     h.diag.reset();
     h.ct.reset();
@@ -577,7 +588,7 @@ void build_device_basis(Handle& h) {
                                        " bytes, budget is " + std::to_string(budget) + " bytes");
 
     for (int c = 0; c < 2; ++c) build_pair_tables(h, c);
-    build_mixed_sell(h);
+    build_mixed_sell(h, h.sell_m[0], 1);
     build_diag(h);
     const size_t scratch = static_cast<size_t>(h.max_blk) * h.nb();
     h.ct.alloc(std::max<size_t>(scratch, 1));

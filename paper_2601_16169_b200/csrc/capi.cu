@@ -410,6 +410,23 @@ int detci_gpu_davidson(detci_gpu_handle* hh, const detci_dav_opts* opts, detci_d
     });
 }
 
+int detci_gpu_davidson_roots(detci_gpu_handle* hh, const detci_dav_block_opts* opts,
+                             detci_dav_block_result* res) {
+    return guarded(hh, [&] {
+        require(hh && opts && res, DETCI_GPU_E_INPUT, "davidson_roots: null argument");
+        activate(hh->h);
+        davidson_roots_device(hh->h, *opts, res);
+    });
+}
+
+int detci_gpu_sigma_block(detci_gpu_handle* hh, const double* const* dx, double* const* dy, int m) {
+    return guarded(hh, [&] {
+        require(hh && dx && dy && m >= 1, DETCI_GPU_E_INPUT, "sigma_block: bad argument");
+        activate(hh->h);
+        sigma_block(hh->h, dx, dy, m);
+    });
+}
+
 int detci_gpu_inner_product(detci_gpu_handle* hh, const double* x, const double* y, uint64_t n,
                             double* out) {
     return guarded(hh, [&] {

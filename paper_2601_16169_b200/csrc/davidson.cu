@@ -258,9 +258,12 @@ double device_dot(Handle& h, const double* x, const double* y, uint64_t n) {
     return v;
 }
 
-// Smallest eigenpair of the k x k symmetric matrix given by its lower
-// triangle lower[i * ld + j], j <= i.  Cyclic Jacobi to machine precision.
-double smallest_eigenpair(const std::vector<double>& lower, int ld, int k, std::vector<double>& vec) {
+// All eigenpairs of the k x k symmetric matrix given by its lower triangle
+// lower[i * ld + j], j <= i (Eigen's SelfAdjointEigenSolver reads only that
+// triangle, davidson.cpp:22-30).  Cyclic Jacobi to machine precision;
+// eigenvalues ascending, vecs[m * k + i] = component i of eigenvector m.
+void jacobi_eigen(const std::vector<double>& lower, int ld, int k, std::vector<double>& evals,
+                  std::vector<double>& vecs) {
     std::vector<double> a(static_cast<size_t>(k) * k), v(static_cast<size_t>(k) * k, 0.0);
     for (int i = 0; i < k; ++i) {
         for (int j = 0; j < k; ++j) a[i * k + j] = i >= j ? lower[i * ld + j] : lower[j * ld + i];
@@ -298,12 +301,22 @@ double smallest_eigenpair(const std::vector<double>& lower, int ld, int k, std::
                 }
             }
     }
-    int m = 0;
-    for (int i = 1; i < k; ++i)
-        if (a[i * k + i] < a[m * k + m]) m = i;
-    vec.assign(k, 0.0);
-    for (int i = 0; i < k; ++i) vec[i] = v[i * k + m];
-    return a[m * k + m];
+    std::vector<int> order(k);
+    for (int i = 0; i < k; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return a[x * k + x] < a[y * k + y]; });
+    evals.resize(k);
+    vecs.assign(static_cast<size_t>(k) * k, 0.0);
+    for (int m = 0; m < k; ++m) {
+        evals[m] = a[order[m] * k + order[m]];
+        for (int i = 0; i < k; ++i) vecs[static_cast<size_t>(m) * k + i] = v[i * k + order[m]];
+    }
+}
+
+double smallest_eigenpair(const std::vector<double>& lower, int ld, int k, std::vector<double>& vec) {
+    std::vector<double> evals, vecs;
+    jacobi_eigen(lower, ld, k, evals, vecs);
+    vec.assign(vecs.begin(), vecs.begin() + k);
+    return evals[0];
 }
 
 void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* res,
@@ -518,6 +531,233 @@ void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* re
         CUDA_LAUNCH_CHECK();
         CUDA_CHECK(cudaMemcpyAsync(res->eigenvector, ritz, n * sizeof(double), cudaMemcpyDeviceToHost,
                                    h.stream));
+    }
+    if (res->trace)
+        for (int i = 0; i < std::min(res->trace_cap, iters); ++i) res->trace[i] = trace[i];
+    CUDA_CHECK(cudaStreamSynchronize(h.stream));
+    res->seconds = seconds_since(wall0);
+}
+
+
+// ---------------------------------------------------------------------------
+// Multi-root block Davidson (Davidson-Liu): SURVEY.md 8(f) rank 1, BASELINE
+// config C5.  A capability beyond the reference (single root,
+// davidson.hpp:83-86) built from the same rules: guesses are unit vectors at
+// the nroots lowest diagonal entries (lowest index on ties), lower-triangle
+// projected fill, Jacobi on the host, per-root residual and the clamped
+// diagonal preconditioner, 2-pass MGS against the subspace (and the
+// corrections added before it in the same iteration) with the 1e-10
+// dependence threshold, and collapse to the nroots Ritz pairs when the next
+// block would exceed max_subspace.  New vectors of one iteration go through
+// one blocked sigma call.
+// ---------------------------------------------------------------------------
+void davidson_roots_device(Handle& h, const detci_dav_block_opts& opts, detci_dav_block_result* res) {
+    if (!h.built) fail(DETCI_GPU_E_INPUT, "davidson_solve: basis not built");
+    const uint64_t n = h.local_len();
+    const int m = opts.nroots;
+    if (n == 0) fail(DETCI_GPU_E_INPUT, "davidson_solve: empty diagonal");
+    if (m < 1) fail(DETCI_GPU_E_CONFIG, "davidson_roots: nroots must be positive");
+    if (!(opts.tol > 0.0)) fail(DETCI_GPU_E_CONFIG, "davidson_solve: tol must be positive");
+    if (opts.max_iter < 1) fail(DETCI_GPU_E_CONFIG, "davidson_solve: max_iter must be positive");
+    if (opts.max_subspace < 2 * m) fail(DETCI_GPU_E_CONFIG, "davidson_roots: max_subspace must be >= 2*nroots");
+    if (opts.max_subspace > kMaxVec) fail(DETCI_GPU_E_UNSUPPORTED, "davidson_solve: max_subspace above 64");
+    const uint64_t dim_global = static_cast<uint64_t>(h.na()) * h.nb();
+    if (static_cast<uint64_t>(m) > dim_global) fail(DETCI_GPU_E_INPUT, "davidson_roots: nroots exceeds the dimension");
+    ensure_red(h);
+    const int ms = opts.max_subspace;
+    const auto wall0 = std::chrono::steady_clock::now();
+
+    size_t free_b = 0, total_b = 0;
+    CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+    const size_t nvec = 2 * static_cast<size_t>(ms) + 3 * static_cast<size_t>(m);
+    const size_t need = nvec * n * sizeof(double);
+    const uint64_t budget = std::min<uint64_t>(h.budget ? h.budget : free_b, free_b);
+    if (need > budget)
+        fail(DETCI_GPU_E_CAPACITY, "davidson vectors require " + std::to_string(need) + " bytes, budget is " +
+                                       std::to_string(budget) + " bytes");
+    DevBuf<double> store;
+    store.alloc(nvec * n);
+    auto V = [&](int j) { return store.p + static_cast<size_t>(j) * n; };
+    auto Wv = [&](int j) { return store.p + static_cast<size_t>(ms + j) * n; };
+    auto RZ = [&](int r) { return store.p + static_cast<size_t>(2 * ms + r) * n; };
+    auto IM = [&](int r) { return store.p + static_cast<size_t>(2 * ms + m + r) * n; };
+    auto CR = [&](int r) { return store.p + static_cast<size_t>(2 * ms + 2 * m + r) * n; };
+
+    // guesses: the m lowest diagonal entries (lowest index first on ties)
+    {
+        std::vector<double> d(n);
+        CUDA_CHECK(cudaMemcpy(d.data(), h.diag.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+        std::vector<uint64_t> idx(n);
+        for (uint64_t i = 0; i < n; ++i) idx[i] = i;
+        const uint64_t keep = std::min<uint64_t>(n, static_cast<uint64_t>(m));
+        std::partial_sort(idx.begin(), idx.begin() + keep, idx.end(), [&](uint64_t x, uint64_t y) {
+            return d[x] < d[y] || (d[x] == d[y] && x < y);
+        });
+        std::vector<double> cand(2 * m, INFINITY);  // (value, global index) of local best
+        for (uint64_t r = 0; r < keep; ++r) {
+            cand[2 * r] = d[idx[r]];
+            cand[2 * r + 1] = static_cast<double>(idx[r] + h.a0 * h.nb());
+        }
+        std::vector<double> all(2 * static_cast<size_t>(m) * h.world, 0.0);
+        std::copy(cand.begin(), cand.end(), all.begin() + 2 * static_cast<size_t>(m) * h.rank);
+        allreduce_sum(h, all.data(), static_cast<int>(all.size()));
+        std::vector<std::pair<double, double>> pool;
+        for (size_t i = 0; i < all.size(); i += 2)
+            if (std::isfinite(all[i])) pool.emplace_back(all[i], all[i + 1]);
+        std::sort(pool.begin(), pool.end());
+        const uint64_t lo = h.a0 * h.nb();
+        for (int r = 0; r < m; ++r) {
+            const uint64_t gi = static_cast<uint64_t>(pool[r].second);
+            k_set_unit<<<kRedBlocks, kRedThreads, 0, h.stream>>>(V(r), n, gi >= lo && gi < lo + n ? gi - lo : ~0ull);
+            CUDA_LAUNCH_CHECK();
+        }
+    }
+
+    std::vector<double> proj(static_cast<size_t>(ms) * ms, 0.0), gram(static_cast<size_t>(ms) * ms, 0.0);
+    std::vector<double> evals, evecs, theta(m, 0.0), rnorm(m, 0.0);
+    int k_sub = m, k_img = 0, status = 0, iters = 0;
+    bool restart_pending = false;
+    std::vector<detci_dav_iter> trace;
+
+    auto fill_rows = [&](int from, int to) {  // projected + Gram rows [from, to)
+        for (int i = from; i < to; ++i) {
+            std::vector<const double*> ys(2 * (i + 1));
+            for (int j = 0; j <= i; ++j) {
+                ys[j] = Wv(j);
+                ys[i + 1 + j] = V(j);
+            }
+            std::vector<double> dots(2 * (i + 1));
+            device_dot_many(h, V(i), ys.data(), 2 * (i + 1), n, dots.data());
+            for (int j = 0; j <= i; ++j) {
+                proj[i * ms + j] = dots[j];
+                gram[i * ms + j] = dots[i + 1 + j];
+            }
+        }
+    };
+
+    for (int iter = 0; iter < opts.max_iter; ++iter) {
+        detci_dav_iter st{};
+        st.restarted = restart_pending ? 1 : 0;
+        restart_pending = false;
+        auto t0 = std::chrono::steady_clock::now();
+        if (k_img < k_sub) {  // one blocked sigma for the new vectors
+            std::vector<const double*> xs;
+            std::vector<double*> ys;
+            for (int j = k_img; j < k_sub; ++j) {
+                xs.push_back(V(j));
+                ys.push_back(Wv(j));
+            }
+            sigma_block(h, xs.data(), ys.data(), static_cast<int>(xs.size()));
+            const int first = k_img;
+            k_img = k_sub;
+            st.matvec_seconds = seconds_since(t0);
+            t0 = std::chrono::steady_clock::now();
+            fill_rows(first, k_sub);
+        } else {
+            st.matvec_seconds = seconds_since(t0);
+            t0 = std::chrono::steady_clock::now();
+        }
+        const int k = k_sub;
+        jacobi_eigen(proj, ms, k, evals, evecs);
+        st.subspace_solve_seconds = seconds_since(t0);
+
+        t0 = std::chrono::steady_clock::now();
+        double worst = 0.0;
+        std::vector<double> cnorm(m, 0.0);
+        for (int r = 0; r < m; ++r) {
+            RitzArgs ra{};
+            for (int j = 0; j < k; ++j) {
+                ra.v[j] = V(j);
+                ra.w[j] = Wv(j);
+                ra.c[j] = evecs[static_cast<size_t>(r) * k + j];
+            }
+            ra.k = k;
+            ra.theta = evals[r];
+            k_ritz<<<kRedBlocks, kRedThreads, 0, h.stream>>>(ra, h.diag.p, n, RZ(r), IM(r), CR(r), h.red.p);
+            CUDA_LAUNCH_CHECK();
+            finalize_to(h, 2, 0);
+            double nn2[2];
+            read_slots(h, 0, 2, nn2);
+            theta[r] = evals[r];
+            rnorm[r] = std::sqrt(nn2[0]);
+            cnorm[r] = std::sqrt(nn2[1]);
+            worst = std::max(worst, rnorm[r]);
+        }
+        double gdev = 0.0;
+        for (int i = 0; i < k; ++i)
+            for (int j = 0; j <= i; ++j)
+                gdev = std::max(gdev, std::fabs(gram[i * ms + j] - (i == j ? 1.0 : 0.0)));
+        st.max_gram_deviation = gdev;
+        st.ritz_value = theta[0];
+        st.residual_norm = worst;
+        auto push = [&]() {
+            st.orthogonalization_seconds = seconds_since(t0);
+            trace.push_back(st);
+            ++iters;
+        };
+        const bool converged = worst <= opts.tol;
+        if (converged || iter + 1 == opts.max_iter) {
+            push();
+            status = converged ? 0 : 1;
+            break;
+        }
+        int unconverged = 0;
+        for (int r = 0; r < m; ++r) unconverged += rnorm[r] > opts.tol && cnorm[r] > 0.0;
+        if (k_sub + unconverged > ms) {  // collapse to the m Ritz pairs
+            for (int r = 0; r < m; ++r) {
+                CUDA_CHECK(cudaMemcpyAsync(V(r), RZ(r), n * 8, cudaMemcpyDeviceToDevice, h.stream));
+                CUDA_CHECK(cudaMemcpyAsync(Wv(r), IM(r), n * 8, cudaMemcpyDeviceToDevice, h.stream));
+            }
+            k_sub = k_img = m;
+            fill_rows(0, m);
+            restart_pending = true;
+        }
+        int added = 0;
+        for (int r = 0; r < m; ++r) {
+            if (!(rnorm[r] > opts.tol) || !(cnorm[r] > 0.0)) continue;
+            if (k_sub >= ms) break;
+            double* cand = V(k_sub);
+            const int kk = k_sub;
+            const int steps = 2 * kk;
+            for (int t = 0; t <= steps; ++t) {
+                const double* src = t == 0 ? CR(r) : nullptr;
+                const double* vprev = t == 0 ? nullptr : V((t - 1) % kk);
+                const double* vnext = t == steps ? nullptr : V(t % kk);
+                k_mgs_step<<<kRedBlocks, kRedThreads, 0, h.stream>>>(cand, src, cnorm[r], vprev,
+                                                                      scalar_slot(h, 4 + (t + 1) % 2), vnext, n,
+                                                                      h.red.p);
+                CUDA_LAUNCH_CHECK();
+                finalize_to(h, 1, 4 + t % 2);
+            }
+            double nrm2 = 0.0;
+            read_slots(h, 4 + steps % 2, 1, &nrm2);
+            const double norm = std::sqrt(nrm2);
+            if (!(norm >= 1e-10)) continue;
+            k_scale_div<<<kRedBlocks, kRedThreads, 0, h.stream>>>(cand, n, norm);
+            CUDA_LAUNCH_CHECK();
+            ++k_sub;
+            ++added;
+        }
+        push();
+        if (added == 0) {
+            status = 2;
+            break;
+        }
+    }
+
+    res->status = status;
+    res->converged = status == 0;
+    res->iterations = iters;
+    for (int r = 0; r < m; ++r) {
+        if (res->energies) res->energies[r] = theta[r];
+        if (res->residuals) res->residuals[r] = rnorm[r];
+        if (res->eigenvectors) {
+            const double nrm = std::sqrt(device_dot(h, RZ(r), RZ(r), n));
+            k_scale_div<<<kRedBlocks, kRedThreads, 0, h.stream>>>(RZ(r), n, nrm);
+            CUDA_LAUNCH_CHECK();
+            CUDA_CHECK(cudaMemcpyAsync(res->eigenvectors + static_cast<size_t>(r) * n, RZ(r), n * 8,
+                                       cudaMemcpyDeviceToHost, h.stream));
+        }
     }
     if (res->trace)
         for (int i = 0; i < std::min(res->trace_cap, iters); ++i) res->trace[i] = trace[i];

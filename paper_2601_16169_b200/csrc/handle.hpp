@@ -62,6 +62,14 @@ struct ChannelTables {
     DevBuf<double> J;
 };
 
+struct SellTable {
+    DevBuf<uint32_t> sell;
+    DevBuf<uint64_t> off;              // [slice * nseg + seg]
+    DevBuf<uint32_t> len;              // [slice * nseg + seg]
+    uint32_t seg_cols = 0, nseg = 0;
+    bool built = false;
+};
+
 struct Handle {
     int device = 0;
     int rank = 0;
@@ -79,12 +87,12 @@ struct Handle {
 
     ChannelTables ch[2];
 
-    // mixed term: beta singles in SELL-32, bucketed by jb segment
-    DevBuf<uint32_t> sell;
-    DevBuf<uint64_t> sell_off;         // [slice * nseg + seg]
-    DevBuf<uint32_t> sell_len;         // [slice * nseg + seg]
+    // mixed term: beta singles in SELL-32, bucketed by jb segment; one
+    // segmentation per vector count M in {1, 2, 4} (the staged C rows of M
+    // vectors share the CTA's shared memory), built on first use
+    SellTable sell_m[3];
     DevBuf<uint32_t> sell_perm;        // slot -> beta string (degree-sorted)
-    uint32_t seg_cols = 0, nseg = 1, nslices = 0;
+    uint32_t nslices = 0;
 
     // alpha-block partition: P = world (NCCL) or vblocks (virtual)
     std::vector<uint64_t> blk;
@@ -116,11 +124,15 @@ struct Handle {
 void plan_partition(uint64_t na, uint64_t nb, const uint32_t* sa, const uint32_t* da,
                     const uint32_t* sb, const uint32_t* db, int P, int weighted, uint64_t* blk);
 void build_device_basis(Handle& h);
+const SellTable& mixed_table(Handle& h, int M);   // M in {1, 2, 4}
 void release_basis(Handle& h);
 
 // sigma.cu
 void sigma_device(Handle& h, const double* dx, double* dy, detci_gpu_timings* tm);
 void sigma_enqueue(Handle& h, const double* dx, double* dy);  // no host sync
+// m vectors through one blocked pass (element evaluations shared across
+// vectors where the kernels support it); synchronous.
+void sigma_block(Handle& h, const double* const* dx, double* const* dy, int m);
 
 // davidson.cu
 struct DavidsonOutcome {
@@ -134,5 +146,8 @@ void device_dot_many(Handle& h, const double* x, const double* const* ys, int k,
                      double* out_host);
 void allreduce_sum(Handle& h, double* host_vals, int count);
 double smallest_eigenpair(const std::vector<double>& lower, int ld, int k, std::vector<double>& vec);
+void jacobi_eigen(const std::vector<double>& lower, int ld, int k, std::vector<double>& evals,
+                  std::vector<double>& vecs);
+void davidson_roots_device(Handle& h, const detci_dav_block_opts& opts, detci_dav_block_result* res);
 
 } // namespace detci_gpu

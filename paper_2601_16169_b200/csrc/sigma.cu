@@ -1,5 +1,5 @@
 // sigma = H C over the alpha x beta tensor-product basis (matvec,
-// matvec.cpp:125-228), B200-native.
+// matvec.cpp:125-228), B200-native, for M = 1, 2 or 4 vectors per pass.
 //
 //   y  = diag*C + sum_ja Ha(ia,ja;B_ib) C[ja,ib]              k_samespin on C
 //   yT =          sum_jb Hb(ib,jb;A_ia) C^T[jb,ia]            k_samespin on C^T
@@ -10,7 +10,9 @@
 // so there are no atomics and the result is deterministic.  The beta term
 // runs the alpha kernel on the transposed block, which turns its per-row
 // gathers into coalesced row reads (the transposes cost 32 B/det against
-// ~8 B x thousands of elements per det).
+// ~8 B x thousands of elements per det).  With M vectors, every element's
+// sign/value work (same-spin) and its W gather and SELL entry (mixed) are
+// shared by the M vectors (the multi-root block Davidson's new block).
 //
 // Multi-GPU / virtual blocks: alpha rows are partitioned into P blocks;
 // the alpha and mixed terms need C rows from every block, which rotate
@@ -18,6 +20,7 @@
 // with the compute of the resident block).  The beta term and diagonal are
 // block-local.
 #include <algorithm>
+#include <array>
 #include <vector>
 
 #include "formulas.cuh"
@@ -27,27 +30,33 @@ namespace detci_gpu {
 
 namespace {
 
+constexpr int kMaxM = 4;
+
 // ---------------------------------------------------------------------------
 // Same-spin kernel.  CTA = (output row, column chunk); threads own R columns
 // each (coalesced), loop over the row's helper-list entries staged in smem.
-// Per element: one coalesced 8 B load of C[ja, col], AND+POPC against the
-// spectator string, sign flip, DFMA (+ one coalesced J load for singles).
-// Grid is chunk-major so CTAs in flight share C[:, chunk] in L2.
+// Per element: one coalesced 8 B load of C[ja, col] per vector, AND+POPC
+// against the spectator string, sign flip, DFMA (+ one coalesced J load for
+// singles).  Grid is chunk-major so CTAs in flight share C[:, chunk] in L2.
 // ---------------------------------------------------------------------------
 constexpr int kSSBlock = 128;
-constexpr int kSSR = 4;
 constexpr int kStage = 256;
 
+template <int M>
+struct SSR {
+    static constexpr int value = M == 1 ? 4 : (M == 2 ? 2 : 1);
+};
+
 struct SameSpinArgs {
-    const double* C;        // C row ja at C + (ja - c_row0) * ldc
+    const double* C[kMaxM];   // C row ja of vector v at C[v] + (ja - c_row0) * ldc
     size_t ldc;
     uint32_t c_row0, j0, j1;  // window [j0, j1) of target rows
-    double* Y;              // output row r at Y + r * ldy
+    double* Y[kMaxM];         // output row r at Y[v] + r * ldy
     size_t ldy;
-    uint32_t row0, nrows;   // list rows [row0, row0 + nrows)
+    uint32_t row0, nrows;     // list rows [row0, row0 + nrows)
     uint32_t ncols;
-    const uint64_t* spec;   // spectator string per column
-    const double* J;        // J[tri * ldj + col]
+    const uint64_t* spec;     // spectator string per column
+    const double* J;          // J[tri * ldj + col]
     size_t ldj;
     const uint32_t* flat[2];
     const uint64_t* off[2];
@@ -55,8 +64,8 @@ struct SameSpinArgs {
     const double* pv[2];
     const uint64_t* pm[2];
     const uint32_t* pab;
-    const double* diag;     // if set (write mode): Y = diag * Cself + acc
-    const double* Cself;
+    const double* diag;       // if set (write mode): Y = diag * Cself + acc
+    const double* Cself[kMaxM];
     int accumulate;
 };
 
@@ -70,20 +79,23 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t 
     return lo;
 }
 
-// (-1)^{popc(S & M)} applied to the high word of x: parity of a 64-bit AND
-// via one 32-bit POPC of (lo ^ hi).
-__device__ __forceinline__ double spectator_signed(double x, uint32_t slo, uint32_t shi, uint32_t mlo,
-                                                   uint32_t mhi) {
-    const uint32_t par = __popc((slo & mlo) ^ (shi & mhi));
-    return __hiloint2double(__double2hiint(x) ^ static_cast<int>(par << 31), __double2loint(x));
+// (-1)^{popc(S & M)} as a sign bit in position 31 (parity of a 64-bit AND
+// via one 32-bit POPC of lo ^ hi).
+__device__ __forceinline__ uint32_t spectator_sign(uint32_t slo, uint32_t shi, uint32_t mlo, uint32_t mhi) {
+    return __popc((slo & mlo) ^ (shi & mhi)) << 31;
+}
+
+__device__ __forceinline__ double xor_sign(double x, uint32_t sign31) {
+    return __hiloint2double(__double2hiint(x) ^ static_cast<int>(sign31), __double2loint(x));
 }
 
 // kTail: the CTA's column chunk crosses ncols, so column indices are clamped
 // (loads stay in bounds, stores are masked); full chunks use one base
 // pointer per entry with immediate offsets.
-template <bool kTail>
+template <bool kTail, int M>
 __global__ void __launch_bounds__(kSSBlock)
 k_samespin(const SameSpinArgs a, uint32_t chunk0) {
+    constexpr int R = SSR<M>::value;
     __shared__ uint32_t s_ja[kStage];
     __shared__ double s_v[kStage];
     __shared__ uint64_t s_m[kStage];
@@ -94,19 +106,20 @@ k_samespin(const SameSpinArgs a, uint32_t chunk0) {
     const uint32_t chunk = chunk0 + blockIdx.x / a.nrows;
     const uint32_t row = a.row0 + r;
     const uint32_t tid = threadIdx.x;
-    const uint32_t col0 = chunk * (kSSBlock * kSSR) + tid;
+    const uint32_t col0 = chunk * (kSSBlock * R) + tid;
 
-    uint32_t col[kSSR];
-    uint32_t slo[kSSR], shi[kSSR];
-    double acc[kSSR];
+    uint32_t col[R];
+    uint32_t slo[R], shi[R];
+    double acc[M][R];
 #pragma unroll
-    for (int q = 0; q < kSSR; ++q) {
+    for (int q = 0; q < R; ++q) {
         const uint32_t c = col0 + q * kSSBlock;
         col[q] = kTail ? min(c, a.ncols - 1) : c;
         const uint64_t sp = a.spec[col[q]];
         slo[q] = static_cast<uint32_t>(sp);
         shi[q] = static_cast<uint32_t>(sp >> 32);
-        acc[q] = 0.0;
+#pragma unroll
+        for (int v = 0; v < M; ++v) acc[v][q] = 0.0;
     }
 
     if (tid < 2) {
@@ -145,26 +158,31 @@ k_samespin(const SameSpinArgs a, uint32_t chunk0) {
                     const uint32_t mlo = static_cast<uint32_t>(m), mhi = static_cast<uint32_t>(m >> 32);
                     const uint32_t jsign = ab & 0x80000000u;
 #pragma unroll
-                    for (int q = 0; q < kSSR; ++q) {
+                    for (int q = 0; q < R; ++q) {
                         const uint32_t cq = kTail ? col[q] : col0 + q * kSSBlock;
-                        const double c = __ldg(a.C + rowoff + cq);
-                        const double j = __ldg(jrow + cq);
-                        const double val =
-                            v + __hiloint2double(__double2hiint(j) ^ static_cast<int>(jsign), __double2loint(j));
-                        acc[q] = fma(val, spectator_signed(c, slo[q], shi[q], mlo, mhi), acc[q]);
+                        const double val = v + xor_sign(__ldg(jrow + cq), jsign);
+                        const uint32_t sg = spectator_sign(slo[q], shi[q], mlo, mhi);
+#pragma unroll
+                        for (int vv = 0; vv < M; ++vv)
+                            acc[vv][q] = fma(val, xor_sign(__ldg(a.C[vv] + rowoff + cq), sg), acc[vv][q]);
                     }
                 }
             } else {
 #pragma unroll 4
                 for (int e = 0; e < cnt; ++e) {
-                    const double* base = a.C + static_cast<size_t>(s_ja[e]) * a.ldc + (kTail ? 0 : col0);
+                    const size_t rowoff = static_cast<size_t>(s_ja[e]) * a.ldc + (kTail ? 0 : col0);
                     const double v = s_v[e];
                     const uint64_t m = s_m[e];
                     const uint32_t mlo = static_cast<uint32_t>(m), mhi = static_cast<uint32_t>(m >> 32);
 #pragma unroll
-                    for (int q = 0; q < kSSR; ++q) {
-                        const double c = __ldg(kTail ? base + col[q] : base + q * kSSBlock);
-                        acc[q] = fma(v, spectator_signed(c, slo[q], shi[q], mlo, mhi), acc[q]);
+                    for (int q = 0; q < R; ++q) {
+                        const uint32_t sg = spectator_sign(slo[q], shi[q], mlo, mhi);
+#pragma unroll
+                        for (int vv = 0; vv < M; ++vv) {
+                            const double* base = a.C[vv] + rowoff;
+                            const double c = __ldg(kTail ? base + col[q] : base + q * kSSBlock);
+                            acc[vv][q] = fma(v, xor_sign(c, sg), acc[vv][q]);
+                        }
                     }
                 }
             }
@@ -172,37 +190,48 @@ k_samespin(const SameSpinArgs a, uint32_t chunk0) {
     }
 
 #pragma unroll
-    for (int q = 0; q < kSSR; ++q) {
+    for (int q = 0; q < R; ++q) {
         const uint32_t c = col0 + q * kSSBlock;
         if (kTail && c >= a.ncols) continue;
         const size_t yi = static_cast<size_t>(r) * a.ldy + c;
-        if (a.accumulate) {
-            a.Y[yi] += acc[q];
-        } else if (a.diag) {
-            a.Y[yi] = fma(a.diag[yi], a.Cself[yi], acc[q]);
-        } else {
-            a.Y[yi] = acc[q];
+#pragma unroll
+        for (int vv = 0; vv < M; ++vv) {
+            if (a.accumulate) {
+                a.Y[vv][yi] += acc[vv][q];
+            } else if (a.diag) {
+                a.Y[vv][yi] = fma(a.diag[yi], a.Cself[vv][yi], acc[vv][q]);
+            } else {
+                a.Y[vv][yi] = acc[vv][q];
+            }
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// Mixed alpha-beta kernel.  CTA = (output row ia, column part of
-// kMxBlock*kMxR beta strings).  For each alpha single ja of ia in the window:
-//   W[cd] = (pa qa|c d) (-1)^{popc(A_ja & Mbeta(c,d))}   built in smem,
-//   C[ja, segment] staged in smem (cp.async),
+// Mixed alpha-beta kernel.  CTA = (output row ia, 2048 beta slots).  Stage =
+// (alpha single ja of ia in the window, column segment g).  Two stage
+// buffers, each [ +W | -W | C_0[ja, seg] | ... | C_{M-1}[ja, seg] ]; the next
+// stage's row segments stream in with cp.async (and its W is built) while
+// the current one is consumed:
+//   W[cd] = (pa qa|c d) (-1)^{popc(A_ja & Mbeta(c,d))},
 // then each thread walks its beta strings' singles from the SELL-32 table
-// (one coalesced 4 B entry per element) gathering W[cd] and C[ja, jb] from
-// smem.  The ib-dependent alpha sign is applied once per (ja, ib).
+// (one coalesced 4 B entry per element, shared by the M vectors) gathering
+// W[cd] once and C_v[ja, jb] per vector from smem.  The ib-dependent alpha
+// sign is applied once per (ja, ib).
 // ---------------------------------------------------------------------------
 constexpr int kMxBlock = 1024;   // one CTA per SM, 32 warps
-constexpr int kMxR = 2;          // beta slots per thread -> 2048 slots per CTA
+
+// beta slots per thread (1024 * R slots per CTA); M = 4 keeps 64 registers
+template <int M>
+struct MxR {
+    static constexpr int value = M >= 4 ? 1 : 2;
+};
 
 struct MixedArgs {
-    const double* C;
+    const double* C[kMaxM];
     size_t ldc;
     uint32_t c_row0, j0, j1;
-    double* Y;
+    double* Y[kMaxM];
     size_t ldy;
     uint32_t row0, nrows, nb, nparts;
     const uint64_t* alpha;
@@ -227,15 +256,15 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
-// Stage = (alpha single ja, column segment g).  Two stage buffers, each
-// [ +W | -W | C[ja, segment] ]; the next stage's row segment streams in with
-// cp.async (and its W is built) while the current one is consumed.
+template <int M>
 __global__ void __launch_bounds__(kMxBlock, 1)
 k_mixed(const MixedArgs a) {
+    constexpr int kMxR = MxR<M>::value;
     extern __shared__ double smem[];
     const int nn = a.norbs * a.norbs;
     const uint32_t wdbl = static_cast<uint32_t>((2 * nn + 1) & ~1);
-    const uint32_t stage_dbl = wdbl + ((a.seg_cols + 1) & ~1u);
+    const uint32_t segpad = (a.seg_cols + 1) & ~1u;
+    const uint32_t stage_dbl = wdbl + M * segpad;
 
     const uint32_t r = blockIdx.x / a.nparts;
     const uint32_t part = blockIdx.x % a.nparts;
@@ -246,14 +275,14 @@ k_mixed(const MixedArgs a) {
 
     uint64_t B[kMxR];
     uint32_t slice[kMxR];
-    double sig[kMxR], acc[kMxR];
+    double sig[M][kMxR], acc[M][kMxR];
 #pragma unroll
     for (int q = 0; q < kMxR; ++q) {
         const uint32_t slot = part * (kMxBlock * kMxR) + q * kMxBlock + tid;
         B[q] = a.beta[a.perm[min(slot, a.nb - 1)]];
         slice[q] = slot / kWarp;
-        sig[q] = 0.0;
-        acc[q] = 0.0;
+#pragma unroll
+        for (int v = 0; v < M; ++v) sig[v][q] = acc[v][q] = 0.0;
     }
 
     const uint64_t o = a.sa_off[ia];
@@ -263,15 +292,19 @@ k_mixed(const MixedArgs a) {
     const uint32_t ke = lower_bound_u32(f, n, a.j1);
     const uint32_t nstages = (ke - kb) * a.nseg;
 
-    // issue stage i into buffer i & 1: C row segment (async) + +-W (threads)
+    // issue stage i into buffer i & 1: C row segments (async) + +-W (threads)
     auto issue = [&](uint32_t i) {
         double* buf = smem + (i & 1) * stage_dbl;
         const uint32_t k = kb + i / a.nseg, g = i % a.nseg;
         const uint32_t ja = f[k];
-        const double* src = a.C + static_cast<size_t>(ja - a.c_row0) * a.ldc + g * a.seg_cols;
         const uint32_t segw = min(a.seg_cols, a.nb - g * a.seg_cols);
-        double* crow = buf + wdbl;
-        for (uint32_t c = tid; c < segw; c += kMxBlock) cp_async8(crow + c, src + c);
+        const size_t src_off = static_cast<size_t>(ja - a.c_row0) * a.ldc + g * a.seg_cols;
+#pragma unroll
+        for (int v = 0; v < M; ++v) {
+            double* crow = buf + wdbl + v * segpad;
+            const double* src = a.C[v] + src_off;
+            for (uint32_t c = tid; c < segw; c += kMxBlock) cp_async8(crow + c, src + c);
+        }
         cp_async_commit();
         const uint64_t Ak = a.alpha[ja];
         const int pa = __ffsll(static_cast<long long>(A & ~Ak)) - 1;
@@ -294,20 +327,23 @@ k_mixed(const MixedArgs a) {
     for (uint32_t i = 0; i < nstages; ++i) {
         if (i + 1 < nstages) {
             issue(i + 1);          // buffer (i+1)&1 was released by the barrier ending stage i-1
-            cp_async_wait_prev();  // stage i's row has landed
+            cp_async_wait_prev();  // stage i's rows have landed
         } else {
             cp_async_wait_all();
         }
         __syncthreads();
         const char* wbase = reinterpret_cast<const char*>(smem + (i & 1) * stage_dbl);
         const char* cbase = reinterpret_cast<const char*>(smem + (i & 1) * stage_dbl + wdbl);
+        const uint32_t cstride = segpad * 8;  // bytes between the M staged rows
         const uint32_t g = i % a.nseg;
 #pragma unroll
         for (int q = 0; q < kMxR; ++q) {
             if (slice[q] >= a.nslices) continue;
             const uint32_t L = a.sell_len[slice[q] * a.nseg + g];
             const uint32_t* ent = a.sell + a.sell_off[slice[q] * a.nseg + g] + lane;
-            double s0 = 0.0, s1 = 0.0;
+            double s0[M], s1[M];
+#pragma unroll
+            for (int v = 0; v < M; ++v) s0[v] = s1[v] = 0.0;
             uint32_t t = 0;
 #pragma unroll 1
             for (; t + 8 <= L; t += 8) {
@@ -317,21 +353,26 @@ k_mixed(const MixedArgs a) {
 #pragma unroll
                 for (int u = 0; u < 8; u += 2) {
                     const double w0 = *reinterpret_cast<const double*>(wbase + ((e[u] >> 17) << 3));
-                    const double c0 = *reinterpret_cast<const double*>(cbase + (e[u] & 0x1ffffu));
                     const double w1 = *reinterpret_cast<const double*>(wbase + ((e[u + 1] >> 17) << 3));
-                    const double c1 = *reinterpret_cast<const double*>(cbase + (e[u + 1] & 0x1ffffu));
-                    s0 = fma(w0, c0, s0);
-                    s1 = fma(w1, c1, s1);
+                    const char* c0 = cbase + (e[u] & 0x1ffffu);
+                    const char* c1 = cbase + (e[u + 1] & 0x1ffffu);
+#pragma unroll
+                    for (int v = 0; v < M; ++v) {
+                        s0[v] = fma(w0, *reinterpret_cast<const double*>(c0 + v * cstride), s0[v]);
+                        s1[v] = fma(w1, *reinterpret_cast<const double*>(c1 + v * cstride), s1[v]);
+                    }
                 }
             }
 #pragma unroll 1
             for (; t < L; ++t) {
                 const uint32_t e0 = __ldg(ent + static_cast<size_t>(t) * kWarp);
                 const double w0 = *reinterpret_cast<const double*>(wbase + ((e0 >> 17) << 3));
-                const double c0 = *reinterpret_cast<const double*>(cbase + (e0 & 0x1ffffu));
-                s0 = fma(w0, c0, s0);
+                const char* c0 = cbase + (e0 & 0x1ffffu);
+#pragma unroll
+                for (int v = 0; v < M; ++v) s0[v] = fma(w0, *reinterpret_cast<const double*>(c0 + v * cstride), s0[v]);
             }
-            acc[q] += s0 + s1;
+#pragma unroll
+            for (int v = 0; v < M; ++v) acc[v][q] += s0[v] + s1[v];
         }
         if (g + 1 == a.nseg) {  // last segment of this ja: apply the alpha sign
             const uint32_t ja = f[kb + i / a.nseg];
@@ -342,8 +383,12 @@ k_mixed(const MixedArgs a) {
             const uint64_t ma = spectator_mask(0, pa, qa);
 #pragma unroll
             for (int q = 0; q < kMxR; ++q) {
-                sig[q] += flip_sign(acc[q], static_cast<uint32_t>(sA ^ (__popcll(B[q] & ma) & 1)));
-                acc[q] = 0.0;
+                const uint32_t sb = static_cast<uint32_t>(sA ^ (__popcll(B[q] & ma) & 1));
+#pragma unroll
+                for (int v = 0; v < M; ++v) {
+                    sig[v][q] += flip_sign(acc[v][q], sb);
+                    acc[v][q] = 0.0;
+                }
             }
         }
         __syncthreads();  // buffer i&1 free for stage i+2
@@ -352,7 +397,11 @@ k_mixed(const MixedArgs a) {
 #pragma unroll
     for (int q = 0; q < kMxR; ++q) {
         const uint32_t slot = part * (kMxBlock * kMxR) + q * kMxBlock + tid;
-        if (slot < a.nb) a.Y[static_cast<size_t>(r) * a.ldy + a.perm[slot]] += sig[q];
+        if (slot < a.nb) {
+            const size_t yi = static_cast<size_t>(r) * a.ldy + a.perm[slot];
+#pragma unroll
+            for (int v = 0; v < M; ++v) a.Y[v][yi] += sig[v][q];
+        }
     }
 }
 
@@ -434,160 +483,186 @@ struct PhaseTimer {
     }
 };
 
-SameSpinArgs alpha_args(const Handle& h, const double* Cb, uint32_t b0, uint32_t b1,
-                        const double* x_loc, double* y_loc, uint64_t a0, uint64_t a1, bool first) {
-    const ChannelTables& A = h.ch[0];
-    const ChannelTables& B = h.ch[1];
+using Ptrs = std::array<const double*, kMaxM>;
+using MPtrs = std::array<double*, kMaxM>;
+
+template <int M>
+void launch_samespin(const SameSpinArgs& s, cudaStream_t st) {
+    if (s.nrows == 0 || s.ncols == 0) return;
+    constexpr uint32_t kChunk = kSSBlock * SSR<M>::value;
+    const uint64_t full = s.ncols / kChunk;
+    const bool tail = s.ncols % kChunk != 0;
+    if (full) {
+        k_samespin<false, M><<<static_cast<unsigned>(full * s.nrows), kSSBlock, 0, st>>>(s, 0);
+        CUDA_LAUNCH_CHECK();
+    }
+    if (tail) {
+        k_samespin<true, M><<<s.nrows, kSSBlock, 0, st>>>(s, static_cast<uint32_t>(full));
+        CUDA_LAUNCH_CHECK();
+    }
+}
+
+void fill_lists(SameSpinArgs& s, const ChannelTables& t) {
+    for (int k = 0; k < 2; ++k) {
+        s.flat[k] = t.flat[k].p;
+        s.off[k] = t.offset[k].p;
+        s.len[k] = t.len[k].p;
+        s.pv[k] = t.pv[k].p;
+        s.pm[k] = t.pmask[k].p;
+    }
+    s.pab = t.pab.p;
+}
+
+template <int M>
+void launch_alpha(const Handle& h, const Ptrs& Cb, uint32_t b0, uint32_t b1, const Ptrs& x_loc,
+                  const MPtrs& y_loc, uint64_t a0, uint64_t a1, bool first) {
     SameSpinArgs s{};
-    s.C = Cb;
+    for (int v = 0; v < M; ++v) {
+        s.C[v] = Cb[v];
+        s.Y[v] = y_loc[v];
+        s.Cself[v] = x_loc[v];
+    }
     s.ldc = h.nb();
     s.c_row0 = b0;
     s.j0 = b0;
     s.j1 = b1;
-    s.Y = y_loc;
     s.ldy = h.nb();
     s.row0 = static_cast<uint32_t>(a0);
     s.nrows = static_cast<uint32_t>(a1 - a0);
     s.ncols = static_cast<uint32_t>(h.nb());
-    s.spec = B.strings.p;
-    s.J = B.J.p;
+    s.spec = h.ch[1].strings.p;
+    s.J = h.ch[1].J.p;
     s.ldj = h.nb();
-    for (int k = 0; k < 2; ++k) {
-        s.flat[k] = A.flat[k].p;
-        s.off[k] = A.offset[k].p;
-        s.len[k] = A.len[k].p;
-        s.pv[k] = A.pv[k].p;
-        s.pm[k] = A.pmask[k].p;
-    }
-    s.pab = A.pab.p;
+    fill_lists(s, h.ch[0]);
     s.diag = first ? h.diag.p + (a0 - h.a0) * h.nb() : nullptr;
-    s.Cself = x_loc;
     s.accumulate = first ? 0 : 1;
-    return s;
+    launch_samespin<M>(s, h.stream);
 }
 
-void launch_samespin(const SameSpinArgs& s, cudaStream_t st) {
-    if (s.nrows == 0 || s.ncols == 0) return;
-    constexpr uint32_t kChunk = kSSBlock * kSSR;
-    const uint64_t full = s.ncols / kChunk;
-    const bool tail = s.ncols % kChunk != 0;
-    if (full) {
-        k_samespin<false><<<static_cast<unsigned>(full * s.nrows), kSSBlock, 0, st>>>(s, 0);
-        CUDA_LAUNCH_CHECK();
-    }
-    if (tail) {
-        k_samespin<true><<<s.nrows, kSSBlock, 0, st>>>(s, static_cast<uint32_t>(full));
-        CUDA_LAUNCH_CHECK();
-    }
-}
-
-size_t mixed_smem(const Handle& h) {
+size_t mixed_smem(const Handle& h, const SellTable& t, int M) {
     const size_t nn = static_cast<size_t>(h.norbs) * h.norbs;
-    return 2 * (((2 * nn + 1) & ~size_t{1}) + ((h.seg_cols + 1) & ~size_t{1})) * sizeof(double);
+    return 2 * (((2 * nn + 1) & ~size_t{1}) + M * ((t.seg_cols + 1) & ~size_t{1})) * sizeof(double);
 }
 
-void launch_mixed(const Handle& h, const double* Cb, uint32_t b0, uint32_t b1, double* y_loc,
-                  uint64_t a0, uint64_t a1, cudaStream_t st) {
+template <int M>
+void launch_mixed(Handle& h, const Ptrs& Cb, uint32_t b0, uint32_t b1, const MPtrs& y_loc, uint64_t a0,
+                  uint64_t a1) {
+    const SellTable& t = mixed_table(h, M);
     MixedArgs m{};
-    m.C = Cb;
+    for (int v = 0; v < M; ++v) {
+        m.C[v] = Cb[v];
+        m.Y[v] = y_loc[v];
+    }
     m.ldc = h.nb();
     m.c_row0 = b0;
     m.j0 = b0;
     m.j1 = b1;
-    m.Y = y_loc;
     m.ldy = h.nb();
     m.row0 = static_cast<uint32_t>(a0);
     m.nrows = static_cast<uint32_t>(a1 - a0);
     m.nb = static_cast<uint32_t>(h.nb());
-    m.nparts = (m.nb + kMxBlock * kMxR - 1) / (kMxBlock * kMxR);
+    m.nparts = (m.nb + kMxBlock * MxR<M>::value - 1) / (kMxBlock * MxR<M>::value);
     m.alpha = h.ch[0].strings.p;
     m.beta = h.ch[1].strings.p;
     m.sa_flat = h.ch[0].flat[0].p;
     m.sa_off = h.ch[0].offset[0].p;
     m.sa_len = h.ch[0].len[0].p;
-    m.sell = h.sell.p;
-    m.sell_off = h.sell_off.p;
-    m.sell_len = h.sell_len.p;
+    m.sell = t.sell.p;
+    m.sell_off = t.off.p;
+    m.sell_len = t.len.p;
     m.perm = h.sell_perm.p;
-    m.seg_cols = h.seg_cols;
-    m.nseg = h.nseg;
+    m.seg_cols = t.seg_cols;
+    m.nseg = t.nseg;
     m.nslices = h.nslices;
     m.eri = h.d_eri.p;
     m.norbs = h.norbs;
     if (m.nrows == 0) return;
-    const size_t smem = mixed_smem(h);
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        CUDA_CHECK(cudaFuncSetAttribute(k_mixed, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const size_t smem = mixed_smem(h, t, M);
+    static size_t configured[kMaxM + 1] = {0};
+    if (smem > configured[M]) {
+        CUDA_CHECK(cudaFuncSetAttribute(k_mixed<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
-        configured = smem;
+        configured[M] = smem;
     }
     const uint64_t grid = static_cast<uint64_t>(m.nrows) * m.nparts;
-    k_mixed<<<static_cast<unsigned>(grid), kMxBlock, smem, st>>>(m);
+    k_mixed<M><<<static_cast<unsigned>(grid), kMxBlock, smem, h.stream>>>(m);
     CUDA_LAUNCH_CHECK();
 }
 
+// Scratch for M vectors: C^T / sigma^T blocks and ring buffers.
+void ensure_scratch(Handle& h, int M, int P) {
+    const size_t block = static_cast<size_t>(h.max_blk) * h.nb();
+    if (h.ct.n < M * block) {
+        h.ct.alloc(M * block);
+        h.yt.alloc(M * block);
+    }
+    if (P > 1 && h.ring[0].n < M * block) {
+        h.ring[0].alloc(M * block);
+        h.ring[1].alloc(M * block);
+    }
+}
+
 // The beta term for rows [a0, a1): transpose, same-spin kernel on C^T with
-// the alpha strings as spectators, result in h.yt ([nb][nloc]).
-void beta_term(Handle& h, const double* x_loc, uint64_t a0, uint64_t a1, PhaseTimer& tm) {
+// the alpha strings as spectators, result in h.yt (M x [nb][nloc]).
+template <int M>
+void beta_term(Handle& h, const Ptrs& x_loc, uint64_t a0, uint64_t a1, PhaseTimer& tm) {
     const uint32_t nloc = static_cast<uint32_t>(a1 - a0), nb = static_cast<uint32_t>(h.nb());
+    const size_t block = static_cast<size_t>(h.max_blk) * h.nb();
     const int id = tm.begin(1);
     dim3 tb(kTile, 8), tg((nb + kTile - 1) / kTile, (nloc + kTile - 1) / kTile);
-    k_transpose<<<tg, tb, 0, h.stream>>>(x_loc, nb, h.ct.p, nloc, nloc, nb);
-    CUDA_LAUNCH_CHECK();
-    const ChannelTables& A = h.ch[0];
-    const ChannelTables& B = h.ch[1];
     SameSpinArgs s{};
-    s.C = h.ct.p;
+    for (int v = 0; v < M; ++v) {
+        k_transpose<<<tg, tb, 0, h.stream>>>(x_loc[v], nb, h.ct.p + v * block, nloc, nloc, nb);
+        CUDA_LAUNCH_CHECK();
+        s.C[v] = h.ct.p + v * block;
+        s.Y[v] = h.yt.p + v * block;
+    }
     s.ldc = nloc;
     s.c_row0 = 0;
     s.j0 = 0;
     s.j1 = nb;
-    s.Y = h.yt.p;
     s.ldy = nloc;
     s.row0 = 0;
     s.nrows = nb;
     s.ncols = nloc;
-    s.spec = A.strings.p + a0;
-    s.J = A.J.p + a0;
+    s.spec = h.ch[0].strings.p + a0;
+    s.J = h.ch[0].J.p + a0;
     s.ldj = h.na();
-    for (int k = 0; k < 2; ++k) {
-        s.flat[k] = B.flat[k].p;
-        s.off[k] = B.offset[k].p;
-        s.len[k] = B.len[k].p;
-        s.pv[k] = B.pv[k].p;
-        s.pm[k] = B.pmask[k].p;
-    }
-    s.pab = B.pab.p;
+    fill_lists(s, h.ch[1]);
     s.accumulate = 0;
-    launch_samespin(s, h.stream);
+    launch_samespin<M>(s, h.stream);
     tm.end(id);
 }
 
-void combine(Handle& h, double* y_loc, uint64_t a0, uint64_t a1, PhaseTimer& tm) {
+template <int M>
+void combine(Handle& h, const MPtrs& y_loc, uint64_t a0, uint64_t a1, PhaseTimer& tm) {
     const uint32_t nloc = static_cast<uint32_t>(a1 - a0), nb = static_cast<uint32_t>(h.nb());
+    const size_t block = static_cast<size_t>(h.max_blk) * h.nb();
     const int id = tm.begin(3);
     dim3 tb(kTile, 8), tg((nb + kTile - 1) / kTile, (nloc + kTile - 1) / kTile);
-    k_transpose_add<<<tg, tb, 0, h.stream>>>(h.yt.p, nloc, y_loc, nb, nloc, nb);
-    CUDA_LAUNCH_CHECK();
+    for (int v = 0; v < M; ++v) {
+        k_transpose_add<<<tg, tb, 0, h.stream>>>(h.yt.p + v * block, nloc, y_loc[v], nb, nloc, nb);
+        CUDA_LAUNCH_CHECK();
+    }
     tm.end(id);
 }
 
-// One block-rank's sigma with the C ring.  `fetch(s, dst, block)` enqueues on
-// h.comm_stream the transfer that makes block `block` resident in dst for
-// step s (NCCL send/recv, or a device copy for virtual blocks).
-template <class Fetch>
-void sigma_ring(Handle& h, int g, int P, const double* x_loc, double* y_loc, PhaseTimer& tm,
-                Fetch&& fetch) {
+// One block-rank's sigma with the C ring.  `fetch(s, held, dst, block)`
+// enqueues on h.comm_stream the transfer that makes alpha block `block`
+// resident in dst (M consecutive block-sized slabs) for step s + 1 (NCCL
+// send/recv, or a device copy for virtual blocks).
+template <int M, class Fetch>
+void sigma_ring(Handle& h, int g, int P, const Ptrs& x_loc, const MPtrs& y_loc, PhaseTimer& tm, Fetch&& fetch) {
     const uint64_t a0 = h.blk[g], a1 = h.blk[g + 1];
+    const size_t block = static_cast<size_t>(h.max_blk) * h.nb();
     cudaEvent_t* done_compute = h.ev;      // [0..1]
     cudaEvent_t* done_comm = h.ev + 2;     // [2..3]
     // x and the ring buffers are produced / last read on the compute stream:
     // the comm stream must not send or overwrite them before that work ends.
     CUDA_CHECK(cudaEventRecord(h.ev[4], h.stream));
     CUDA_CHECK(cudaStreamWaitEvent(h.comm_stream, h.ev[4], 0));
-    beta_term(h, x_loc, a0, a1, tm);
-    const double* held = x_loc;
+    beta_term<M>(h, x_loc, a0, a1, tm);
+    Ptrs held = x_loc;
     for (int s = 0; s < P; ++s) {
         const int b = (g + s) % P;
         if (s + 1 < P) {
@@ -598,53 +673,67 @@ void sigma_ring(Handle& h, int g, int P, const double* x_loc, double* y_loc, Pha
         }
         const uint32_t b0 = static_cast<uint32_t>(h.blk[b]), b1 = static_cast<uint32_t>(h.blk[b + 1]);
         int id = tm.begin(0);
-        launch_samespin(alpha_args(h, held, b0, b1, x_loc, y_loc, a0, a1, s == 0), h.stream);
+        launch_alpha<M>(h, held, b0, b1, x_loc, y_loc, a0, a1, s == 0);
         tm.end(id);
         id = tm.begin(2);
-        launch_mixed(h, held, b0, b1, y_loc, a0, a1, h.stream);
+        launch_mixed<M>(h, held, b0, b1, y_loc, a0, a1);
         tm.end(id);
         CUDA_CHECK(cudaEventRecord(done_compute[s % 2], h.stream));
         if (s + 1 < P) {
             CUDA_CHECK(cudaStreamWaitEvent(h.stream, done_comm[s % 2], 0));
-            held = h.ring[s % 2].p;
+            for (int v = 0; v < M; ++v) held[v] = h.ring[s % 2].p + v * block;
         }
     }
-    combine(h, y_loc, a0, a1, tm);
+    combine<M>(h, y_loc, a0, a1, tm);
 }
 
-} // namespace
-
-namespace {
-
-void sigma_schedule(Handle& h, const double* dx, double* dy, PhaseTimer& tm) {
+template <int M>
+void sigma_schedule_m(Handle& h, const Ptrs& dx, const MPtrs& dy, PhaseTimer& tm) {
     const size_t nb = h.nb();
     const int P = std::max(h.world, h.vblocks);
+    const size_t block = static_cast<size_t>(h.max_blk) * nb;
+    ensure_scratch(h, M, P);
     if (h.world > 1) {
         const int g = h.rank;
-        sigma_ring(h, g, P, dx, dy, tm, [&](int s, const double* held, double* dst, int next) {
+        sigma_ring<M>(h, g, P, dx, dy, tm, [&](int s, const Ptrs& held, double* dst, int next) {
             const int cur = (g + s) % P;
             const size_t send_n = (h.blk[cur + 1] - h.blk[cur]) * nb;
             const size_t recv_n = (h.blk[next + 1] - h.blk[next]) * nb;
             if (ncclGroupStart() != ncclSuccess) fail(DETCI_GPU_E_CUDA, "ncclGroupStart");
-            ncclSend(held, send_n, ncclDouble, (g - 1 + P) % P, h.nccl, h.comm_stream);
-            ncclRecv(dst, recv_n, ncclDouble, (g + 1) % P, h.nccl, h.comm_stream);
+            for (int v = 0; v < M; ++v) {
+                ncclSend(held[v], send_n, ncclDouble, (g - 1 + P) % P, h.nccl, h.comm_stream);
+                ncclRecv(dst + v * block, recv_n, ncclDouble, (g + 1) % P, h.nccl, h.comm_stream);
+            }
             if (ncclGroupEnd() != ncclSuccess) fail(DETCI_GPU_E_CUDA, "ncclGroupEnd (ring)");
         });
     } else if (P > 1) {
         // Virtual blocks: every block-rank's schedule runs in turn on this GPU;
         // the ring transport is a device copy out of the full x.
         for (int g = 0; g < P; ++g) {
-            const double* xg = dx + h.blk[g] * nb;
-            double* yg = dy + h.blk[g] * nb;
-            sigma_ring(h, g, P, xg, yg, tm, [&](int, const double*, double* dst, int next) {
+            Ptrs xg{};
+            MPtrs yg{};
+            for (int v = 0; v < M; ++v) {
+                xg[v] = dx[v] + h.blk[g] * nb;
+                yg[v] = dy[v] + h.blk[g] * nb;
+            }
+            sigma_ring<M>(h, g, P, xg, yg, tm, [&](int, const Ptrs&, double* dst, int next) {
                 const size_t n = (h.blk[next + 1] - h.blk[next]) * nb;
-                CUDA_CHECK(cudaMemcpyAsync(dst, dx + h.blk[next] * nb, n * sizeof(double),
-                                           cudaMemcpyDeviceToDevice, h.comm_stream));
+                for (int v = 0; v < M; ++v)
+                    CUDA_CHECK(cudaMemcpyAsync(dst + v * block, dx[v] + h.blk[next] * nb, n * sizeof(double),
+                                               cudaMemcpyDeviceToDevice, h.comm_stream));
             });
         }
     } else {
-        sigma_ring(h, 0, 1, dx, dy, tm, [](int, const double*, double*, int) {});
+        sigma_ring<M>(h, 0, 1, dx, dy, tm, [](int, const Ptrs&, double*, int) {});
     }
+}
+
+void sigma_schedule(Handle& h, const double* dx, double* dy, PhaseTimer& tm) {
+    Ptrs x{};
+    MPtrs y{};
+    x[0] = dx;
+    y[0] = dy;
+    sigma_schedule_m<1>(h, x, y, tm);
 }
 
 } // namespace
@@ -653,6 +742,29 @@ void sigma_enqueue(Handle& h, const double* dx, double* dy) {
     if (!h.built) fail(DETCI_GPU_E_INPUT, "sigma: basis not built");
     PhaseTimer tm(h, false);
     sigma_schedule(h, dx, dy, tm);
+}
+
+void sigma_block(Handle& h, const double* const* dx, double* const* dy, int m) {
+    if (!h.built) fail(DETCI_GPU_E_INPUT, "sigma: basis not built");
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j)
+            if (dx[i] == dy[j]) fail(DETCI_GPU_E_INPUT, "sigma: x and y must not alias");
+    PhaseTimer tm(h, false);
+    int i = 0;
+    while (i < m) {
+        Ptrs x{};
+        MPtrs y{};
+        const int take = m - i >= 4 ? 4 : (m - i >= 2 ? 2 : 1);
+        for (int v = 0; v < take; ++v) {
+            x[v] = dx[i + v];
+            y[v] = dy[i + v];
+        }
+        if (take == 4) sigma_schedule_m<4>(h, x, y, tm);
+        else if (take == 2) sigma_schedule_m<2>(h, x, y, tm);
+        else sigma_schedule_m<1>(h, x, y, tm);
+        i += take;
+    }
+    CUDA_CHECK(cudaStreamSynchronize(h.stream));
 }
 
 void sigma_device(Handle& h, const double* dx, double* dy, detci_gpu_timings* out) {

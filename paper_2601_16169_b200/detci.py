@@ -214,6 +214,35 @@ def matvec(basis: GpuBasis, x: np.ndarray, y: Optional[np.ndarray] = None, timin
     return out
 
 
+def matvec_block(basis: GpuBasis, X: np.ndarray) -> np.ndarray:
+    """Y[i] = H X[i] for m vectors through one blocked device pass
+    (detci_gpu_sigma_block; element work shared by the vectors)."""
+    X = _f64(X)
+    X = X.reshape(-1, basis.local_dim)
+    m = X.shape[0]
+    lib = basis._lib
+    dx = (C.c_void_p * m)()
+    dy = (C.c_void_p * m)()
+    try:
+        for i in range(m):
+            for arr in (dx, dy):
+                p = C.c_void_p()
+                basis._check(lib.detci_gpu_alloc_vector(basis.handle, C.byref(p)))
+                arr[i] = p.value
+            basis._check(lib.detci_gpu_copy_vector(basis.handle, dx[i], X[i].ctypes.data, 0))
+        basis._check(lib.detci_gpu_sigma_block(basis.handle, C.cast(dx, C.POINTER(C.c_void_p)),
+                                               C.cast(dy, C.POINTER(C.c_void_p)), m))
+        Y = np.empty_like(X)
+        for i in range(m):
+            basis._check(lib.detci_gpu_copy_vector(basis.handle, Y[i].ctypes.data, dy[i], 1))
+        return Y
+    finally:
+        for arr in (dx, dy):
+            for i in range(m):
+                if arr[i]:
+                    lib.detci_gpu_free_vector(basis.handle, arr[i])
+
+
 def davidson_solve(basis: GpuBasis, opts: DavidsonOptions = DavidsonOptions(), want_vector: bool = True,
                    callback: Optional[Callable[[IterationStats, int], None]] = None) -> DavidsonResult:
     """davidson_solve (davidson.hpp:85-86) over the device sigma and device vector ops."""
@@ -246,6 +275,44 @@ def davidson_solve(basis: GpuBasis, opts: DavidsonOptions = DavidsonOptions(), w
     its = [_iter_stats(trace[i]) for i in range(r.iterations)]
     return DavidsonResult(status=SOLVE_STATUS[r.status], converged=bool(r.converged), energy=r.energy,
                           eigenvector=vec, iterations=its, seconds=r.seconds)
+
+
+@dataclass
+class MultiRootResult:
+    status: str
+    converged: bool
+    energies: np.ndarray
+    residuals: np.ndarray
+    eigenvectors: Optional[np.ndarray]     # (nroots, local_dim)
+    iterations: List[IterationStats] = field(default_factory=list)
+    seconds: float = 0.0
+
+
+def davidson_roots(basis: GpuBasis, nroots: int, tol: float = 1e-8, max_iter: int = 200,
+                   max_subspace: int = 0, want_vectors: bool = True) -> MultiRootResult:
+    """Lowest `nroots` eigenpairs by block Davidson (BASELINE config C5); the
+    reference itself is single-root (davidson.hpp:83-86)."""
+    o = _lib.DavBlockOpts()
+    o.tol = tol
+    o.max_iter = max_iter
+    o.max_subspace = max_subspace or max(20, 2 * nroots + 4)
+    o.nroots = nroots
+    r = _lib.DavBlockResult()
+    e = np.zeros(max(nroots, 1))
+    res = np.zeros(max(nroots, 1))
+    r.energies = _ptr(e, C.c_double)
+    r.residuals = _ptr(res, C.c_double)
+    vec = np.zeros((max(nroots, 1), basis.local_dim)) if want_vectors else None
+    if vec is not None:
+        r.eigenvectors = _ptr(vec, C.c_double)
+    cap = max(1, max_iter)
+    trace = (_lib.DavIter * cap)()
+    r.trace = C.cast(trace, C.POINTER(_lib.DavIter))
+    r.trace_cap = cap
+    basis._check(basis._lib.detci_gpu_davidson_roots(basis.handle, C.byref(o), C.byref(r)))
+    return MultiRootResult(status=SOLVE_STATUS[r.status], converged=bool(r.converged), energies=e[:nroots],
+                           residuals=res[:nroots], eigenvectors=vec,
+                           iterations=[_iter_stats(trace[i]) for i in range(r.iterations)], seconds=r.seconds)
 
 
 def _iter_stats(it) -> IterationStats:

@@ -132,3 +132,28 @@ def test_config_sigma_rows_vs_reference(cfg):
         hz = detci.matvec(b, z)
         assert rel_diff(detci.matvec(b, x + z), y + hz) <= 1e-12
         assert abs(x @ hz - y @ z) <= 1e-10 * max(1.0, abs(x @ hz))
+
+
+@pytest.mark.parametrize("m,blocks", [(4, 1), (3, 1), (2, 1), (4, 3), (5, 2)])
+def test_blocked_sigma_equals_per_vector(m, blocks):
+    """detci_gpu_sigma_block (M = 4/2/1 kernels, virtual blocks too) against
+    one sigma per vector."""
+    ints = synth.synthetic_integrals(12, 8)
+    s = synth.synthetic_strings(12, 4, 200)
+    with gpu_basis(ints, s, s, virtual_blocks=blocks, weighted_partition=True) as b:
+        X = np.stack([synth.random_vector(b.dimension(), 30 + i) for i in range(m)])
+        Y = detci.matvec_block(b, X)
+        for i in range(m):
+            assert rel_diff(Y[i], detci.matvec(b, X[i])) <= 1e-12
+
+
+def test_blocked_sigma_c1_rows():
+    rows = np.load(GOLDEN / "rows_C1.npz")
+    ints, a, bb = synth.synthetic_system("C1")
+    with gpu_basis(ints, a, bb) as b:
+        x = synth.random_vector(b.dimension(), 11)
+        X = np.stack([x, 2.0 * x, -x, 0.5 * x])
+        Y = detci.matvec_block(b, X)
+        r = rows["rows"].astype(np.int64)
+        for i, scale in enumerate((1.0, 2.0, -1.0, 0.5)):
+            assert rel_diff(Y[i].reshape(len(a), -1)[r], scale * rows["sigma_rows"]) <= 1e-12
