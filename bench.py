@@ -311,6 +311,28 @@ def run_gpu_arm(args):
     roofline_sigma = {"bytes_per_sigma": sigma_bytes, "achieved": sigma_achieved, "unit": "GB/s",
                       "frac_of_measured": sigma_achieved / peak, "frac_of_8TBs": sigma_achieved / 8000.0}
 
+    # ---- blocked sigma over 4 vectors (the multi-root Davidson's block)
+    blocked = None
+    if args.block > 1 and world == 1:
+        mvec = args.block
+        xs = [dx] + [torch.from_numpy(synth.random_vector(dim_loc, 40 + i)).cuda() for i in range(mvec - 1)]
+        ys = [torch.empty_like(dx) for _ in range(mvec)]
+        px = (C.c_void_p * mvec)(*[t.data_ptr() for t in xs])
+        py = (C.c_void_p * mvec)(*[t.data_ptr() for t in ys])
+        pxp, pyp = C.cast(px, C.POINTER(C.c_void_p)), C.cast(py, C.POINTER(C.c_void_p))
+        assert lib.detci_gpu_sigma_block(basis.handle, pxp, pyp, mvec) == 0     # warm (builds the M-table)
+        b0e, b1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nrep = max(1, min(3, args.steps))
+        b0e.record(ext)
+        for _ in range(nrep):
+            assert lib.detci_gpu_sigma_block(basis.handle, pxp, pyp, mvec) == 0
+        b1e.record(ext)
+        b1e.synchronize()
+        per_block = b0e.elapsed_time(b1e) * 1e-3 / nrep
+        blocked = {"vectors": mvec, "seconds_per_block": per_block, "seconds_per_vector": per_block / mvec,
+                   "dets_per_s_per_vector": dim * mvec / per_block, "speedup_vs_single": per_step * mvec / per_block}
+        del xs, ys
+
     # ---- full Davidson (s/iter of the whole solver) on the same basis
     dav = None
     if args.davidson:
@@ -353,6 +375,7 @@ def run_gpu_arm(args):
             "gpu_launches": launches,
             "clocks": clocks,
             "davidson": dav,
+            "blocked_sigma": blocked,
         }
         print(json.dumps(line), flush=True)
     basis.close()
@@ -372,6 +395,7 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=8.0, help="target CPU seconds per reference sample")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-davidson", dest="davidson", action="store_false")
+    ap.add_argument("--block", type=int, default=4, help="vectors in the blocked-sigma measurement (0 = skip)")
     ap.add_argument("--davidson-iters", type=int, default=30,
                     help="Davidson iterations timed for s/iter (reference defaults otherwise)")
     args = ap.parse_args()

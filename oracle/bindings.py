@@ -82,6 +82,9 @@ class RefLib:
                                    C.POINTER(C.c_int), dp, dp, C.c_int, dp]
         L.ref_dense_hamiltonian.argtypes = [vp, dp, C.c_uint64]
         L.ref_hij.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, dp]
+        self.APPLY = C.CFUNCTYPE(None, dp, dp, C.c_uint64, vp)
+        L.ref_davidson_operator.argtypes = [self.APPLY, vp, dp, C.c_uint64, C.c_double, C.c_int, C.c_int, dp,
+                                            C.POINTER(C.c_int), C.POINTER(C.c_int), dp, C.c_int]
         L.ref_brute_force_hij.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, dp]
 
     def check(self, code):
@@ -129,6 +132,26 @@ class RefLib:
         self.check(self.lib.ref_generate_table(_p(m, C.c_uint64), len(m), norbs, kind, _p(flat, C.c_uint32),
                                                _p(off, C.c_uint64), _p(ln, C.c_uint32), C.byref(nflat)))
         return flat[: nflat.value], off, ln
+
+    def davidson_operator(self, apply, diag, tol=1e-8, max_iter=200, max_subspace=20):
+        """The reference davidson_solve over a caller-supplied operator
+        apply(x: ndarray, y: ndarray) (SURVEY.md 7.2.7 mixed oracle)."""
+        diag = np.ascontiguousarray(diag, dtype=np.float64)
+        n = len(diag)
+
+        def cb(xp, yp, nn, _user):
+            x = np.ctypeslib.as_array(xp, shape=(nn,))
+            y = np.ctypeslib.as_array(yp, shape=(nn,))
+            apply(x, y)
+
+        fn = self.APPLY(cb)
+        e = C.c_double()
+        it, st = C.c_int(), C.c_int()
+        trace = np.zeros((max_iter, 4))
+        self.check(self.lib.ref_davidson_operator(fn, None, _p(diag, C.c_double), n, tol, max_iter, max_subspace,
+                                                  C.byref(e), C.byref(it), C.byref(st), _p(trace, C.c_double),
+                                                  max_iter))
+        return {"energy": e.value, "iterations": it.value, "status": st.value, "trace": trace[: it.value]}
 
     def shuffle(self, masks, norbs, seed):
         m = np.ascontiguousarray(masks, dtype=np.uint64).copy()

@@ -28,3 +28,25 @@ def test_reference_pipeline_with_device_sigma(name):
         assert abs(float(lines[k][0]) - e_ref) <= 1e-10 * abs(e_ref), (k, lines)
     if name == "chain8":
         assert lines["reference"][0] == "-2.420193979007e+00"
+
+
+def test_reference_solver_over_device_sigma_c1():
+    """The unmodified reference davidson_solve driving the device sigma
+    (ctypes LinearOperator callback) at the C1 shape, against the device
+    Davidson: same energy (1e-8 Ha) and iteration count."""
+    from oracle.bindings import REF_SO, RefLib
+    from paper_2601_16169_b200 import detci, synth
+
+    if not REF_SO.exists():
+        pytest.skip("reference library not built")
+    ref = RefLib()
+    ints, a, b = synth.synthetic_system("C1")
+    with detci.GpuBasis(ints.norbs, a, b, ints.core, ints.h1, ints.eri) as basis:
+        diag = basis.diag()
+        mixed = ref.davidson_operator(lambda x, y: detci.matvec(basis, x, y), diag)
+        dev = detci.davidson_solve(basis, want_vector=False)
+    assert mixed["status"] == 0 and dev.converged
+    assert abs(mixed["energy"] - dev.energy) <= 1e-8
+    assert abs(mixed["iterations"] - len(dev.iterations)) <= 2
+    for r, it in zip(mixed["trace"][:20], dev.iterations[:20]):
+        assert abs(r[0] - it.ritz_value) <= 1e-9 * abs(r[0])
