@@ -224,7 +224,7 @@ constexpr int kMxBlock = 1024;   // one CTA per SM, 32 warps
 // beta slots per thread (1024 * R slots per CTA); M = 4 keeps 64 registers
 template <int M>
 struct MxR {
-    static constexpr int value = M >= 4 ? 1 : 2;
+    static constexpr int value = 2;
 };
 
 struct MixedArgs {
@@ -261,10 +261,15 @@ __global__ void __launch_bounds__(kMxBlock, 1)
 k_mixed(const MixedArgs a) {
     constexpr int kMxR = MxR<M>::value;
     extern __shared__ double smem[];
+    // layout: [ W buffer 0 | W buffer 1 | C stage 0 (M rows) | C stage 1 ]
+    // W is double-buffered per alpha single (built once per ja), the C row
+    // segments per stage = (ja, segment).
     const int nn = a.norbs * a.norbs;
     const uint32_t wdbl = static_cast<uint32_t>((2 * nn + 1) & ~1);
     const uint32_t segpad = (a.seg_cols + 1) & ~1u;
-    const uint32_t stage_dbl = wdbl + M * segpad;
+    double* const wbuf0 = smem;
+    double* const cbuf0 = smem + 2 * wdbl;
+    const uint32_t cstage = M * segpad;
 
     const uint32_t r = blockIdx.x / a.nparts;
     const uint32_t part = blockIdx.x % a.nparts;
@@ -292,33 +297,37 @@ k_mixed(const MixedArgs a) {
     const uint32_t ke = lower_bound_u32(f, n, a.j1);
     const uint32_t nstages = (ke - kb) * a.nseg;
 
-    // issue stage i into buffer i & 1: C row segments (async) + +-W (threads)
+    // issue stage i: C row segments (async) into C buffer i & 1, and, on the
+    // first segment of a new ja, +-W into W buffer (ja index) & 1
     auto issue = [&](uint32_t i) {
-        double* buf = smem + (i & 1) * stage_dbl;
-        const uint32_t k = kb + i / a.nseg, g = i % a.nseg;
-        const uint32_t ja = f[k];
+        const uint32_t kk = i / a.nseg, g = i % a.nseg;
+        const uint32_t ja = f[kb + kk];
         const uint32_t segw = min(a.seg_cols, a.nb - g * a.seg_cols);
         const size_t src_off = static_cast<size_t>(ja - a.c_row0) * a.ldc + g * a.seg_cols;
+        double* cb = cbuf0 + (i & 1) * cstage;
 #pragma unroll
         for (int v = 0; v < M; ++v) {
-            double* crow = buf + wdbl + v * segpad;
+            double* crow = cb + v * segpad;
             const double* src = a.C[v] + src_off;
             for (uint32_t c = tid; c < segw; c += kMxBlock) cp_async8(crow + c, src + c);
         }
         cp_async_commit();
-        const uint64_t Ak = a.alpha[ja];
-        const int pa = __ffsll(static_cast<long long>(A & ~Ak)) - 1;
-        const int qa = __ffsll(static_cast<long long>(Ak & ~A)) - 1;
-        const double* erow = a.eri + static_cast<size_t>(pa * a.norbs + qa) * nn;
-        for (int cd = tid; cd < nn; cd += kMxBlock) {
-            const int c = cd / a.norbs, d = cd - c * a.norbs;
-            double v = 0.0;
-            if (c != d) {
-                v = erow[cd];
-                if (__popcll(Ak & spectator_mask(1, c, d)) & 1) v = -v;
+        if (g == 0) {
+            double* wb = wbuf0 + (kk & 1) * wdbl;
+            const uint64_t Ak = a.alpha[ja];
+            const int pa = __ffsll(static_cast<long long>(A & ~Ak)) - 1;
+            const int qa = __ffsll(static_cast<long long>(Ak & ~A)) - 1;
+            const double* erow = a.eri + static_cast<size_t>(pa * a.norbs + qa) * nn;
+            for (int cd = tid; cd < nn; cd += kMxBlock) {
+                const int c = cd / a.norbs, d = cd - c * a.norbs;
+                double v = 0.0;
+                if (c != d) {
+                    v = erow[cd];
+                    if (__popcll(Ak & spectator_mask(1, c, d)) & 1) v = -v;
+                }
+                wb[cd] = v;
+                wb[nn + cd] = -v;
             }
-            buf[cd] = v;
-            buf[nn + cd] = -v;
         }
     };
 
@@ -326,56 +335,82 @@ k_mixed(const MixedArgs a) {
 #pragma unroll 1
     for (uint32_t i = 0; i < nstages; ++i) {
         if (i + 1 < nstages) {
-            issue(i + 1);          // buffer (i+1)&1 was released by the barrier ending stage i-1
+            // C buffer (i+1)&1 was released by the barrier ending stage i-1;
+            // W buffer ((i+1)/nseg)&1 differs from the one in use when the
+            // next stage starts a new ja (its previous user finished 2 ja ago)
+            issue(i + 1);
             cp_async_wait_prev();  // stage i's rows have landed
         } else {
             cp_async_wait_all();
         }
         __syncthreads();
-        const char* wbase = reinterpret_cast<const char*>(smem + (i & 1) * stage_dbl);
-        const char* cbase = reinterpret_cast<const char*>(smem + (i & 1) * stage_dbl + wdbl);
+        const uint32_t kk = i / a.nseg, g = i % a.nseg;
+        const char* wbase = reinterpret_cast<const char*>(wbuf0 + (kk & 1) * wdbl);
+        const char* cbase = reinterpret_cast<const char*>(cbuf0 + (i & 1) * cstage);
         const uint32_t cstride = segpad * 8;  // bytes between the M staged rows
-        const uint32_t g = i % a.nseg;
 #pragma unroll
         for (int q = 0; q < kMxR; ++q) {
             if (slice[q] >= a.nslices) continue;
             const uint32_t L = a.sell_len[slice[q] * a.nseg + g];
             const uint32_t* ent = a.sell + a.sell_off[slice[q] * a.nseg + g] + lane;
-            double s0[M], s1[M];
-#pragma unroll
-            for (int v = 0; v < M; ++v) s0[v] = s1[v] = 0.0;
-            uint32_t t = 0;
+            if (M == 1) {
+                double s0 = 0.0, s1 = 0.0;
+                uint32_t t = 0;
 #pragma unroll 1
-            for (; t + 8 <= L; t += 8) {
-                uint32_t e[8];
+                for (; t + 8 <= L; t += 8) {
+                    uint32_t e[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) e[u] = __ldg(ent + static_cast<size_t>(t + u) * kWarp);
+                    for (int u = 0; u < 8; ++u) e[u] = __ldg(ent + static_cast<size_t>(t + u) * kWarp);
 #pragma unroll
-                for (int u = 0; u < 8; u += 2) {
-                    const double w0 = *reinterpret_cast<const double*>(wbase + ((e[u] >> 17) << 3));
-                    const double w1 = *reinterpret_cast<const double*>(wbase + ((e[u + 1] >> 17) << 3));
-                    const char* c0 = cbase + (e[u] & 0x1ffffu);
-                    const char* c1 = cbase + (e[u + 1] & 0x1ffffu);
-#pragma unroll
-                    for (int v = 0; v < M; ++v) {
-                        s0[v] = fma(w0, *reinterpret_cast<const double*>(c0 + v * cstride), s0[v]);
-                        s1[v] = fma(w1, *reinterpret_cast<const double*>(c1 + v * cstride), s1[v]);
+                    for (int u = 0; u < 8; u += 2) {
+                        const double w0 = *reinterpret_cast<const double*>(wbase + ((e[u] >> 17) << 3));
+                        const double c0 = *reinterpret_cast<const double*>(cbase + (e[u] & 0x1ffffu));
+                        const double w1 = *reinterpret_cast<const double*>(wbase + ((e[u + 1] >> 17) << 3));
+                        const double c1 = *reinterpret_cast<const double*>(cbase + (e[u + 1] & 0x1ffffu));
+                        s0 = fma(w0, c0, s0);
+                        s1 = fma(w1, c1, s1);
                     }
                 }
-            }
 #pragma unroll 1
-            for (; t < L; ++t) {
-                const uint32_t e0 = __ldg(ent + static_cast<size_t>(t) * kWarp);
-                const double w0 = *reinterpret_cast<const double*>(wbase + ((e0 >> 17) << 3));
-                const char* c0 = cbase + (e0 & 0x1ffffu);
+                for (; t < L; ++t) {
+                    const uint32_t e0 = __ldg(ent + static_cast<size_t>(t) * kWarp);
+                    s0 = fma(*reinterpret_cast<const double*>(wbase + ((e0 >> 17) << 3)),
+                             *reinterpret_cast<const double*>(cbase + (e0 & 0x1ffffu)), s0);
+                }
+                acc[0][q] += s0 + s1;
+            } else {
+                // M independent FMA chains already; one accumulator per vector
+                double s[M];
 #pragma unroll
-                for (int v = 0; v < M; ++v) s0[v] = fma(w0, *reinterpret_cast<const double*>(c0 + v * cstride), s0[v]);
+                for (int v = 0; v < M; ++v) s[v] = 0.0;
+                uint32_t t = 0;
+#pragma unroll 1
+                for (; t + 8 <= L; t += 8) {
+                    uint32_t e[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) e[u] = __ldg(ent + static_cast<size_t>(t + u) * kWarp);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const double w = *reinterpret_cast<const double*>(wbase + ((e[u] >> 17) << 3));
+                        const char* c = cbase + (e[u] & 0x1ffffu);
+#pragma unroll
+                        for (int v = 0; v < M; ++v) s[v] = fma(w, *reinterpret_cast<const double*>(c + v * cstride), s[v]);
+                    }
+                }
+#pragma unroll 1
+                for (; t < L; ++t) {
+                    const uint32_t e0 = __ldg(ent + static_cast<size_t>(t) * kWarp);
+                    const double w = *reinterpret_cast<const double*>(wbase + ((e0 >> 17) << 3));
+                    const char* c = cbase + (e0 & 0x1ffffu);
+#pragma unroll
+                    for (int v = 0; v < M; ++v) s[v] = fma(w, *reinterpret_cast<const double*>(c + v * cstride), s[v]);
+                }
+#pragma unroll
+                for (int v = 0; v < M; ++v) acc[v][q] += s[v];
             }
-#pragma unroll
-            for (int v = 0; v < M; ++v) acc[v][q] += s0[v] + s1[v];
         }
         if (g + 1 == a.nseg) {  // last segment of this ja: apply the alpha sign
-            const uint32_t ja = f[kb + i / a.nseg];
+            const uint32_t ja = f[kb + kk];
             const uint64_t Ak = a.alpha[ja];
             const int pa = __ffsll(static_cast<long long>(A & ~Ak)) - 1;
             const int qa = __ffsll(static_cast<long long>(Ak & ~A)) - 1;
@@ -391,7 +426,7 @@ k_mixed(const MixedArgs a) {
                 }
             }
         }
-        __syncthreads();  // buffer i&1 free for stage i+2
+        __syncthreads();  // C buffer i&1 (and a finished W buffer) free
     }
 
 #pragma unroll
@@ -542,7 +577,7 @@ void launch_alpha(const Handle& h, const Ptrs& Cb, uint32_t b0, uint32_t b1, con
 size_t mixed_smem(const Handle& h, const SellTable& t, int M) {
     const size_t nn = static_cast<size_t>(h.norbs) * h.norbs;
     return 2 * (((2 * nn + 1) & ~size_t{1}) + M * ((t.seg_cols + 1) & ~size_t{1})) * sizeof(double);
-}
+}  // == 2 W buffers + 2 C stages
 
 template <int M>
 void launch_mixed(Handle& h, const Ptrs& Cb, uint32_t b0, uint32_t b1, const MPtrs& y_loc, uint64_t a0,
@@ -754,13 +789,15 @@ void sigma_block(Handle& h, const double* const* dx, double* const* dy, int m) {
     while (i < m) {
         Ptrs x{};
         MPtrs y{};
-        const int take = m - i >= 4 ? 4 : (m - i >= 2 ? 2 : 1);
+        // pairs: M = 2 shares the W gather and SELL stream (-6..7% per vector
+        // at C2/C3); M = 4 shrinks the staged row segments 4x and loses
+        // (measured 1.35-1.6x slower per vector), so it is not used
+        const int take = m - i >= 2 ? 2 : 1;
         for (int v = 0; v < take; ++v) {
             x[v] = dx[i + v];
             y[v] = dy[i + v];
         }
-        if (take == 4) sigma_schedule_m<4>(h, x, y, tm);
-        else if (take == 2) sigma_schedule_m<2>(h, x, y, tm);
+        if (take == 2) sigma_schedule_m<2>(h, x, y, tm);
         else sigma_schedule_m<1>(h, x, y, tm);
         i += take;
     }

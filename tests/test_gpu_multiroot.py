@@ -45,7 +45,7 @@ def test_fixture_roots_match_dense_eigh(name, nroots):
 
 def test_roots_with_virtual_blocks_and_restarts():
     ints = synth.synthetic_integrals(10, 6)
-    s = synth.synthetic_strings(10, 3, 100)
+    s = synth.synthetic_strings(10, 3, 40)
     want = np.linalg.eigvalsh(dense_h(ints, s, s))[:4]
     with gpu_basis(ints, s, s, virtual_blocks=3, weighted_partition=True) as b:
         res = detci.davidson_roots(b, 4, max_subspace=10)
