@@ -21,6 +21,8 @@
 // block-local.
 #include <algorithm>
 #include <array>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "formulas.cuh"
@@ -192,6 +194,133 @@ k_samespin(const SameSpinArgs a, uint32_t chunk0) {
 #pragma unroll
     for (int q = 0; q < R; ++q) {
         const uint32_t c = col0 + q * kSSBlock;
+        if (kTail && c >= a.ncols) continue;
+        const size_t yi = static_cast<size_t>(r) * a.ldy + c;
+#pragma unroll
+        for (int vv = 0; vv < M; ++vv) {
+            if (a.accumulate) {
+                a.Y[vv][yi] += acc[vv][q];
+            } else if (a.diag) {
+                a.Y[vv][yi] = fma(a.diag[yi], a.Cself[vv][yi], acc[vv][q]);
+            } else {
+                a.Y[vv][yi] = acc[vv][q];
+            }
+        }
+    }
+}
+
+// Grouped variant: CTA = (8 consecutive output rows, one 32*R-column chunk),
+// one row per warp.  Consecutive rows share most of their helper-list
+// targets (sorted strings), and the warps walk their own sorted lists at
+// similar paces, so C[ja, chunk] lines fetched by one warp are re-read by the
+// others from L1 (simulated 45-59% L1 hits at C2) instead of L2, which bounds
+// the one-row-per-CTA kernel (84.6% L2 throughput, 98% L2 hits, ncu C2).
+constexpr int kGW = 8;        // warps = rows per CTA
+constexpr int kGStage = 32;   // entries staged per warp (6 KB per CTA)
+
+template <bool kTail, int M>
+__global__ void __launch_bounds__(kGW * kWarp, 4)
+k_samespin_g(const SameSpinArgs a, uint32_t chunk0, uint32_t ngroups) {
+    constexpr int R = SSR<M>::value;
+    __shared__ uint32_t s_ja[kGW][kGStage];
+    __shared__ double s_v[kGW][kGStage];
+    __shared__ uint64_t s_m[kGW][kGStage];
+    __shared__ uint32_t s_ab[kGW][kGStage];
+
+    const uint32_t warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+    const uint32_t group = blockIdx.x % ngroups;
+    const uint32_t chunk = chunk0 + blockIdx.x / ngroups;
+    const uint32_t r = group * kGW + warp;
+    if (r >= a.nrows) return;   // no CTA-wide barriers below
+    const uint32_t row = a.row0 + r;
+    const uint32_t col0 = chunk * (kWarp * R) + lane;
+
+    uint32_t col[R];
+    uint32_t slo[R], shi[R];
+    double acc[M][R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+        const uint32_t c = col0 + q * kWarp;
+        col[q] = kTail ? min(c, a.ncols - 1) : c;
+        const uint64_t sp = a.spec[col[q]];
+        slo[q] = static_cast<uint32_t>(sp);
+        shi[q] = static_cast<uint32_t>(sp >> 32);
+#pragma unroll
+        for (int v = 0; v < M; ++v) acc[v][q] = 0.0;
+    }
+
+    uint64_t rb = 0, re = 0;
+    if (lane < 2) {
+        const uint64_t o = a.off[lane][row];
+        const uint32_t n = a.len[lane][row];
+        const uint32_t* f = a.flat[lane] + o;
+        rb = o + (a.j0 == 0 ? 0 : lower_bound_u32(f, n, a.j0));
+        re = o + lower_bound_u32(f, n, a.j1);
+    }
+    uint32_t* sja = s_ja[warp];
+    double* sv = s_v[warp];
+    uint64_t* sm = s_m[warp];
+    uint32_t* sab = s_ab[warp];
+
+#pragma unroll 1
+    for (int kind = 0; kind < 2; ++kind) {
+        const uint64_t kb = __shfl_sync(0xffffffffu, rb, kind), ke = __shfl_sync(0xffffffffu, re, kind);
+#pragma unroll 1
+        for (uint64_t k0 = kb; k0 < ke; k0 += kGStage) {
+            const int cnt = static_cast<int>(min(static_cast<uint64_t>(kGStage), ke - k0));
+            __syncwarp();
+            for (int t = lane; t < cnt; t += kWarp) {
+                sja[t] = a.flat[kind][k0 + t] - a.c_row0;
+                sv[t] = a.pv[kind][k0 + t];
+                sm[t] = a.pm[kind][k0 + t];
+                if (kind == 0) sab[t] = a.pab[k0 + t];
+            }
+            __syncwarp();
+            if (kind == 0) {
+#pragma unroll 2
+                for (int e = 0; e < cnt; ++e) {
+                    const size_t rowoff = static_cast<size_t>(sja[e]) * a.ldc;
+                    const uint32_t ab = sab[e];
+                    const double* jrow = a.J + static_cast<size_t>(ab & 0x7fffffffu) * a.ldj;
+                    const double v = sv[e];
+                    const uint64_t m = sm[e];
+                    const uint32_t mlo = static_cast<uint32_t>(m), mhi = static_cast<uint32_t>(m >> 32);
+                    const uint32_t jsign = ab & 0x80000000u;
+#pragma unroll
+                    for (int q = 0; q < R; ++q) {
+                        const uint32_t cq = kTail ? col[q] : col0 + q * kWarp;
+                        const double val = v + xor_sign(__ldg(jrow + cq), jsign);
+                        const uint32_t sg = spectator_sign(slo[q], shi[q], mlo, mhi);
+#pragma unroll
+                        for (int vv = 0; vv < M; ++vv)
+                            acc[vv][q] = fma(val, xor_sign(__ldg(a.C[vv] + rowoff + cq), sg), acc[vv][q]);
+                    }
+                }
+            } else {
+#pragma unroll 4
+                for (int e = 0; e < cnt; ++e) {
+                    const size_t rowoff = static_cast<size_t>(sja[e]) * a.ldc + (kTail ? 0 : col0);
+                    const double v = sv[e];
+                    const uint64_t m = sm[e];
+                    const uint32_t mlo = static_cast<uint32_t>(m), mhi = static_cast<uint32_t>(m >> 32);
+#pragma unroll
+                    for (int q = 0; q < R; ++q) {
+                        const uint32_t sg = spectator_sign(slo[q], shi[q], mlo, mhi);
+#pragma unroll
+                        for (int vv = 0; vv < M; ++vv) {
+                            const double* base = a.C[vv] + rowoff;
+                            const double c = __ldg(kTail ? base + col[q] : base + q * kWarp);
+                            acc[vv][q] = fma(v, xor_sign(c, sg), acc[vv][q]);
+                        }
+                    }
+                }
+            }
+        }
+    }
+
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+        const uint32_t c = col0 + q * kWarp;
         if (kTail && c >= a.ncols) continue;
         const size_t yi = static_cast<size_t>(r) * a.ldy + c;
 #pragma unroll
@@ -521,9 +650,42 @@ struct PhaseTimer {
 using Ptrs = std::array<const double*, kMaxM>;
 using MPtrs = std::array<double*, kMaxM>;
 
+// DETCI_SAMESPIN=grouped selects the 8-rows-per-CTA kernel.  Measured on
+// B200: 51% L1 hits and L2 load down from 85% to 24%, but the kernel is then
+// issue/latency-bound and runs level with the row kernel (C2 28.5 vs 27 ms,
+// C3 157 vs 165 ms), so the row kernel stays the default.
+bool grouped_samespin() {
+    static const int mode = [] {
+        const char* e = std::getenv("DETCI_SAMESPIN");
+        return (e && std::string(e) == "grouped") ? 1 : 0;
+    }();
+    return mode == 1;
+}
+
 template <int M>
 void launch_samespin(const SameSpinArgs& s, cudaStream_t st) {
     if (s.nrows == 0 || s.ncols == 0) return;
+    if (grouped_samespin()) {
+        constexpr uint32_t kChunk = kWarp * SSR<M>::value;
+        const uint64_t full = s.ncols / kChunk;
+        const bool tail = s.ncols % kChunk != 0;
+        const uint32_t ngroups = (s.nrows + kGW - 1) / kGW;
+        static bool configured = false;
+        if (!configured) {  // favour L1 over shared memory (the kernel uses ~24 KB)
+            CUDA_CHECK(cudaFuncSetAttribute(k_samespin_g<false, M>, cudaFuncAttributePreferredSharedMemoryCarveout, 10));
+            CUDA_CHECK(cudaFuncSetAttribute(k_samespin_g<true, M>, cudaFuncAttributePreferredSharedMemoryCarveout, 10));
+            configured = true;
+        }
+        if (full) {
+            k_samespin_g<false, M><<<static_cast<unsigned>(full * ngroups), kGW * kWarp, 0, st>>>(s, 0, ngroups);
+            CUDA_LAUNCH_CHECK();
+        }
+        if (tail) {
+            k_samespin_g<true, M><<<ngroups, kGW * kWarp, 0, st>>>(s, static_cast<uint32_t>(full), ngroups);
+            CUDA_LAUNCH_CHECK();
+        }
+        return;
+    }
     constexpr uint32_t kChunk = kSSBlock * SSR<M>::value;
     const uint64_t full = s.ncols / kChunk;
     const bool tail = s.ncols % kChunk != 0;
