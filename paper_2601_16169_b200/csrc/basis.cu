@@ -312,12 +312,24 @@ void build_mixed_sell(Handle& h, SellTable& st, int M) {
     const uint32_t nb = static_cast<uint32_t>(b.n);
     const int n = h.norbs;
     const uint32_t nn = static_cast<uint32_t>(n * n);
-    // two stage buffers of [+-W | M C-row segments] must fit in 220 KB of smem
+    // Shared memory per CTA (<= 220 KB): two +-W buffers plus either two
+    // double-buffered C stages of M row segments, or -- preferred, because
+    // segmenting a row splits every SELL row and costs ~18% fill -- one stage
+    // holding the M rows in as few segments as fit.
     const uint32_t wdbl = (2 * nn + 1) & ~1u;
-    const uint32_t max_seg = std::min<uint32_t>(16000, ((220u * 1024 / 8 / 2 - wdbl) / M) & ~1u);
+    const uint32_t budget = 220u * 1024 / 8 - 2 * wdbl;           // doubles for C stages
+    const uint32_t single_seg = std::min<uint32_t>(32766, (budget / M) & ~1u);   // 18-bit byte offsets
+    const uint32_t double_seg = std::min<uint32_t>(16000, (budget / 2 / M) & ~1u);
+    const uint32_t nseg_single = (nb + single_seg - 1) / single_seg;
+    const uint32_t nseg_double = (nb + double_seg - 1) / double_seg;
+    st.double_buffer = nseg_double <= nseg_single;   // overlap only when it costs no extra segments
+    const uint32_t max_seg = st.double_buffer ? double_seg : single_seg;
     st.nseg = (nb + max_seg - 1) / max_seg;
     if (st.nseg > 16) fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: more than 16 column segments");
+    if (2 * nn >= (1u << 14)) fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: +-W index exceeds 14 bits");
     st.seg_cols = (nb + st.nseg - 1) / st.nseg;
+    if (static_cast<uint64_t>(st.seg_cols) * 8 >= (1u << 18))
+        fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: row segment exceeds the 18-bit entry offset");
     h.nslices = (nb + kWarp - 1) / kWarp;
     const uint32_t nseg = st.nseg, seg_cols = st.seg_cols, nslices = h.nslices;
 

@@ -90,10 +90,10 @@ DG_HD PairEntry make_pair_entry(int ch, int kind, uint64_t si, uint64_t sj, cons
 }
 
 // Packed beta-single entry for the mixed term (SELL-32 table):
-//   bits 0..16  byte offset of C[ja, jb] inside the staged row segment
-//               (jb relative to its segment, times 8; segments <= 16383 cols)
-//   bits 17..31 index into the +-W table: cd + sbit * n^2 with cd = pb*n+qb
-//               and sbit = parity of popc(B_ib & open(pb, qb))
+//   bits 0..17  byte offset of C[ja, jb] inside the staged row segment
+//               (jb relative to its segment, times 8; segments <= 32767 cols)
+//   bits 18..31 index into the +-W table: cd + sbit * n^2 with cd = pb*n+qb
+//               and sbit = parity of popc(B_ib & open(pb, qb)) (< 2*64^2)
 // so the kernel needs one AND and one shift to address both gathers and the
 // sign of the beta half is folded into which half of +-W is read.
 struct MixedMove {
@@ -111,7 +111,7 @@ DG_HD MixedMove mixed_move(uint64_t b_bra, uint64_t b_ket, int n) {
 }
 
 DG_HD uint32_t encode_mixed_entry(uint32_t jb_local, uint32_t w_index) {
-    return (jb_local * 8u) | (w_index << 17);
+    return (jb_local * 8u) | (w_index << 18);
 }
 
 // W_ja[cd] of the mixed term: (pa qa | c d) * (-1)^{popc(A'_ja & Mbeta(c,d))}

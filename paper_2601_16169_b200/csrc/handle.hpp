@@ -67,6 +67,7 @@ struct SellTable {
     DevBuf<uint64_t> off;              // [slice * nseg + seg]
     DevBuf<uint32_t> len;              // [slice * nseg + seg]
     uint32_t seg_cols = 0, nseg = 0;
+    bool double_buffer = true;         // C stages double-buffered (else one)
     bool built = false;
 };
 

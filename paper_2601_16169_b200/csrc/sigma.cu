@@ -385,7 +385,10 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
-template <int M>
+// kDB: C stages double-buffered (row segments stream in under the compute of
+// the previous stage); otherwise one C stage, refilled after a barrier (used
+// when a whole row fits, which avoids segmenting the SELL table).
+template <int M, bool kDB>
 __global__ void __launch_bounds__(kMxBlock, 1)
 k_mixed(const MixedArgs a) {
     constexpr int kMxR = MxR<M>::value;
@@ -433,7 +436,7 @@ k_mixed(const MixedArgs a) {
         const uint32_t ja = f[kb + kk];
         const uint32_t segw = min(a.seg_cols, a.nb - g * a.seg_cols);
         const size_t src_off = static_cast<size_t>(ja - a.c_row0) * a.ldc + g * a.seg_cols;
-        double* cb = cbuf0 + (i & 1) * cstage;
+        double* cb = cbuf0 + (kDB ? (i & 1) * cstage : 0);
 #pragma unroll
         for (int v = 0; v < M; ++v) {
             double* crow = cb + v * segpad;
@@ -460,22 +463,27 @@ k_mixed(const MixedArgs a) {
         }
     };
 
-    if (nstages > 0) issue(0);
+    if (kDB && nstages > 0) issue(0);
 #pragma unroll 1
     for (uint32_t i = 0; i < nstages; ++i) {
-        if (i + 1 < nstages) {
-            // C buffer (i+1)&1 was released by the barrier ending stage i-1;
-            // W buffer ((i+1)/nseg)&1 differs from the one in use when the
-            // next stage starts a new ja (its previous user finished 2 ja ago)
-            issue(i + 1);
-            cp_async_wait_prev();  // stage i's rows have landed
+        if (kDB) {
+            if (i + 1 < nstages) {
+                // C buffer (i+1)&1 was released by the barrier ending stage
+                // i-1; W buffer ((i+1)/nseg)&1 differs from the one in use
+                // when the next stage starts a new ja
+                issue(i + 1);
+                cp_async_wait_prev();  // stage i's rows have landed
+            } else {
+                cp_async_wait_all();
+            }
         } else {
+            issue(i);  // the barrier ending stage i-1 released the C buffer
             cp_async_wait_all();
         }
         __syncthreads();
         const uint32_t kk = i / a.nseg, g = i % a.nseg;
         const char* wbase = reinterpret_cast<const char*>(wbuf0 + (kk & 1) * wdbl);
-        const char* cbase = reinterpret_cast<const char*>(cbuf0 + (i & 1) * cstage);
+        const char* cbase = reinterpret_cast<const char*>(cbuf0 + (kDB ? (i & 1) * cstage : 0));
         const uint32_t cstride = segpad * 8;  // bytes between the M staged rows
 #pragma unroll
         for (int q = 0; q < kMxR; ++q) {
@@ -492,10 +500,10 @@ k_mixed(const MixedArgs a) {
                     for (int u = 0; u < 8; ++u) e[u] = __ldg(ent + static_cast<size_t>(t + u) * kWarp);
 #pragma unroll
                     for (int u = 0; u < 8; u += 2) {
-                        const double w0 = *reinterpret_cast<const double*>(wbase + ((e[u] >> 17) << 3));
-                        const double c0 = *reinterpret_cast<const double*>(cbase + (e[u] & 0x1ffffu));
-                        const double w1 = *reinterpret_cast<const double*>(wbase + ((e[u + 1] >> 17) << 3));
-                        const double c1 = *reinterpret_cast<const double*>(cbase + (e[u + 1] & 0x1ffffu));
+                        const double w0 = *reinterpret_cast<const double*>(wbase + ((e[u] >> 18) << 3));
+                        const double c0 = *reinterpret_cast<const double*>(cbase + (e[u] & 0x3ffffu));
+                        const double w1 = *reinterpret_cast<const double*>(wbase + ((e[u + 1] >> 18) << 3));
+                        const double c1 = *reinterpret_cast<const double*>(cbase + (e[u + 1] & 0x3ffffu));
                         s0 = fma(w0, c0, s0);
                         s1 = fma(w1, c1, s1);
                     }
@@ -503,8 +511,8 @@ k_mixed(const MixedArgs a) {
 #pragma unroll 1
                 for (; t < L; ++t) {
                     const uint32_t e0 = __ldg(ent + static_cast<size_t>(t) * kWarp);
-                    s0 = fma(*reinterpret_cast<const double*>(wbase + ((e0 >> 17) << 3)),
-                             *reinterpret_cast<const double*>(cbase + (e0 & 0x1ffffu)), s0);
+                    s0 = fma(*reinterpret_cast<const double*>(wbase + ((e0 >> 18) << 3)),
+                             *reinterpret_cast<const double*>(cbase + (e0 & 0x3ffffu)), s0);
                 }
                 acc[0][q] += s0 + s1;
             } else {
@@ -520,8 +528,8 @@ k_mixed(const MixedArgs a) {
                     for (int u = 0; u < 8; ++u) e[u] = __ldg(ent + static_cast<size_t>(t + u) * kWarp);
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
-                        const double w = *reinterpret_cast<const double*>(wbase + ((e[u] >> 17) << 3));
-                        const char* c = cbase + (e[u] & 0x1ffffu);
+                        const double w = *reinterpret_cast<const double*>(wbase + ((e[u] >> 18) << 3));
+                        const char* c = cbase + (e[u] & 0x3ffffu);
 #pragma unroll
                         for (int v = 0; v < M; ++v) s[v] = fma(w, *reinterpret_cast<const double*>(c + v * cstride), s[v]);
                     }
@@ -529,8 +537,8 @@ k_mixed(const MixedArgs a) {
 #pragma unroll 1
                 for (; t < L; ++t) {
                     const uint32_t e0 = __ldg(ent + static_cast<size_t>(t) * kWarp);
-                    const double w = *reinterpret_cast<const double*>(wbase + ((e0 >> 17) << 3));
-                    const char* c = cbase + (e0 & 0x1ffffu);
+                    const double w = *reinterpret_cast<const double*>(wbase + ((e0 >> 18) << 3));
+                    const char* c = cbase + (e0 & 0x3ffffu);
 #pragma unroll
                     for (int v = 0; v < M; ++v) s[v] = fma(w, *reinterpret_cast<const double*>(c + v * cstride), s[v]);
                 }
@@ -738,8 +746,9 @@ void launch_alpha(const Handle& h, const Ptrs& Cb, uint32_t b0, uint32_t b1, con
 
 size_t mixed_smem(const Handle& h, const SellTable& t, int M) {
     const size_t nn = static_cast<size_t>(h.norbs) * h.norbs;
-    return 2 * (((2 * nn + 1) & ~size_t{1}) + M * ((t.seg_cols + 1) & ~size_t{1})) * sizeof(double);
-}  // == 2 W buffers + 2 C stages
+    const size_t w = (2 * nn + 1) & ~size_t{1}, c = M * ((t.seg_cols + 1) & ~size_t{1});
+    return (2 * w + (t.double_buffer ? 2 : 1) * c) * sizeof(double);   // 2 W buffers + 1 or 2 C stages
+}
 
 template <int M>
 void launch_mixed(Handle& h, const Ptrs& Cb, uint32_t b0, uint32_t b1, const MPtrs& y_loc, uint64_t a0,
@@ -775,14 +784,22 @@ void launch_mixed(Handle& h, const Ptrs& Cb, uint32_t b0, uint32_t b1, const MPt
     m.norbs = h.norbs;
     if (m.nrows == 0) return;
     const size_t smem = mixed_smem(h, t, M);
-    static size_t configured[kMaxM + 1] = {0};
-    if (smem > configured[M]) {
-        CUDA_CHECK(cudaFuncSetAttribute(k_mixed<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem)));
-        configured[M] = smem;
+    static size_t configured[2][kMaxM + 1] = {};
+    const int db = t.double_buffer ? 1 : 0;
+    if (smem > configured[db][M]) {
+        if (db)
+            CUDA_CHECK(cudaFuncSetAttribute(k_mixed<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(smem)));
+        else
+            CUDA_CHECK(cudaFuncSetAttribute(k_mixed<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(smem)));
+        configured[db][M] = smem;
     }
     const uint64_t grid = static_cast<uint64_t>(m.nrows) * m.nparts;
-    k_mixed<M><<<static_cast<unsigned>(grid), kMxBlock, smem, h.stream>>>(m);
+    if (db)
+        k_mixed<M, true><<<static_cast<unsigned>(grid), kMxBlock, smem, h.stream>>>(m);
+    else
+        k_mixed<M, false><<<static_cast<unsigned>(grid), kMxBlock, smem, h.stream>>>(m);
     CUDA_LAUNCH_CHECK();
 }
 
