@@ -341,6 +341,25 @@ def run_gpu_arm(args):
                "s_per_iter": res.seconds / max(1, len(res.iterations)), "energy": res.energy,
                "sigma_share": sum(i.matvec_seconds for i in res.iterations) / res.seconds}
 
+    # ---- full Davidson to convergence at C1 ("full-Davidson
+    # wall time at C1"), energy against the reference pipeline's golden
+    dav_c1 = None
+    if args.davidson and world == 1:
+        ints1, a1, b1 = synth.synthetic_system("C1")
+        with detci.GpuBasis(ints1.norbs, a1, b1, ints1.core, ints1.h1, ints1.eri,
+                            detci.BasisOptions(device=local_rank)) as basis1:
+            t1 = time.time()
+            r1 = detci.davidson_solve(basis1, want_vector=False)
+            wall1 = time.time() - t1
+        ref_e = None
+        gpath = ROOT / "tests" / "golden" / "golden.json"
+        if gpath.exists():
+            ref_e = json.loads(gpath.read_text()).get("C1", {}).get("energy")
+        dav_c1 = {"status": r1.status, "iterations": len(r1.iterations), "seconds": wall1, "energy": r1.energy,
+                  "reference_energy": ref_e, "abs_err_vs_reference": abs(r1.energy - ref_e) if ref_e else None,
+                  "reference_seconds_8core_container": json.loads(gpath.read_text()).get("C1", {}).get("davidson_seconds")
+                  if gpath.exists() else None}
+
     # ---- CPU baseline (reference on this host), rank 0 at N=1 only
     cpu = None
     if rank == 0 and world == 1 and args.cpu_baseline:
@@ -375,6 +394,7 @@ def run_gpu_arm(args):
             "gpu_launches": launches,
             "clocks": clocks,
             "davidson": dav,
+            "davidson_c1_full": dav_c1,
             "blocked_sigma": blocked,
         }
         print(json.dumps(line), flush=True)
