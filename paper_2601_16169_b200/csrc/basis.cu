@@ -3,6 +3,7 @@
 // basis.cpp:78-148; generate_singles/doubles, connectivity.cpp:64-122).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -316,10 +317,14 @@ void build_mixed_sell(Handle& h, SellTable& st, int M) {
     // double-buffered C stages of M row segments, or -- preferred, because
     // segmenting a row splits every SELL row and costs ~18% fill -- one stage
     // holding the M rows in as few segments as fit.
+    // DETCI_MIXED_MAX_SEG caps the segment width (tests force multi-segment
+    // tables on small systems with it).
+    uint32_t cap = 32766;   // 18-bit byte offsets
+    if (const char* e = std::getenv("DETCI_MIXED_MAX_SEG")) cap = std::max(2, std::atoi(e)) & ~1u;
     const uint32_t wdbl = (2 * nn + 1) & ~1u;
     const uint32_t budget = 220u * 1024 / 8 - 2 * wdbl;           // doubles for C stages
-    const uint32_t single_seg = std::min<uint32_t>(32766, (budget / M) & ~1u);   // 18-bit byte offsets
-    const uint32_t double_seg = std::min<uint32_t>(16000, (budget / 2 / M) & ~1u);
+    const uint32_t single_seg = std::min<uint32_t>(cap, (budget / M) & ~1u);
+    const uint32_t double_seg = std::min<uint32_t>(std::min<uint32_t>(16000, cap), (budget / 2 / M) & ~1u);
     const uint32_t nseg_single = (nb + single_seg - 1) / single_seg;
     const uint32_t nseg_double = (nb + double_seg - 1) / double_seg;
     st.double_buffer = nseg_double <= nseg_single;   // overlap only when it costs no extra segments

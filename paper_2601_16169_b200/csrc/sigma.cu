@@ -93,8 +93,9 @@ __device__ __forceinline__ double xor_sign(double x, uint32_t sign31) {
 
 // kTail: the CTA's column chunk crosses ncols, so column indices are clamped
 // (loads stay in bounds, stores are masked); full chunks use one base
-// pointer per entry with immediate offsets.
-template <bool kTail, int M>
+// pointer per entry with immediate offsets.  kNarrow: norbs <= 32, strings
+// and masks fit 32 bits and the parity is one AND + POPC.
+template <bool kTail, int M, bool kNarrow>
 __global__ void __launch_bounds__(kSSBlock)
 k_samespin(const SameSpinArgs a, uint32_t chunk0) {
     constexpr int R = SSR<M>::value;
@@ -163,7 +164,7 @@ k_samespin(const SameSpinArgs a, uint32_t chunk0) {
                     for (int q = 0; q < R; ++q) {
                         const uint32_t cq = kTail ? col[q] : col0 + q * kSSBlock;
                         const double val = v + xor_sign(__ldg(jrow + cq), jsign);
-                        const uint32_t sg = spectator_sign(slo[q], shi[q], mlo, mhi);
+                        const uint32_t sg = (kNarrow ? (__popc(slo[q] & mlo) << 31) : spectator_sign(slo[q], shi[q], mlo, mhi));
 #pragma unroll
                         for (int vv = 0; vv < M; ++vv)
                             acc[vv][q] = fma(val, xor_sign(__ldg(a.C[vv] + rowoff + cq), sg), acc[vv][q]);
@@ -178,7 +179,7 @@ k_samespin(const SameSpinArgs a, uint32_t chunk0) {
                     const uint32_t mlo = static_cast<uint32_t>(m), mhi = static_cast<uint32_t>(m >> 32);
 #pragma unroll
                     for (int q = 0; q < R; ++q) {
-                        const uint32_t sg = spectator_sign(slo[q], shi[q], mlo, mhi);
+                        const uint32_t sg = (kNarrow ? (__popc(slo[q] & mlo) << 31) : spectator_sign(slo[q], shi[q], mlo, mhi));
 #pragma unroll
                         for (int vv = 0; vv < M; ++vv) {
                             const double* base = a.C[vv] + rowoff;
@@ -671,7 +672,7 @@ bool grouped_samespin() {
 }
 
 template <int M>
-void launch_samespin(const SameSpinArgs& s, cudaStream_t st) {
+void launch_samespin(const SameSpinArgs& s, cudaStream_t st, bool narrow) {
     if (s.nrows == 0 || s.ncols == 0) return;
     if (grouped_samespin()) {
         constexpr uint32_t kChunk = kWarp * SSR<M>::value;
@@ -698,11 +699,17 @@ void launch_samespin(const SameSpinArgs& s, cudaStream_t st) {
     const uint64_t full = s.ncols / kChunk;
     const bool tail = s.ncols % kChunk != 0;
     if (full) {
-        k_samespin<false, M><<<static_cast<unsigned>(full * s.nrows), kSSBlock, 0, st>>>(s, 0);
+        if (narrow)
+            k_samespin<false, M, true><<<static_cast<unsigned>(full * s.nrows), kSSBlock, 0, st>>>(s, 0);
+        else
+            k_samespin<false, M, false><<<static_cast<unsigned>(full * s.nrows), kSSBlock, 0, st>>>(s, 0);
         CUDA_LAUNCH_CHECK();
     }
     if (tail) {
-        k_samespin<true, M><<<s.nrows, kSSBlock, 0, st>>>(s, static_cast<uint32_t>(full));
+        if (narrow)
+            k_samespin<true, M, true><<<s.nrows, kSSBlock, 0, st>>>(s, static_cast<uint32_t>(full));
+        else
+            k_samespin<true, M, false><<<s.nrows, kSSBlock, 0, st>>>(s, static_cast<uint32_t>(full));
         CUDA_LAUNCH_CHECK();
     }
 }
@@ -741,7 +748,7 @@ void launch_alpha(const Handle& h, const Ptrs& Cb, uint32_t b0, uint32_t b1, con
     fill_lists(s, h.ch[0]);
     s.diag = first ? h.diag.p + (a0 - h.a0) * h.nb() : nullptr;
     s.accumulate = first ? 0 : 1;
-    launch_samespin<M>(s, h.stream);
+    launch_samespin<M>(s, h.stream, h.norbs <= 32);
 }
 
 size_t mixed_smem(const Handle& h, const SellTable& t, int M) {
@@ -844,7 +851,7 @@ void beta_term(Handle& h, const Ptrs& x_loc, uint64_t a0, uint64_t a1, PhaseTime
     s.ldj = h.na();
     fill_lists(s, h.ch[1]);
     s.accumulate = 0;
-    launch_samespin<M>(s, h.stream);
+    launch_samespin<M>(s, h.stream, h.norbs <= 32);
     tm.end(id);
 }
 

@@ -157,3 +157,31 @@ def test_blocked_sigma_c1_rows():
         r = rows["rows"].astype(np.int64)
         for i, scale in enumerate((1.0, 2.0, -1.0, 0.5)):
             assert rel_diff(Y[i].reshape(len(a), -1)[r], scale * rows["sigma_rows"]) <= 1e-12
+
+
+@pytest.mark.parametrize("max_seg", [300, 128])
+def test_segmented_mixed_rows_c1(max_seg, monkeypatch):
+    """Multi-segment C rows (per-segment slot order + shared accumulator, as at
+    C4), forced on C1 with DETCI_MIXED_MAX_SEG, against the reference rows;
+    single and paired (blocked) vectors."""
+    monkeypatch.setenv("DETCI_MIXED_MAX_SEG", str(max_seg))
+    rows = np.load(GOLDEN / "rows_C1.npz")
+    ints, a, bb = synth.synthetic_system("C1")
+    with gpu_basis(ints, a, bb) as b:
+        x = synth.random_vector(b.dimension(), 11)
+        y = detci.matvec(b, x)
+        r = rows["rows"].astype(np.int64)
+        assert rel_diff(y.reshape(len(a), -1)[r], rows["sigma_rows"]) <= 1e-12
+        Y = detci.matvec_block(b, np.stack([x, -2.0 * x, x]))
+        for i, scale in enumerate((1.0, -2.0, 1.0)):
+            assert rel_diff(Y[i], scale * y) <= 1e-12
+
+
+def test_segmented_virtual_blocks(monkeypatch):
+    monkeypatch.setenv("DETCI_MIXED_MAX_SEG", "64")
+    ints = synth.synthetic_integrals(12, 8)
+    s = synth.synthetic_strings(12, 4, 200)
+    x = synth.random_vector(len(s) ** 2, 3)
+    d = np.load(GOLDEN / "synthetic_s12.npz")
+    with gpu_basis(ints, s, s, virtual_blocks=3, weighted_partition=True) as b:
+        assert rel_diff(detci.matvec(b, synth.random_vector(len(s) ** 2, 11)), d["sigma11"]) <= 1e-12
