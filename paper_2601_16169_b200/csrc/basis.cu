@@ -131,21 +131,42 @@ k_scan_offsets(const uint32_t* __restrict__ len, uint64_t* __restrict__ off, uin
     if (t == 1023) off[n] = sums[1023];
 }
 
+// Transpose positions of the alpha singles lists (scatter mixed term):
+// tpos[off[ja] + k] = index of ja in the list of ia = flat[off[ja] + k]
+// (singles are mutual, so it exists).
+__global__ void k_tpos(const uint32_t* __restrict__ flat, const uint64_t* __restrict__ off,
+                       const uint32_t* __restrict__ len, uint32_t n, uint32_t* __restrict__ tpos) {
+    const uint32_t ja = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
+    const int lane = threadIdx.x % kWarp;
+    if (ja >= n) return;
+    const uint64_t o = off[ja];
+    for (uint32_t k = lane; k < len[ja]; k += kWarp) {
+        const uint32_t ia = flat[o + k];
+        const uint32_t* f = flat + off[ia];
+        uint32_t lo = 0, hi = len[ia];
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (f[mid] < ja) lo = mid + 1;
+            else hi = mid;
+        }
+        tpos[o + k] = lo;
+    }
+}
+
 // Same-spin pair tables, one warp per source row, lanes over entries.
-__global__ void k_pair_tables(int ch, int kind, const uint64_t* __restrict__ s, uint32_t n,
+__global__ void k_pair_tables(int kind, const uint64_t* __restrict__ s, uint32_t n,
                               const uint32_t* __restrict__ flat, const uint64_t* __restrict__ off,
                               const uint32_t* __restrict__ len, const double* __restrict__ h1,
                               const double* __restrict__ eri, int norbs, double* __restrict__ pv,
-                              uint64_t* __restrict__ pmask, uint32_t* __restrict__ pab) {
+                              uint32_t* __restrict__ pab) {
     const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
     const int lane = threadIdx.x % kWarp;
     if (i >= n) return;
     const uint64_t si = s[i];
     const uint64_t o = off[i];
     for (uint32_t k = lane; k < len[i]; k += kWarp) {
-        const PairEntry e = make_pair_entry(ch, kind, si, s[flat[o + k]], h1, eri, norbs);
+        const PairEntry e = make_pair_entry(kind, si, s[flat[o + k]], h1, eri, norbs);
         pv[o + k] = e.v;
-        pmask[o + k] = e.mask;
         if (kind == 0) pab[o + k] = e.ab_sign;
     }
 }
@@ -278,12 +299,11 @@ void build_pair_tables(Handle& h, int c) {
     for (int k = 0; k < 2; ++k) {
         const size_t m = std::max<uint64_t>(t.nflat[k], 1);
         t.pv[k].alloc(m);
-        t.pmask[k].alloc(m);
         if (k == 0) t.pab.alloc(m);
         const unsigned grid = (n * kWarp + 255) / 256;
-        k_pair_tables<<<grid, 256, 0, h.stream>>>(c, k, t.strings.p, n, t.flat[k].p,
+        k_pair_tables<<<grid, 256, 0, h.stream>>>(k, t.strings.p, n, t.flat[k].p,
                                                   t.offset[k].p, t.len[k].p, h.d_h1.p, h.d_eri.p,
-                                                  h.norbs, t.pv[k].p, t.pmask[k].p, t.pab.p);
+                                                  h.norbs, t.pv[k].p, t.pab.p);
         CUDA_LAUNCH_CHECK();
     }
     const uint32_t ntri = static_cast<uint32_t>(h.norbs * (h.norbs - 1) / 2);
@@ -308,7 +328,11 @@ void build_pair_tables(Handle& h, int c) {
 //    C[ja, jb]); padding entries point at a zero of W and reuse a
 //    C address already read in that step (broadcast).  Simulated on C2 this
 //    cuts shared-memory wavefronts per element step from 9.2 to 5.6.
-void build_mixed_sell(Handle& h, SellTable& st, int M) {
+//  * format 2 (scatter kernel, k_mixed_scatter): the same slots, segments
+//    and schedule, but the entry carries cd and the beta sign separately
+//    (encode_scatter_entry) because the kernel reads V[k][cd] for kScatterK
+//    output rows per C gather; the schedule weights V-bank conflicts double.
+void build_mixed_sell(Handle& h, SellTable& st, int M, int format) {
     ChannelTables& b = h.ch[1];
     const uint32_t nb = static_cast<uint32_t>(b.n);
     const int n = h.norbs;
@@ -322,16 +346,21 @@ void build_mixed_sell(Handle& h, SellTable& st, int M) {
     uint32_t cap = 32766;   // 18-bit byte offsets
     if (const char* e = std::getenv("DETCI_MIXED_MAX_SEG")) cap = std::max(2, std::atoi(e)) & ~1u;
     const uint32_t wdbl = (2 * nn + 1) & ~1u;
-    const uint32_t budget = 220u * 1024 / 8 - 2 * wdbl;           // doubles for C stages
+    const uint32_t budget = format == 2 ? kScatterSmem / 8 - kScatterK * scatter_vpitch(n)
+                                        : 220u * 1024 / 8 - 2 * wdbl;   // doubles for C stages
     const uint32_t single_seg = std::min<uint32_t>(cap, (budget / M) & ~1u);
     const uint32_t double_seg = std::min<uint32_t>(std::min<uint32_t>(16000, cap), (budget / 2 / M) & ~1u);
     const uint32_t nseg_single = (nb + single_seg - 1) / single_seg;
     const uint32_t nseg_double = (nb + double_seg - 1) / double_seg;
-    st.double_buffer = nseg_double <= nseg_single;   // overlap only when it costs no extra segments
+    // overlap only when it costs no extra segments (the scatter kernel
+    // stages one row per CTA: single buffer)
+    st.double_buffer = format == 1 && nseg_double <= nseg_single;
+    st.format = format;
     const uint32_t max_seg = st.double_buffer ? double_seg : single_seg;
     st.nseg = (nb + max_seg - 1) / max_seg;
     if (st.nseg > 16) fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: more than 16 column segments");
     if (2 * nn >= (1u << 14)) fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: +-W index exceeds 14 bits");
+    const int wv = format == 2 ? 2 : 1;   // weight of a V/W bank conflict in the schedule
     st.seg_cols = (nb + st.nseg - 1) / st.nseg;
     if (static_cast<uint64_t>(st.seg_cols) * 8 >= (1u << 18))
         fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: row segment exceeds the 18-bit entry offset");
@@ -369,7 +398,8 @@ void build_mixed_sell(Handle& h, SellTable& st, int M) {
 
     #pragma omp parallel for schedule(dynamic, 4)
     for (int64_t sl = 0; sl < static_cast<int64_t>(nslices); ++sl) {
-        std::vector<std::pair<uint32_t, uint32_t>> lanes[kWarp];  // (jb_local, w_index)
+        // (jb_local, bank key: w_index (format 1) or cd | sbit << 31 (format 2))
+        std::vector<std::pair<uint32_t, uint32_t>> lanes[kWarp];
         uint64_t rng = 0x9e3779b97f4a7c15ull ^ static_cast<uint64_t>(sl);  // deterministic per slice
         for (uint32_t g = 0; g < nseg; ++g) {
             for (int l = 0; l < kWarp; ++l) {
@@ -381,7 +411,8 @@ void build_mixed_sell(Handle& h, SellTable& st, int M) {
                     const uint32_t jb = flat[off[ib] + k];
                     if (jb / seg_cols != g) continue;
                     const MixedMove mv = mixed_move(bs[ib], bs[jb], n);
-                    lanes[l].emplace_back(jb - g * seg_cols, mv.cd + mv.sbit * nn);
+                    lanes[l].emplace_back(jb - g * seg_cols,
+                                          format == 2 ? (mv.cd | mv.sbit << 31) : mv.cd + mv.sbit * nn);
                 }
             }
             const uint32_t L = slen[sl * nseg + g];
@@ -389,10 +420,12 @@ void build_mixed_sell(Handle& h, SellTable& st, int M) {
             for (uint32_t k = 0; k < L; ++k) {
                 for (int half = 0; half < 2; ++half) {
                     int64_t used_w[16], used_c[16];
-                    auto cost = [&](uint32_t jbl, uint32_t wi) {
+                    auto cost = [&](uint32_t jbl, uint32_t key) {
+                        const uint32_t wi = key & 0x7fffffffu;
                         const int64_t uw = used_w[wi % 16], uc = used_c[jbl % 16];
-                        return (uw >= 0 && uw != wi) + (uc >= 0 && uc != jbl);
+                        return wv * (uw >= 0 && uw != wi) + (uc >= 0 && uc != jbl);
                     };
+                    auto wkey = [](uint32_t key) { return key & 0x7fffffffu; };
                     // greedy first-fit over the 16 lanes, best of a few lane orders
                     int order[16], best_order[16], best_total = 1 << 30;
                     size_t pick[16], best_pick[16];
@@ -409,7 +442,7 @@ void build_mixed_sell(Handle& h, SellTable& st, int M) {
                             const auto& r = lanes[order[oi]];
                             if (r.empty()) continue;
                             size_t best = 0;
-                            int best_cost = 3;
+                            int best_cost = 1 << 20;
                             for (size_t i = 0; i < r.size(); ++i) {
                                 const int c = cost(r[i].first, r[i].second);
                                 if (c < best_cost) {
@@ -420,7 +453,8 @@ void build_mixed_sell(Handle& h, SellTable& st, int M) {
                             }
                             pick[oi] = best;
                             total += best_cost;
-                            if (used_w[r[best].second % 16] < 0) used_w[r[best].second % 16] = r[best].second;
+                            const uint32_t bw = wkey(r[best].second);
+                            if (used_w[bw % 16] < 0) used_w[bw % 16] = bw;
                             if (used_c[r[best].first % 16] < 0) used_c[r[best].first % 16] = r[best].first;
                         }
                         if (total < best_total) {
@@ -441,9 +475,12 @@ void build_mixed_sell(Handle& h, SellTable& st, int M) {
                         const auto e = r[best_pick[oi]];
                         r[best_pick[oi]] = r.back();
                         r.pop_back();
-                        if (used_w[e.second % 16] < 0) used_w[e.second % 16] = e.second;
+                        const uint32_t ew = wkey(e.second);
+                        if (used_w[ew % 16] < 0) used_w[ew % 16] = ew;
                         if (used_c[e.first % 16] < 0) used_c[e.first % 16] = e.first;
-                        out[static_cast<size_t>(k) * kWarp + l] = encode_mixed_entry(e.first, e.second);
+                        out[static_cast<size_t>(k) * kWarp + l] =
+                            format == 2 ? encode_scatter_entry(e.first, ew, e.second >> 31)
+                                        : encode_mixed_entry(e.first, e.second);
                     }
                     for (int p = 0; p < npad; ++p) {
                         // a zero of W (diagonal c == d) on a free or same-address bank
@@ -462,7 +499,8 @@ void build_mixed_sell(Handle& h, SellTable& st, int M) {
                                 jz = static_cast<uint32_t>(used_c[i]);
                                 break;
                             }
-                        out[static_cast<size_t>(k) * kWarp + pads[p]] = encode_mixed_entry(jz, wz);
+                        out[static_cast<size_t>(k) * kWarp + pads[p]] =
+                            format == 2 ? encode_scatter_entry(jz, wz, 0) : encode_mixed_entry(jz, wz);
                     }
                 }
             }
@@ -537,7 +575,7 @@ size_t estimate_bytes(const Handle& h) {
     for (int c = 0; c < 2; ++c) {
         const auto& t = h.ch[c];
         const size_t e = t.nflat[0] + t.nflat[1];
-        b += e * (4 + 8 + 8) + t.nflat[0] * 4 + t.n * (8 + 2 * (12 + 4)) + ntri * t.n * 8;
+        b += e * (4 + 8) + t.nflat[0] * 4 + t.n * (16 + 2 * (12 + 4)) + ntri * t.n * 8;
     }
     b += (h.ch[1].nflat[0] * 4) * 2;             // SELL incl. padding slack
     const int P = std::max(h.world, h.vblocks);
@@ -545,7 +583,7 @@ size_t estimate_bytes(const Handle& h) {
     if (P > 1) max_blk = std::max<size_t>(max_blk, na / P + 2);
     const size_t loc = (h.world > 1 ? max_blk : na) * nb;
     b += loc * 8;                                 // diag
-    b += 2 * max_blk * nb * 8;                    // ct, yt
+    b += 3 * max_blk * nb * 8;                    // ct, yt, xs
     if (P > 1) b += 2 * max_blk * nb * 8;         // ring buffers
     return b;
 }
@@ -555,8 +593,36 @@ size_t estimate_bytes(const Handle& h) {
 const SellTable& mixed_table(Handle& h, int M) {
     const int idx = M == 1 ? 0 : (M == 2 ? 1 : 2);
     SellTable& t = h.sell_m[idx];
-    if (!t.built) build_mixed_sell(h, t, M);
+    if (!t.built) build_mixed_sell(h, t, M, 1);
     return t;
+}
+
+const SellTable& scatter_table(Handle& h) {
+    SellTable& t = h.sell_scatter;
+    if (!t.built) {
+        build_mixed_sell(h, t, 1, 2);
+        build_scatter_tpos(h);
+    }
+    return t;
+}
+
+void build_scatter_tpos(Handle& h) {
+    ChannelTables& a = h.ch[0];
+    const uint32_t n = static_cast<uint32_t>(a.n);
+    h.tpos.alloc(std::max<uint64_t>(a.nflat[0], 1));
+    k_tpos<<<(n * kWarp + 255) / 256, 256, 0, h.stream>>>(a.flat[0].p, a.offset[0].p, a.len[0].p, n, h.tpos.p);
+    CUDA_LAUNCH_CHECK();
+    h.h_sa_flat.resize(std::max<uint64_t>(a.nflat[0], 1));
+    h.h_sa_off.resize(n + 1);
+    CUDA_CHECK(cudaMemcpyAsync(h.h_sa_flat.data(), a.flat[0].p, a.nflat[0] * 4, cudaMemcpyDeviceToHost, h.stream));
+    CUDA_CHECK(cudaMemcpyAsync(h.h_sa_off.data(), a.offset[0].p, (n + 1) * 8, cudaMemcpyDeviceToHost, h.stream));
+    CUDA_CHECK(cudaStreamSynchronize(h.stream));
+}
+
+void release_sigma_scratch(Handle& h) {
+    h.dbuf.reset();
+    h.dcap_rows = 0;
+    h.scatter_plan.clear();
 }
 
 void release_basis(Handle& h) {
@@ -566,21 +632,26 @@ void release_basis(Handle& h) {
             t.offset[k].reset();
             t.len[k].reset();
             t.pv[k].reset();
-            t.pmask[k].reset();
         }
         t.pab.reset();
         t.J.reset();
     }
-    for (auto& t : h.sell_m) {
+    for (SellTable* tp : {&h.sell_m[0], &h.sell_m[1], &h.sell_m[2], &h.sell_scatter}) {
+        SellTable& t = *tp;
         t.sell.reset();
         t.off.reset();
         t.len.reset();
         t.built = false;
     }
     h.sell_perm.reset();
+    h.tpos.reset();
+    h.h_sa_flat.clear();
+    h.h_sa_off.clear();
+    release_sigma_scratch(h);
     h.diag.reset();
     h.ct.reset();
     h.yt.reset();
+    h.xs.reset();
     h.ring[0].reset();
     h.ring[1].reset();
     h.xbuf.reset();
@@ -605,11 +676,13 @@ void build_device_basis(Handle& h) {
                                        " bytes, budget is " + std::to_string(budget) + " bytes");
 
     for (int c = 0; c < 2; ++c) build_pair_tables(h, c);
-    build_mixed_sell(h, h.sell_m[0], 1);
+    if (mixed_scatter_enabled()) scatter_table(h);
+    else build_mixed_sell(h, h.sell_m[0], 1, 1);
     build_diag(h);
     const size_t scratch = static_cast<size_t>(h.max_blk) * h.nb();
     h.ct.alloc(std::max<size_t>(scratch, 1));
     h.yt.alloc(std::max<size_t>(scratch, 1));
+    h.xs.alloc(std::max<size_t>(h.vblocks > 1 ? h.na() * h.nb() : scratch, 1));
     if (std::max(h.world, h.vblocks) > 1) {
         h.ring[0].alloc(scratch);
         h.ring[1].alloc(scratch);

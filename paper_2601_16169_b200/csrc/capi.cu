@@ -154,7 +154,10 @@ void detci_gpu_destroy(detci_gpu_handle* hh) {
     if (h.stream) cudaStreamSynchronize(h.stream);
     if (h.comm_stream) cudaStreamSynchronize(h.comm_stream);
     release_basis(h);
-    for (auto& c : h.ch) c.strings.reset();
+    for (auto& c : h.ch) {
+        c.strings.reset();
+        c.prefix.reset();
+    }
     h.d_h1.reset();
     h.d_eri.reset();
     h.red.reset();
@@ -211,6 +214,11 @@ int detci_gpu_set_strings(detci_gpu_handle* hh, int norbs, const uint64_t* alpha
             t.strings.alloc(t.n);
             CUDA_CHECK(cudaMemcpy(t.strings.p, t.h_strings.data(), t.n * sizeof(uint64_t),
                                   cudaMemcpyHostToDevice));
+            // exclusive prefix parities P(s) for eps(A,B) = popc(A & P(B)) & 1
+            std::vector<uint64_t> pre(t.n);
+            for (size_t i = 0; i < t.n; ++i) pre[i] = prefix_parity(t.h_strings[i]);
+            t.prefix.alloc(t.n);
+            CUDA_CHECK(cudaMemcpy(t.prefix.p, pre.data(), t.n * sizeof(uint64_t), cudaMemcpyHostToDevice));
         }
         h.have_strings = true;
     });
@@ -529,28 +537,29 @@ int detci_gpu_factorized_element(int norbs, double core, const double* h1, const
             *out = core + energy(bra_a) + energy(bra_b) + x;
             return;
         }
+        // separated-ordering element times eps(bra) eps(ket) (formulas.cuh)
+        const int eps = eps_parity(bra_a, prefix_parity(bra_b)) ^ eps_parity(ket_a, prefix_parity(ket_b));
         if (db == 0 || da == 0) {  // same-spin: alpha (ch 0) or beta (ch 1)
             const int ch = db == 0 ? 0 : 1;
             const uint64_t si = ch == 0 ? bra_a : bra_b, sj = ch == 0 ? ket_a : ket_b;
             const uint64_t spec = ch == 0 ? bra_b : bra_a;
             const int kind = (ch == 0 ? da : db) - 1;
-            const PairEntry e = make_pair_entry(ch, kind, si, sj, h1, eri, norbs);
+            const PairEntry e = make_pair_entry(kind, si, sj, h1, eri, norbs);
             double v = e.v;
             if (kind == 0) {
                 const uint64_t x = si & ~sj, y = sj & ~si;
                 const double j = host_j(eri, norbs, __builtin_ctzll(x), __builtin_ctzll(y), spec);
                 v += (e.ab_sign >> 31) ? -j : j;
             }
-            *out = (popc64(spec & e.mask) & 1) ? -v : v;
+            *out = eps ? -v : v;
             return;
         }
         // mixed alpha single x beta single
         const int pa = __builtin_ctzll(bra_a & ~ket_a), qa = __builtin_ctzll(ket_a & ~bra_a);
         const MixedMove mv = mixed_move(bra_b, ket_b, norbs);
         const int cd = static_cast<int>(mv.cd);
-        double w = mixed_weight(eri, norbs, pa, qa, ket_a, cd / norbs, cd % norbs);
-        if (mv.sbit) w = -w;
-        if (mixed_outer_parity(bra_a, bra_b, pa, qa)) w = -w;
+        double w = mixed_weight(eri, norbs, pa, qa, cd / norbs, cd % norbs);
+        if (mv.sbit ^ mixed_alpha_parity(bra_a, pa, qa) ^ eps) w = -w;
         *out = w;
     });
 }

@@ -342,6 +342,7 @@ void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* re
                                        " bytes, budget is " + std::to_string(std::min<uint64_t>(budget, free_b)) +
                                        " bytes");
     DevBuf<double> store;
+    release_sigma_scratch(h);   // the scatter D buffer is re-planned around the subspace
     store.alloc((2 * static_cast<size_t>(ms) + 3) * n);
     auto V = [&](int j) { return store.p + static_cast<size_t>(j) * n; };
     auto Wv = [&](int j) { return store.p + static_cast<size_t>(ms + j) * n; };
@@ -576,6 +577,7 @@ void davidson_roots_device(Handle& h, const detci_dav_block_opts& opts, detci_da
         fail(DETCI_GPU_E_CAPACITY, "davidson vectors require " + std::to_string(need) + " bytes, budget is " +
                                        std::to_string(budget) + " bytes");
     DevBuf<double> store;
+    release_sigma_scratch(h);
     store.alloc(nvec * n);
     auto V = [&](int j) { return store.p + static_cast<size_t>(j) * n; };
     auto Wv = [&](int j) { return store.p + static_cast<size_t>(ms + j) * n; };

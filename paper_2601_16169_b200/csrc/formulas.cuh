@@ -1,13 +1,24 @@
 // Per-channel Slater-Condon closed forms used by the sigma kernels.
 //
 // The reference evaluates every element from the full interleaved
-// determinant (hij_words, slater_condon.cpp:96-105).  The kernels instead
-// factor each element into a part that depends only on the moving channel's
-// string pair (precomputed once per helper-list entry) and a spectator part
-// evaluated per determinant with one AND + POPC.  These functions are
-// __host__ __device__ so the same code runs in the table-building kernels and
-// in the CPU self-check exported as detci_gpu_factorized_element (tests
-// compare it with the reference hij on random pairs, no GPU needed).
+// determinant (hij_words, slater_condon.cpp:96-105; alpha p is spin-orbital
+// 2p, beta p is 2p+1, bitstring.hpp:13-16).  The kernels work in the
+// *separated* ordering instead (all alpha spin-orbitals, then all beta).
+// The two orderings of a determinant |A,B> differ by the permutation sign
+//   eps(A,B) = (-1)^{#{(p in A, q in B) : q < p}} = (-1)^{popc(A & P(B))},
+// P(B) bit p = parity of popc(B & ((1<<p)-1)) (exclusive prefix parity), so
+//   H_ref[(A,B),(A',B')] = eps(A,B) eps(A',B') H_sep[(A,B),(A',B')]
+// and sigma = eps o (H_sep (eps o C)).  In H_sep every sign is a
+// same-channel parity: the spectator masks of the interleaved phase
+// (popc(B & [lo,hi-1]) for alpha moves, popc(A & [lo+1,hi]) for beta moves)
+// are exactly eps(A,B)eps(A',B) resp. eps(A,B)eps(A,B'), so same-spin
+// elements and the mixed element
+//   H_sep = (-1)^{popc(A & open(pa,qa)) + popc(B & open(pb,qb))} (pa qa|pb qb)
+// no longer depend on the other channel's string except through the J term
+// of singles.  These functions are __host__ __device__ so the same code runs
+// in the table-building kernels and in the CPU self-check exported as
+// detci_gpu_factorized_element (tests compare it with the reference hij on
+// random pairs, no GPU needed).
 #pragma once
 
 #include "common.cuh"
@@ -40,19 +51,33 @@ DG_HD double eri_at(const double* eri, int n, int p, int q, int r, int s) {
     return eri[((static_cast<size_t>(p) * n + q) * n + r) * n + s];
 }
 
+// Exclusive prefix parity P(B): bit p = parity(popc(B & ((1 << p) - 1))).
+DG_HD uint64_t prefix_parity(uint64_t b) {
+    uint64_t x = b << 1;
+    x ^= x << 1;
+    x ^= x << 2;
+    x ^= x << 4;
+    x ^= x << 8;
+    x ^= x << 16;
+    x ^= x << 32;
+    return x;
+}
+
+// eps(A,B) of the separated <-> interleaved reordering as a parity bit.
+DG_HD int eps_parity(uint64_t a, uint64_t pb) { return popc64(a & pb) & 1; }
+
 // One same-spin helper-list entry: bra string si (row), ket string sj
-// (target).  ch = channel that moves (0 alpha, 1 beta), kind 0 single,
-// 1 double.  Element for spectator string S:
-//   single: (-1)^{popc(S & mask)} * (v + (-1)^{sgn} * J_S[tri])
-//   double: (-1)^{popc(S & mask)} * v
+// (target), kind 0 single, 1 double.  Separated-ordering element for
+// spectator string S:
+//   single: v + (-1)^{sgn} * J_S[tri]
+//   double: v
 // one_excite_words / two_excite_words, slater_condon.cpp:41-94.
 struct PairEntry {
     double v;
-    uint64_t mask;
     uint32_t ab_sign; // singles: tri(p,q) | sgn << 31
 };
 
-DG_HD PairEntry make_pair_entry(int ch, int kind, uint64_t si, uint64_t sj, const double* h1,
+DG_HD PairEntry make_pair_entry(int kind, uint64_t si, uint64_t sj, const double* h1,
                                 const double* eri, int n) {
     PairEntry e;
     const uint64_t x = si & ~sj; // bra-only: annihilated
@@ -71,7 +96,6 @@ DG_HD PairEntry make_pair_entry(int ch, int kind, uint64_t si, uint64_t sj, cons
             v -= eri_at(eri, n, p, r, r, q);
         }
         e.v = sgn ? -v : v;
-        e.mask = spectator_mask(ch, p, q);
         e.ab_sign = tri_index(p, q) | (static_cast<uint32_t>(sgn) << 31);
     } else {
         const int p1 = ctz64(x), p2 = ctz64(x & (x - 1));
@@ -83,7 +107,6 @@ DG_HD PairEntry make_pair_entry(int ch, int kind, uint64_t si, uint64_t sj, cons
         const int s2 = popc64(mid & open_mask(p2, q2)) & 1;
         const double v = eri_at(eri, n, p1, q1, p2, q2) - eri_at(eri, n, p1, q2, p2, q1);
         e.v = (s1 ^ s2) ? -v : v;
-        e.mask = spectator_mask(ch, p1, q1) ^ spectator_mask(ch, p2, q2);
         e.ab_sign = 0;
     }
     return e;
@@ -114,19 +137,24 @@ DG_HD uint32_t encode_mixed_entry(uint32_t jb_local, uint32_t w_index) {
     return (jb_local * 8u) | (w_index << 18);
 }
 
-// W_ja[cd] of the mixed term: (pa qa | c d) * (-1)^{popc(A'_ja & Mbeta(c,d))}
-// with the alpha move pa (bra-only) -> qa (ket-only); zero on the diagonal
-// c == d (also the value padding entries point at).
-DG_HD double mixed_weight(const double* eri, int n, int pa, int qa, uint64_t a_ket, int c, int d) {
-    if (c == d) return 0.0;
-    const double v = eri_at(eri, n, pa, qa, c, d);
-    return (popc64(a_ket & spectator_mask(1, c, d)) & 1) ? -v : v;
+// Format 2 (scatter kernel):
+//   bits 0..17  byte offset of Cs[ja, jb] in the staged row segment
+//   bits 18..29 cd = pb * n + qb (n <= 64)
+//   bit  31     sbit (beta same-channel parity)
+DG_HD uint32_t encode_scatter_entry(uint32_t jb_local, uint32_t cd, uint32_t sbit) {
+    return (jb_local * 8u) | (cd << 18) | (sbit << 31);
 }
 
-// Sign of the alpha half of a mixed element that depends on the bra pair:
-// popc(A & open(pa,qa)) + popc(B & [lo, hi-1]).
-DG_HD int mixed_outer_parity(uint64_t a_bra, uint64_t b_bra, int pa, int qa) {
-    return (popc64(a_bra & open_mask(pa, qa)) + popc64(b_bra & spectator_mask(0, pa, qa))) & 1;
+// W_m[cd] of the mixed term for the alpha move m = pa -> qa:
+// (pa qa | c d), zero on the diagonal c == d (also the value padding
+// entries point at).
+DG_HD double mixed_weight(const double* eri, int n, int pa, int qa, int c, int d) {
+    return c == d ? 0.0 : eri_at(eri, n, pa, qa, c, d);
+}
+
+// Same-channel parity of the alpha half of a mixed element: popc(A & open(pa,qa)).
+DG_HD int mixed_alpha_parity(uint64_t a_bra, int pa, int qa) {
+    return popc64(a_bra & open_mask(pa, qa)) & 1;
 }
 
 } // namespace detci_gpu

@@ -1,9 +1,10 @@
 // Internal state of a detci_gpu_handle: the device-resident basis.
 //
-// HBM layout: per channel the uint64 string table,
-// the four helper lists exactly as FlatExcitationTable (flat u32, offset u64,
-// len u32; connectivity.hpp:24-33), a same-spin pair table parallel to each
-// list (value f64, spectator mask u64, J index u32), a spectator J table
+// HBM layout: per channel the uint64 string table
+// and its prefix parities, the four helper lists exactly as
+// FlatExcitationTable (flat u32, offset u64, len u32;
+// connectivity.hpp:24-33), a same-spin pair table parallel to each list
+// (separated-ordering value f64, J index u32), a spectator J table
 // J[tri(p,q)][string] = sum_{r in string} (pq|rr), the beta-singles SELL-32
 // table for the mixed term, this rank's diagonal and the C/sigma scratch.
 #pragma once
@@ -12,6 +13,8 @@
 #include <nccl.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -19,6 +22,17 @@
 #include "common.cuh"
 
 namespace detci_gpu {
+
+// Scatter formulation of the mixed term (sigma.cu k_mixed_scatter): output
+// alpha rows per CTA, shared-memory budget, V-table row pitch (doubles).
+constexpr int kScatterK = 8;
+constexpr uint32_t kScatterSmem = 226u * 1024;
+inline uint32_t scatter_vpitch(int n) { return static_cast<uint32_t>((n * n + 1) & ~1); }
+// DETCI_MIXED=gather selects the gather kernel (k_mixed) for M = 1.
+inline bool mixed_scatter_enabled() {
+    const char* e = std::getenv("DETCI_MIXED");
+    return !(e && std::string(e) == "gather");
+}
 
 template <class T>
 struct DevBuf {
@@ -48,6 +62,7 @@ struct ChannelTables {
     int n_elec = 0;
     std::vector<uint64_t> h_strings;
     DevBuf<uint64_t> strings;
+    DevBuf<uint64_t> prefix;           // prefix_parity(strings[i]) (eps sign)
     // kind 0 = singles, 1 = doubles
     DevBuf<uint32_t> flat[2];
     DevBuf<uint64_t> offset[2];
@@ -56,7 +71,6 @@ struct ChannelTables {
     std::vector<uint32_t> h_len[2];
     // same-spin pair tables (this channel moves, the other is spectator)
     DevBuf<double> pv[2];
-    DevBuf<uint64_t> pmask[2];
     DevBuf<uint32_t> pab;              // singles: tri(p,q) | sign << 31
     // this channel as spectator: J[tri * n + i]
     DevBuf<double> J;
@@ -68,7 +82,18 @@ struct SellTable {
     DevBuf<uint32_t> len;              // [slice * nseg + seg]
     uint32_t seg_cols = 0, nseg = 0;
     bool double_buffer = true;         // C stages double-buffered (else one)
+    int format = 1;                    // 1 gather (k_mixed), 2 scatter (k_mixed_scatter)
     bool built = false;
+};
+
+// One output window of the scatter mixed term: alpha rows [i_lo, i_hi) of
+// this rank, whose D rows (one per (ia, position of ja in ia's singles list))
+// are sa_off[ia] - d_base; per alpha block b the CTA items (ja, kbeg | cnt <<
+// 24) with ja in the block and outputs ia_k in the window.
+struct ScatterWindow {
+    uint64_t i_lo = 0, i_hi = 0, d_base = 0, d_rows = 0;
+    DevBuf<uint2> items;
+    std::vector<uint64_t> item_off;    // per block, size P + 1
 };
 
 struct Handle {
@@ -92,7 +117,17 @@ struct Handle {
     // segmentation per vector count M in {1, 2, 4} (the staged C rows of M
     // vectors share the CTA's shared memory), built on first use
     SellTable sell_m[3];
+    SellTable sell_scatter;            // format 2, M = 1
     DevBuf<uint32_t> sell_perm;        // slot -> beta string (degree-sorted)
+    // scatter mixed term: tpos[sa_off[ja] + k] = position of ja in the
+    // singles list of its k-th single ia; host copies of the alpha singles;
+    // windows per block-rank g (built on first use, dropped with dbuf)
+    DevBuf<uint32_t> tpos;
+    std::vector<uint32_t> h_sa_flat;
+    std::vector<uint64_t> h_sa_off;
+    std::vector<std::vector<std::unique_ptr<ScatterWindow>>> scatter_plan;
+    DevBuf<double> dbuf;               // D partials of the current window
+    uint64_t dcap_rows = 0;            // D rows that fit (set with the plan)
     uint32_t nslices = 0;
 
     // alpha-block partition: P = world (NCCL) or vblocks (virtual)
@@ -104,6 +139,7 @@ struct Handle {
 
     // sigma scratch
     DevBuf<double> ct, yt;             // nb * max_blk
+    DevBuf<double> xs;                 // eps o C of the local block (ring payload)
     DevBuf<double> ring[2];            // max_blk * nb
     DevBuf<double> xbuf, ybuf;         // host-pointer staging, local length
     DevBuf<double> red;                // reduction partials
@@ -126,7 +162,12 @@ void plan_partition(uint64_t na, uint64_t nb, const uint32_t* sa, const uint32_t
                     const uint32_t* sb, const uint32_t* db, int P, int weighted, uint64_t* blk);
 void build_device_basis(Handle& h);
 const SellTable& mixed_table(Handle& h, int M);   // M in {1, 2, 4}
+const SellTable& scatter_table(Handle& h);
 void release_basis(Handle& h);
+void build_scatter_tpos(Handle& h);
+// Drop the scatter D buffer and windows (re-planned against the free memory
+// at the next sigma); the Davidson solvers call it before allocating.
+void release_sigma_scratch(Handle& h);
 
 // sigma.cu
 void sigma_device(Handle& h, const double* dx, double* dy, detci_gpu_timings* tm);

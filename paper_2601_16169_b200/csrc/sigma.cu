@@ -1,21 +1,27 @@
 // sigma = H C over the alpha x beta tensor-product basis (matvec,
 // matvec.cpp:125-228), B200-native, for M = 1, 2 or 4 vectors per pass.
 //
-//   y  = diag*C + sum_ja Ha(ia,ja;B_ib) C[ja,ib]              k_samespin on C
-//   yT =          sum_jb Hb(ib,jb;A_ia) C^T[jb,ia]            k_samespin on C^T
-//   y += sum_ja sum_jb Hm C[ja,jb]                            k_mixed
-//   y += yT^T                                                 k_transpose_add
+// The kernels work in the separated determinant ordering (formulas.cuh):
+// with Cs = eps o C and eps(A,B) = (-1)^{popc(A & P(B))},
+//   y  = diag*C + eps o sum_ja Ha(ia,ja;B_ib) Cs[ja,ib]       k_samespin on Cs
+//   yT =          sum_jb Hb(ib,jb;A_ia) Cs^T[jb,ia]           k_samespin on Cs^T
+//   y += eps o sum_ja sum_jb Hm Cs[ja,jb]                     k_mixed
+//   y += eps o yT^T                                           k_transpose_add_eps
+// where every separated-ordering element carries only same-channel signs, so
+// no kernel evaluates a per-element spectator parity; eps is applied once per
+// determinant in the prologue (k_eps_transpose writes Cs and Cs^T) and in the
+// epilogues.
 //
 // Gather formulation: every output element is owned by exactly one thread,
 // so there are no atomics and the result is deterministic.  The beta term
 // runs the alpha kernel on the transposed block, which turns its per-row
 // gathers into coalesced row reads (the transposes cost 32 B/det against
 // ~8 B x thousands of elements per det).  With M vectors, every element's
-// sign/value work (same-spin) and its W gather and SELL entry (mixed) are
+// value work (same-spin) and its W gather and SELL entry (mixed) are
 // shared by the M vectors (the multi-root block Davidson's new block).
 //
 // Multi-GPU / virtual blocks: alpha rows are partitioned into P blocks;
-// the alpha and mixed terms need C rows from every block, which rotate
+// the alpha and mixed terms need Cs rows from every block, which rotate
 // ring-wise (NCCL send/recv on a comm stream, double-buffered, overlapped
 // with the compute of the resident block).  The beta term and diagonal are
 // block-local.
@@ -37,9 +43,9 @@ constexpr int kMaxM = 4;
 // ---------------------------------------------------------------------------
 // Same-spin kernel.  CTA = (output row, column chunk); threads own R columns
 // each (coalesced), loop over the row's helper-list entries staged in smem.
-// Per element: one coalesced 8 B load of C[ja, col] per vector, AND+POPC
-// against the spectator string, sign flip, DFMA (+ one coalesced J load for
-// singles).  Grid is chunk-major so CTAs in flight share C[:, chunk] in L2.
+// Per element: one coalesced 8 B load of Cs[ja, col] per vector and a DFMA
+// (+ one coalesced J load and a sign flip for singles).  Grid is chunk-major
+// so CTAs in flight share Cs[:, chunk] in L2.
 // ---------------------------------------------------------------------------
 constexpr int kSSBlock = 128;
 constexpr int kStage = 256;
@@ -50,22 +56,22 @@ struct SSR {
 };
 
 struct SameSpinArgs {
-    const double* C[kMaxM];   // C row ja of vector v at C[v] + (ja - c_row0) * ldc
+    const double* C[kMaxM];   // Cs row ja of vector v at C[v] + (ja - c_row0) * ldc
     size_t ldc;
     uint32_t c_row0, j0, j1;  // window [j0, j1) of target rows
     double* Y[kMaxM];         // output row r at Y[v] + r * ldy
     size_t ldy;
     uint32_t row0, nrows;     // list rows [row0, row0 + nrows)
     uint32_t ncols;
-    const uint64_t* spec;     // spectator string per column
     const double* J;          // J[tri * ldj + col]
     size_t ldj;
     const uint32_t* flat[2];
     const uint64_t* off[2];
     const uint32_t* len[2];
     const double* pv[2];
-    const uint64_t* pm[2];
     const uint32_t* pab;
+    const uint64_t* eps_row;  // if set: output *= eps(eps_row[row], eps_col[col])
+    const uint64_t* eps_col;
     const double* diag;       // if set (write mode): Y = diag * Cself + acc
     const double* Cself[kMaxM];
     int accumulate;
@@ -81,27 +87,40 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t 
     return lo;
 }
 
-// (-1)^{popc(S & M)} as a sign bit in position 31 (parity of a 64-bit AND
-// via one 32-bit POPC of lo ^ hi).
-__device__ __forceinline__ uint32_t spectator_sign(uint32_t slo, uint32_t shi, uint32_t mlo, uint32_t mhi) {
-    return __popc((slo & mlo) ^ (shi & mhi)) << 31;
-}
-
+// x * (-1)^{bit 31 of sign31}, by flipping the IEEE sign bit.
 __device__ __forceinline__ double xor_sign(double x, uint32_t sign31) {
     return __hiloint2double(__double2hiint(x) ^ static_cast<int>(sign31), __double2loint(x));
 }
 
+// Epilogue shared by both same-spin variants: eps sign, then write,
+// accumulate, or diag * Cself + acc.
+template <int M>
+__device__ __forceinline__ void samespin_store(const SameSpinArgs& a, uint64_t arow, uint32_t r, uint32_t c,
+                                               const double (&acc)[M]) {
+    const size_t yi = static_cast<size_t>(r) * a.ldy + c;
+    const uint32_t flip = a.eps_row ? static_cast<uint32_t>(__popcll(arow & a.eps_col[c])) : 0u;
+#pragma unroll
+    for (int vv = 0; vv < M; ++vv) {
+        const double v = flip_sign(acc[vv], flip);
+        if (a.accumulate) {
+            a.Y[vv][yi] += v;
+        } else if (a.diag) {
+            a.Y[vv][yi] = fma(a.diag[yi], a.Cself[vv][yi], v);
+        } else {
+            a.Y[vv][yi] = v;
+        }
+    }
+}
+
 // kTail: the CTA's column chunk crosses ncols, so column indices are clamped
 // (loads stay in bounds, stores are masked); full chunks use one base
-// pointer per entry with immediate offsets.  kNarrow: norbs <= 32, strings
-// and masks fit 32 bits and the parity is one AND + POPC.
-template <bool kTail, int M, bool kNarrow>
+// pointer per entry with immediate offsets.
+template <bool kTail, int M>
 __global__ void __launch_bounds__(kSSBlock)
 k_samespin(const SameSpinArgs a, uint32_t chunk0) {
     constexpr int R = SSR<M>::value;
     __shared__ uint32_t s_ja[kStage];
     __shared__ double s_v[kStage];
-    __shared__ uint64_t s_m[kStage];
     __shared__ uint32_t s_ab[kStage];
     __shared__ uint64_t s_range[4];
 
@@ -112,17 +131,13 @@ k_samespin(const SameSpinArgs a, uint32_t chunk0) {
     const uint32_t col0 = chunk * (kSSBlock * R) + tid;
 
     uint32_t col[R];
-    uint32_t slo[R], shi[R];
-    double acc[M][R];
+    double acc[R][M];
 #pragma unroll
     for (int q = 0; q < R; ++q) {
         const uint32_t c = col0 + q * kSSBlock;
         col[q] = kTail ? min(c, a.ncols - 1) : c;
-        const uint64_t sp = a.spec[col[q]];
-        slo[q] = static_cast<uint32_t>(sp);
-        shi[q] = static_cast<uint32_t>(sp >> 32);
 #pragma unroll
-        for (int v = 0; v < M; ++v) acc[v][q] = 0.0;
+        for (int v = 0; v < M; ++v) acc[q][v] = 0.0;
     }
 
     if (tid < 2) {
@@ -146,7 +161,6 @@ k_samespin(const SameSpinArgs a, uint32_t chunk0) {
             for (int t = tid; t < cnt; t += kSSBlock) {
                 s_ja[t] = a.flat[kind][k0 + t] - a.c_row0;
                 s_v[t] = a.pv[kind][k0 + t];
-                s_m[t] = a.pm[kind][k0 + t];
                 if (kind == 0) s_ab[t] = a.pab[k0 + t];
             }
             __syncthreads();
@@ -157,17 +171,14 @@ k_samespin(const SameSpinArgs a, uint32_t chunk0) {
                     const uint32_t ab = s_ab[e];
                     const double* jrow = a.J + static_cast<size_t>(ab & 0x7fffffffu) * a.ldj;
                     const double v = s_v[e];
-                    const uint64_t m = s_m[e];
-                    const uint32_t mlo = static_cast<uint32_t>(m), mhi = static_cast<uint32_t>(m >> 32);
                     const uint32_t jsign = ab & 0x80000000u;
 #pragma unroll
                     for (int q = 0; q < R; ++q) {
                         const uint32_t cq = kTail ? col[q] : col0 + q * kSSBlock;
                         const double val = v + xor_sign(__ldg(jrow + cq), jsign);
-                        const uint32_t sg = (kNarrow ? (__popc(slo[q] & mlo) << 31) : spectator_sign(slo[q], shi[q], mlo, mhi));
 #pragma unroll
                         for (int vv = 0; vv < M; ++vv)
-                            acc[vv][q] = fma(val, xor_sign(__ldg(a.C[vv] + rowoff + cq), sg), acc[vv][q]);
+                            acc[q][vv] = fma(val, __ldg(a.C[vv] + rowoff + cq), acc[q][vv]);
                     }
                 }
             } else {
@@ -175,16 +186,13 @@ k_samespin(const SameSpinArgs a, uint32_t chunk0) {
                 for (int e = 0; e < cnt; ++e) {
                     const size_t rowoff = static_cast<size_t>(s_ja[e]) * a.ldc + (kTail ? 0 : col0);
                     const double v = s_v[e];
-                    const uint64_t m = s_m[e];
-                    const uint32_t mlo = static_cast<uint32_t>(m), mhi = static_cast<uint32_t>(m >> 32);
 #pragma unroll
                     for (int q = 0; q < R; ++q) {
-                        const uint32_t sg = (kNarrow ? (__popc(slo[q] & mlo) << 31) : spectator_sign(slo[q], shi[q], mlo, mhi));
 #pragma unroll
                         for (int vv = 0; vv < M; ++vv) {
                             const double* base = a.C[vv] + rowoff;
                             const double c = __ldg(kTail ? base + col[q] : base + q * kSSBlock);
-                            acc[vv][q] = fma(v, xor_sign(c, sg), acc[vv][q]);
+                            acc[q][vv] = fma(v, c, acc[q][vv]);
                         }
                     }
                 }
@@ -192,32 +200,23 @@ k_samespin(const SameSpinArgs a, uint32_t chunk0) {
         }
     }
 
+    const uint64_t arow = a.eps_row ? a.eps_row[row] : 0;
 #pragma unroll
     for (int q = 0; q < R; ++q) {
         const uint32_t c = col0 + q * kSSBlock;
         if (kTail && c >= a.ncols) continue;
-        const size_t yi = static_cast<size_t>(r) * a.ldy + c;
-#pragma unroll
-        for (int vv = 0; vv < M; ++vv) {
-            if (a.accumulate) {
-                a.Y[vv][yi] += acc[vv][q];
-            } else if (a.diag) {
-                a.Y[vv][yi] = fma(a.diag[yi], a.Cself[vv][yi], acc[vv][q]);
-            } else {
-                a.Y[vv][yi] = acc[vv][q];
-            }
-        }
+        samespin_store<M>(a, arow, r, c, acc[q]);
     }
 }
 
 // Grouped variant: CTA = (8 consecutive output rows, one 32*R-column chunk),
 // one row per warp.  Consecutive rows share most of their helper-list
 // targets (sorted strings), and the warps walk their own sorted lists at
-// similar paces, so C[ja, chunk] lines fetched by one warp are re-read by the
-// others from L1 (simulated 45-59% L1 hits at C2) instead of L2, which bounds
-// the one-row-per-CTA kernel (84.6% L2 throughput, 98% L2 hits, ncu C2).
+// similar paces, so Cs[ja, chunk] lines fetched by one warp are re-read by
+// the others from L1 (simulated 45-59% L1 hits at C2) instead of L2, which
+// bounds the one-row-per-CTA kernel (84.6% L2 throughput, 98% L2 hits).
 constexpr int kGW = 8;        // warps = rows per CTA
-constexpr int kGStage = 32;   // entries staged per warp (6 KB per CTA)
+constexpr int kGStage = 32;   // entries staged per warp
 
 template <bool kTail, int M>
 __global__ void __launch_bounds__(kGW * kWarp, 4)
@@ -225,7 +224,6 @@ k_samespin_g(const SameSpinArgs a, uint32_t chunk0, uint32_t ngroups) {
     constexpr int R = SSR<M>::value;
     __shared__ uint32_t s_ja[kGW][kGStage];
     __shared__ double s_v[kGW][kGStage];
-    __shared__ uint64_t s_m[kGW][kGStage];
     __shared__ uint32_t s_ab[kGW][kGStage];
 
     const uint32_t warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
@@ -237,17 +235,13 @@ k_samespin_g(const SameSpinArgs a, uint32_t chunk0, uint32_t ngroups) {
     const uint32_t col0 = chunk * (kWarp * R) + lane;
 
     uint32_t col[R];
-    uint32_t slo[R], shi[R];
-    double acc[M][R];
+    double acc[R][M];
 #pragma unroll
     for (int q = 0; q < R; ++q) {
         const uint32_t c = col0 + q * kWarp;
         col[q] = kTail ? min(c, a.ncols - 1) : c;
-        const uint64_t sp = a.spec[col[q]];
-        slo[q] = static_cast<uint32_t>(sp);
-        shi[q] = static_cast<uint32_t>(sp >> 32);
 #pragma unroll
-        for (int v = 0; v < M; ++v) acc[v][q] = 0.0;
+        for (int v = 0; v < M; ++v) acc[q][v] = 0.0;
     }
 
     uint64_t rb = 0, re = 0;
@@ -260,7 +254,6 @@ k_samespin_g(const SameSpinArgs a, uint32_t chunk0, uint32_t ngroups) {
     }
     uint32_t* sja = s_ja[warp];
     double* sv = s_v[warp];
-    uint64_t* sm = s_m[warp];
     uint32_t* sab = s_ab[warp];
 
 #pragma unroll 1
@@ -273,7 +266,6 @@ k_samespin_g(const SameSpinArgs a, uint32_t chunk0, uint32_t ngroups) {
             for (int t = lane; t < cnt; t += kWarp) {
                 sja[t] = a.flat[kind][k0 + t] - a.c_row0;
                 sv[t] = a.pv[kind][k0 + t];
-                sm[t] = a.pm[kind][k0 + t];
                 if (kind == 0) sab[t] = a.pab[k0 + t];
             }
             __syncwarp();
@@ -284,17 +276,14 @@ k_samespin_g(const SameSpinArgs a, uint32_t chunk0, uint32_t ngroups) {
                     const uint32_t ab = sab[e];
                     const double* jrow = a.J + static_cast<size_t>(ab & 0x7fffffffu) * a.ldj;
                     const double v = sv[e];
-                    const uint64_t m = sm[e];
-                    const uint32_t mlo = static_cast<uint32_t>(m), mhi = static_cast<uint32_t>(m >> 32);
                     const uint32_t jsign = ab & 0x80000000u;
 #pragma unroll
                     for (int q = 0; q < R; ++q) {
                         const uint32_t cq = kTail ? col[q] : col0 + q * kWarp;
                         const double val = v + xor_sign(__ldg(jrow + cq), jsign);
-                        const uint32_t sg = spectator_sign(slo[q], shi[q], mlo, mhi);
 #pragma unroll
                         for (int vv = 0; vv < M; ++vv)
-                            acc[vv][q] = fma(val, xor_sign(__ldg(a.C[vv] + rowoff + cq), sg), acc[vv][q]);
+                            acc[q][vv] = fma(val, __ldg(a.C[vv] + rowoff + cq), acc[q][vv]);
                     }
                 }
             } else {
@@ -302,16 +291,13 @@ k_samespin_g(const SameSpinArgs a, uint32_t chunk0, uint32_t ngroups) {
                 for (int e = 0; e < cnt; ++e) {
                     const size_t rowoff = static_cast<size_t>(sja[e]) * a.ldc + (kTail ? 0 : col0);
                     const double v = sv[e];
-                    const uint64_t m = sm[e];
-                    const uint32_t mlo = static_cast<uint32_t>(m), mhi = static_cast<uint32_t>(m >> 32);
 #pragma unroll
                     for (int q = 0; q < R; ++q) {
-                        const uint32_t sg = spectator_sign(slo[q], shi[q], mlo, mhi);
 #pragma unroll
                         for (int vv = 0; vv < M; ++vv) {
                             const double* base = a.C[vv] + rowoff;
                             const double c = __ldg(kTail ? base + col[q] : base + q * kWarp);
-                            acc[vv][q] = fma(v, xor_sign(c, sg), acc[vv][q]);
+                            acc[q][vv] = fma(v, c, acc[q][vv]);
                         }
                     }
                 }
@@ -319,35 +305,27 @@ k_samespin_g(const SameSpinArgs a, uint32_t chunk0, uint32_t ngroups) {
         }
     }
 
+    const uint64_t arow = a.eps_row ? a.eps_row[row] : 0;
 #pragma unroll
     for (int q = 0; q < R; ++q) {
         const uint32_t c = col0 + q * kWarp;
         if (kTail && c >= a.ncols) continue;
-        const size_t yi = static_cast<size_t>(r) * a.ldy + c;
-#pragma unroll
-        for (int vv = 0; vv < M; ++vv) {
-            if (a.accumulate) {
-                a.Y[vv][yi] += acc[vv][q];
-            } else if (a.diag) {
-                a.Y[vv][yi] = fma(a.diag[yi], a.Cself[vv][yi], acc[vv][q]);
-            } else {
-                a.Y[vv][yi] = acc[vv][q];
-            }
-        }
+        samespin_store<M>(a, arow, r, c, acc[q]);
     }
 }
 
 // ---------------------------------------------------------------------------
 // Mixed alpha-beta kernel.  CTA = (output row ia, 2048 beta slots).  Stage =
 // (alpha single ja of ia in the window, column segment g).  Two stage
-// buffers, each [ +W | -W | C_0[ja, seg] | ... | C_{M-1}[ja, seg] ]; the next
-// stage's row segments stream in with cp.async (and its W is built) while
-// the current one is consumed:
-//   W[cd] = (pa qa|c d) (-1)^{popc(A_ja & Mbeta(c,d))},
-// then each thread walks its beta strings' singles from the SELL-32 table
-// (one coalesced 4 B entry per element, shared by the M vectors) gathering
-// W[cd] once and C_v[ja, jb] per vector from smem.  The ib-dependent alpha
-// sign is applied once per (ja, ib).
+// buffers, each [ +W | -W | Cs_0[ja, seg] | ... | Cs_{M-1}[ja, seg] ]; the
+// next stage's row segments stream in with cp.async (and its W is built)
+// while the current one is consumed:
+//   W[cd] = (-1)^{popc(A_ia & open(pa,qa))} (pa qa|c d)
+// (separated ordering: the whole alpha half of the sign is uniform over the
+// stage), then each thread walks its beta strings' singles from the SELL-32
+// table (one coalesced 4 B entry per element, shared by the M vectors)
+// gathering W[cd] once and Cs_v[ja, jb] per vector from smem.  eps is
+// applied once per output in the epilogue.
 // ---------------------------------------------------------------------------
 constexpr int kMxBlock = 1024;   // one CTA per SM, 32 warps
 
@@ -365,7 +343,7 @@ struct MixedArgs {
     size_t ldy;
     uint32_t row0, nrows, nb, nparts;
     const uint64_t* alpha;
-    const uint64_t* beta;
+    const uint64_t* beta_prefix;  // prefix_parity of the beta strings (eps)
     const uint32_t* sa_flat;
     const uint64_t* sa_off;
     const uint32_t* sa_len;
@@ -411,16 +389,14 @@ k_mixed(const MixedArgs a) {
     const uint32_t lane = tid % kWarp;
     const uint64_t A = a.alpha[ia];
 
-    uint64_t B[kMxR];
     uint32_t slice[kMxR];
-    double sig[M][kMxR], acc[M][kMxR];
+    double acc[M][kMxR];
 #pragma unroll
     for (int q = 0; q < kMxR; ++q) {
         const uint32_t slot = part * (kMxBlock * kMxR) + q * kMxBlock + tid;
-        B[q] = a.beta[a.perm[min(slot, a.nb - 1)]];
         slice[q] = slot / kWarp;
 #pragma unroll
-        for (int v = 0; v < M; ++v) sig[v][q] = acc[v][q] = 0.0;
+        for (int v = 0; v < M; ++v) acc[v][q] = 0.0;
     }
 
     const uint64_t o = a.sa_off[ia];
@@ -451,13 +427,10 @@ k_mixed(const MixedArgs a) {
             const int pa = __ffsll(static_cast<long long>(A & ~Ak)) - 1;
             const int qa = __ffsll(static_cast<long long>(Ak & ~A)) - 1;
             const double* erow = a.eri + static_cast<size_t>(pa * a.norbs + qa) * nn;
+            const uint32_t sA = static_cast<uint32_t>(mixed_alpha_parity(A, pa, qa));
             for (int cd = tid; cd < nn; cd += kMxBlock) {
                 const int c = cd / a.norbs, d = cd - c * a.norbs;
-                double v = 0.0;
-                if (c != d) {
-                    v = erow[cd];
-                    if (__popcll(Ak & spectator_mask(1, c, d)) & 1) v = -v;
-                }
+                const double v = flip_sign(c != d ? erow[cd] : 0.0, sA);
                 wb[cd] = v;
                 wb[nn + cd] = -v;
             }
@@ -547,23 +520,6 @@ k_mixed(const MixedArgs a) {
                 for (int v = 0; v < M; ++v) acc[v][q] += s[v];
             }
         }
-        if (g + 1 == a.nseg) {  // last segment of this ja: apply the alpha sign
-            const uint32_t ja = f[kb + kk];
-            const uint64_t Ak = a.alpha[ja];
-            const int pa = __ffsll(static_cast<long long>(A & ~Ak)) - 1;
-            const int qa = __ffsll(static_cast<long long>(Ak & ~A)) - 1;
-            const int sA = __popcll(A & open_mask(pa, qa)) & 1;
-            const uint64_t ma = spectator_mask(0, pa, qa);
-#pragma unroll
-            for (int q = 0; q < kMxR; ++q) {
-                const uint32_t sb = static_cast<uint32_t>(sA ^ (__popcll(B[q] & ma) & 1));
-#pragma unroll
-                for (int v = 0; v < M; ++v) {
-                    sig[v][q] += flip_sign(acc[v][q], sb);
-                    acc[v][q] = 0.0;
-                }
-            }
-        }
         __syncthreads();  // C buffer i&1 (and a finished W buffer) free
     }
 
@@ -571,48 +527,253 @@ k_mixed(const MixedArgs a) {
     for (int q = 0; q < kMxR; ++q) {
         const uint32_t slot = part * (kMxBlock * kMxR) + q * kMxBlock + tid;
         if (slot < a.nb) {
-            const size_t yi = static_cast<size_t>(r) * a.ldy + a.perm[slot];
+            const uint32_t ib = a.perm[slot];
+            const uint32_t flip = static_cast<uint32_t>(__popcll(A & a.beta_prefix[ib]));
+            const size_t yi = static_cast<size_t>(r) * a.ldy + ib;
 #pragma unroll
-            for (int v = 0; v < M; ++v) a.Y[v][yi] += sig[v][q];
+            for (int v = 0; v < M; ++v) a.Y[v][yi] += flip_sign(acc[v][q], flip);
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// Transposes through 32x32 smem tiles (coalesced both ways).
+// Scatter formulation of the mixed term (the default for M = 1).
+//
+// The gather kernel above spends two shared-memory gathers (W[cd] and
+// Cs[ja, jb]) per FMA.  Turned around, one staged row Cs[ja, .] feeds every
+// output row ia_k in the singles list of ja, and each gathered Cs[ja, jb]
+// is reused for K of them:
+//   D[ia_k, pos_k, ib] = sum_{jb in S(ib)} (-1)^{sb} V_k[cd(ib,jb)] Cs[ja, jb]
+//   V_k[cd] = (-1)^{popc(A_k & open(pa,qa))} (pa qa|cd),  ia_k -> ja = pa -> qa
+// so an element costs 1 + 1/K gathers instead of 2.  CTA = (item (ja, K
+// consecutive entries of its list), 1024 beta slots); smem holds the K V rows
+// and the row Cs[ja, .] (in segments when it does not fit).  Each partial is
+// stored to its own slot of D (pos_k = position of ja in ia_k's list), and
+// k_mixed_reduce sums D over the positions in ascending order, so the result
+// is deterministic without atomics.
+// ---------------------------------------------------------------------------
+struct ScatterArgs {
+    const double* C;            // Cs row ja at C + (ja - c_row0) * ldc
+    size_t ldc;
+    uint32_t c_row0;
+    const uint2* items;         // (ja, kbeg | cnt << 24)
+    uint32_t nparts, nslices, nb, seg_cols, nseg, vpitch;
+    const uint64_t* alpha;
+    const uint32_t* sa_flat;
+    const uint64_t* sa_off;
+    const uint32_t* tpos;
+    const uint32_t* sell;
+    const uint64_t* sell_off;
+    const uint32_t* sell_len;
+    const double* eri;
+    int norbs;
+    double* D;                  // D row (sa_off[ia] + pos - d_base), ldd slots
+    uint64_t d_base;
+    uint32_t ldd;
+};
+
+template <int K>
+__global__ void __launch_bounds__(kMxBlock, 1)
+k_mixed_scatter(const ScatterArgs a) {
+    extern __shared__ double smem[];
+    double* const vsub = smem;                      // K rows of vpitch
+    double* const cseg = smem + K * a.vpitch;       // Cs[ja, segment]
+    __shared__ uint64_t s_vrow[K];                  // eri row offset | sign << 63
+    __shared__ uint64_t s_drow[K];                  // D row of output k
+
+    const uint32_t item = blockIdx.x / a.nparts, part = blockIdx.x % a.nparts;
+    const uint2 it = a.items[item];
+    const uint32_t ja = it.x, kbeg = it.y & 0xffffffu, cnt = it.y >> 24;
+    const uint64_t oja = a.sa_off[ja];
+    const int n = a.norbs, nn = n * n;
+    const uint32_t tid = threadIdx.x, lane = tid % kWarp;
+
+    if (tid < K) {
+        uint64_t vr = ~0ull, dr = 0;
+        if (tid < cnt) {
+            const uint64_t Aj = a.alpha[ja];
+            const uint32_t ia = a.sa_flat[oja + kbeg + tid];
+            const uint64_t Ak = a.alpha[ia];
+            const int pa = __ffsll(static_cast<long long>(Ak & ~Aj)) - 1;
+            const int qa = __ffsll(static_cast<long long>(Aj & ~Ak)) - 1;
+            vr = static_cast<uint64_t>(pa * n + qa) * nn |
+                 static_cast<uint64_t>(mixed_alpha_parity(Ak, pa, qa)) << 63;
+            dr = a.sa_off[ia] + a.tpos[oja + kbeg + tid] - a.d_base;
+        }
+        s_vrow[tid] = vr;
+        s_drow[tid] = dr;
+    }
+    __syncthreads();
+    for (uint32_t t = tid; t < static_cast<uint32_t>(K * nn); t += kMxBlock) {
+        const uint32_t k = t / nn, cd = t - k * nn;
+        const uint64_t vr = s_vrow[k];
+        double v = 0.0;
+        if (vr != ~0ull && cd % (n + 1) != 0)   // c == d <=> cd divisible by n + 1
+            v = flip_sign(a.eri[(vr & 0x7fffffffffffffffull) + cd], static_cast<uint32_t>(vr >> 63));
+        vsub[k * a.vpitch + cd] = v;
+    }
+
+    const uint32_t slot = part * kMxBlock + tid;
+    const uint32_t sl = slot / kWarp;
+    const bool active = sl < a.nslices;
+    double acc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = 0.0;
+    const char* vb = reinterpret_cast<const char*>(vsub);
+    const char* cb = reinterpret_cast<const char*>(cseg);
+    const uint32_t vstride = a.vpitch * 8;
+    const double* crow = a.C + static_cast<size_t>(ja - a.c_row0) * a.ldc;
+
+#pragma unroll 1
+    for (uint32_t g = 0; g < a.nseg; ++g) {
+        if (g > 0) __syncthreads();   // previous segment consumed
+        const uint32_t segw = min(a.seg_cols, a.nb - g * a.seg_cols);
+        const double* src = crow + static_cast<size_t>(g) * a.seg_cols;
+        for (uint32_t c = tid; c < segw; c += kMxBlock) cp_async8(cseg + c, src + c);
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncthreads();
+        if (!active) continue;
+        const uint32_t L = a.sell_len[sl * a.nseg + g];
+        const uint32_t* ent = a.sell + a.sell_off[sl * a.nseg + g] + lane;
+        uint32_t t = 0;
+#pragma unroll 1
+        for (; t + 4 <= L; t += 4) {
+            uint32_t e[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) e[u] = __ldg(ent + static_cast<size_t>(t + u) * kWarp);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double c = xor_sign(*reinterpret_cast<const double*>(cb + (e[u] & 0x3ffffu)), e[u] & 0x80000000u);
+                const char* v = vb + ((e[u] >> 15) & 0x7ff8u);
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+                    acc[k] = fma(*reinterpret_cast<const double*>(v + k * vstride), c, acc[k]);
+            }
+        }
+#pragma unroll 1
+        for (; t < L; ++t) {
+            const uint32_t e0 = __ldg(ent + static_cast<size_t>(t) * kWarp);
+            const double c = xor_sign(*reinterpret_cast<const double*>(cb + (e0 & 0x3ffffu)), e0 & 0x80000000u);
+            const char* v = vb + ((e0 >> 15) & 0x7ff8u);
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+                acc[k] = fma(*reinterpret_cast<const double*>(v + k * vstride), c, acc[k]);
+        }
+    }
+    if (!active) return;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+        if (k < static_cast<int>(cnt)) a.D[s_drow[k] * a.ldd + slot] = acc[k];
+}
+
+// y[ia, ib] += eps(A_ia, B_ib) sum_{pos in [lo, hi)} D[sa_off[ia] + pos - d_base, slot]
+// with [lo, hi) the positions of the held block's ja in ia's singles list,
+// summed in ascending order (deterministic).  CTA = (row, 256 slots).
+struct ReduceArgs {
+    const double* D;
+    uint64_t d_base;
+    uint32_t ldd, nb, nparts;
+    uint32_t i_lo, j0, j1;
+    const uint32_t* sa_flat;
+    const uint64_t* sa_off;
+    const uint32_t* sa_len;
+    const uint64_t* alpha;
+    const uint64_t* beta_prefix;
+    const uint32_t* perm;
+    double* Y;                  // row ia at Y + (ia - y_row0) * ldy
+    size_t ldy;
+    uint32_t y_row0;
+};
+
+constexpr int kRedBlock = 256;
+
+__global__ void __launch_bounds__(kRedBlock)
+k_mixed_reduce(const ReduceArgs a) {
+    __shared__ uint32_t s_rng[2];
+    const uint32_t ia = a.i_lo + blockIdx.x / a.nparts;
+    const uint32_t slot = (blockIdx.x % a.nparts) * kRedBlock + threadIdx.x;
+    const uint64_t o = a.sa_off[ia];
+    if (threadIdx.x < 2) {
+        const uint32_t* f = a.sa_flat + o;
+        s_rng[threadIdx.x] = lower_bound_u32(f, a.sa_len[ia], threadIdx.x == 0 ? a.j0 : a.j1);
+    }
+    __syncthreads();
+    if (slot >= a.nb) return;
+    const uint32_t lo = s_rng[0], hi = s_rng[1];
+    if (lo == hi) return;
+    const double* d = a.D + (o + lo - a.d_base) * a.ldd + slot;
+    double s = 0.0;
+    uint32_t p = lo;
+#pragma unroll 1
+    for (; p + 4 <= hi; p += 4) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldcs(d + static_cast<size_t>(p - lo + u) * a.ldd);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s += v[u];
+    }
+    for (; p < hi; ++p) s += __ldcs(d + static_cast<size_t>(p - lo) * a.ldd);
+    const uint32_t ib = a.perm[slot];
+    const uint32_t flip = static_cast<uint32_t>(__popcll(a.alpha[ia] & a.beta_prefix[ib]));
+    a.Y[static_cast<size_t>(ia - a.y_row0) * a.ldy + ib] += flip_sign(s, flip);
+}
+
+// ---------------------------------------------------------------------------
+// eps prologue / epilogue, through 32x32 smem tiles (coalesced both ways).
 // ---------------------------------------------------------------------------
 constexpr int kTile = 32;
 
-// dst[c * ldd + r] = src[r * lds + c], src rows x cols
-__global__ void k_transpose(const double* __restrict__ src, size_t lds, double* __restrict__ dst,
-                            size_t ldd, uint32_t rows, uint32_t cols) {
+// Local block x (rows x cols, row r = alpha string a_str[r], column c = beta
+// string with prefix parity b_pre[c]):
+//   xs[r * ldx + c] = eps x      (if xs)     xsT[c * ldt + r] = eps x (if xsT)
+__global__ void k_eps_transpose(const double* __restrict__ x, size_t ldx, double* __restrict__ xs,
+                                double* __restrict__ xsT, size_t ldt, uint32_t rows, uint32_t cols,
+                                const uint64_t* __restrict__ a_str, const uint64_t* __restrict__ b_pre) {
     __shared__ double tile[kTile][kTile + 1];
+    __shared__ uint64_t s_a[kTile];
     const uint32_t c0 = blockIdx.x * kTile, r0 = blockIdx.y * kTile;
-    for (uint32_t y = threadIdx.y; y < kTile; y += blockDim.y) {
-        const uint32_t rr = r0 + y, cc = c0 + threadIdx.x;
-        if (rr < rows && cc < cols) tile[y][threadIdx.x] = src[static_cast<size_t>(rr) * lds + cc];
-    }
+    const uint32_t cc = c0 + threadIdx.x;
+    const uint64_t pb = cc < cols ? b_pre[cc] : 0;
+    if (threadIdx.y == 0 && r0 + threadIdx.x < rows) s_a[threadIdx.x] = a_str[r0 + threadIdx.x];
     __syncthreads();
     for (uint32_t y = threadIdx.y; y < kTile; y += blockDim.y) {
-        const uint32_t cc = c0 + y, rr = r0 + threadIdx.x;
-        if (rr < rows && cc < cols) dst[static_cast<size_t>(cc) * ldd + rr] = tile[threadIdx.x][y];
+        const uint32_t rr = r0 + y;
+        if (rr < rows && cc < cols) {
+            const size_t i = static_cast<size_t>(rr) * ldx + cc;
+            const double v = flip_sign(x[i], static_cast<uint32_t>(__popcll(s_a[y] & pb)));
+            if (xs) xs[i] = v;
+            tile[y][threadIdx.x] = v;
+        }
+    }
+    if (!xsT) return;
+    __syncthreads();
+    for (uint32_t y = threadIdx.y; y < kTile; y += blockDim.y) {
+        const uint32_t c = c0 + y, rr = r0 + threadIdx.x;
+        if (rr < rows && c < cols) xsT[static_cast<size_t>(c) * ldt + rr] = tile[threadIdx.x][y];
     }
 }
 
-// dst[r * ldd + c] += src[c * lds + r], dst rows x cols
-__global__ void k_transpose_add(const double* __restrict__ src, size_t lds,
-                                double* __restrict__ dst, size_t ldd, uint32_t rows,
-                                uint32_t cols) {
+// dst[r * ldd + c] += eps(a_str[r], b_pre[c]) src[c * lds + r], dst rows x cols
+__global__ void k_transpose_add_eps(const double* __restrict__ src, size_t lds, double* __restrict__ dst,
+                                    size_t ldd, uint32_t rows, uint32_t cols,
+                                    const uint64_t* __restrict__ a_str, const uint64_t* __restrict__ b_pre) {
     __shared__ double tile[kTile][kTile + 1];
+    __shared__ uint64_t s_a[kTile];
     const uint32_t c0 = blockIdx.x * kTile, r0 = blockIdx.y * kTile;
     for (uint32_t y = threadIdx.y; y < kTile; y += blockDim.y) {
-        const uint32_t cc = c0 + y, rr = r0 + threadIdx.x;
-        if (rr < rows && cc < cols) tile[y][threadIdx.x] = src[static_cast<size_t>(cc) * lds + rr];
+        const uint32_t c = c0 + y, rr = r0 + threadIdx.x;
+        if (rr < rows && c < cols) tile[y][threadIdx.x] = src[static_cast<size_t>(c) * lds + rr];
     }
+    if (threadIdx.y == 0 && r0 + threadIdx.x < rows) s_a[threadIdx.x] = a_str[r0 + threadIdx.x];
     __syncthreads();
+    const uint32_t cc = c0 + threadIdx.x;
+    const uint64_t pb = cc < cols ? b_pre[cc] : 0;
     for (uint32_t y = threadIdx.y; y < kTile; y += blockDim.y) {
-        const uint32_t rr = r0 + y, cc = c0 + threadIdx.x;
-        if (rr < rows && cc < cols) dst[static_cast<size_t>(rr) * ldd + cc] += tile[threadIdx.x][y];
+        const uint32_t rr = r0 + y;
+        if (rr < rows && cc < cols)
+            dst[static_cast<size_t>(rr) * ldd + cc] +=
+                flip_sign(tile[threadIdx.x][y], static_cast<uint32_t>(__popcll(s_a[y] & pb)));
     }
 }
 
@@ -659,20 +820,18 @@ struct PhaseTimer {
 using Ptrs = std::array<const double*, kMaxM>;
 using MPtrs = std::array<double*, kMaxM>;
 
-// DETCI_SAMESPIN=grouped selects the 8-rows-per-CTA kernel.  Measured on
-// B200: 51% L1 hits and L2 load down from 85% to 24%, but the kernel is then
-// issue/latency-bound and runs level with the row kernel (C2 28.5 vs 27 ms,
-// C3 157 vs 165 ms), so the row kernel stays the default.
+// The grouped kernel (8 rows per CTA, L1 reuse) is the default; set
+// DETCI_SAMESPIN=row for the one-row-per-CTA kernel.  With the spectator
+// parities gone (separated ordering) the grouped kernel is no longer
+// issue-bound: measured on B200, alpha term C2 19.9 vs 25.4 ms, C3 115 vs
+// 159 ms.
 bool grouped_samespin() {
-    static const int mode = [] {
-        const char* e = std::getenv("DETCI_SAMESPIN");
-        return (e && std::string(e) == "grouped") ? 1 : 0;
-    }();
-    return mode == 1;
+    const char* e = std::getenv("DETCI_SAMESPIN");
+    return !(e && std::string(e) == "row");
 }
 
 template <int M>
-void launch_samespin(const SameSpinArgs& s, cudaStream_t st, bool narrow) {
+void launch_samespin(const SameSpinArgs& s, cudaStream_t st) {
     if (s.nrows == 0 || s.ncols == 0) return;
     if (grouped_samespin()) {
         constexpr uint32_t kChunk = kWarp * SSR<M>::value;
@@ -680,7 +839,7 @@ void launch_samespin(const SameSpinArgs& s, cudaStream_t st, bool narrow) {
         const bool tail = s.ncols % kChunk != 0;
         const uint32_t ngroups = (s.nrows + kGW - 1) / kGW;
         static bool configured = false;
-        if (!configured) {  // favour L1 over shared memory (the kernel uses ~24 KB)
+        if (!configured) {  // favour L1 over shared memory (the kernel uses ~16 KB)
             CUDA_CHECK(cudaFuncSetAttribute(k_samespin_g<false, M>, cudaFuncAttributePreferredSharedMemoryCarveout, 10));
             CUDA_CHECK(cudaFuncSetAttribute(k_samespin_g<true, M>, cudaFuncAttributePreferredSharedMemoryCarveout, 10));
             configured = true;
@@ -699,17 +858,11 @@ void launch_samespin(const SameSpinArgs& s, cudaStream_t st, bool narrow) {
     const uint64_t full = s.ncols / kChunk;
     const bool tail = s.ncols % kChunk != 0;
     if (full) {
-        if (narrow)
-            k_samespin<false, M, true><<<static_cast<unsigned>(full * s.nrows), kSSBlock, 0, st>>>(s, 0);
-        else
-            k_samespin<false, M, false><<<static_cast<unsigned>(full * s.nrows), kSSBlock, 0, st>>>(s, 0);
+        k_samespin<false, M><<<static_cast<unsigned>(full * s.nrows), kSSBlock, 0, st>>>(s, 0);
         CUDA_LAUNCH_CHECK();
     }
     if (tail) {
-        if (narrow)
-            k_samespin<true, M, true><<<s.nrows, kSSBlock, 0, st>>>(s, static_cast<uint32_t>(full));
-        else
-            k_samespin<true, M, false><<<s.nrows, kSSBlock, 0, st>>>(s, static_cast<uint32_t>(full));
+        k_samespin<true, M><<<s.nrows, kSSBlock, 0, st>>>(s, static_cast<uint32_t>(full));
         CUDA_LAUNCH_CHECK();
     }
 }
@@ -720,7 +873,6 @@ void fill_lists(SameSpinArgs& s, const ChannelTables& t) {
         s.off[k] = t.offset[k].p;
         s.len[k] = t.len[k].p;
         s.pv[k] = t.pv[k].p;
-        s.pm[k] = t.pmask[k].p;
     }
     s.pab = t.pab.p;
 }
@@ -742,13 +894,14 @@ void launch_alpha(const Handle& h, const Ptrs& Cb, uint32_t b0, uint32_t b1, con
     s.row0 = static_cast<uint32_t>(a0);
     s.nrows = static_cast<uint32_t>(a1 - a0);
     s.ncols = static_cast<uint32_t>(h.nb());
-    s.spec = h.ch[1].strings.p;
     s.J = h.ch[1].J.p;
     s.ldj = h.nb();
     fill_lists(s, h.ch[0]);
+    s.eps_row = h.ch[0].strings.p;
+    s.eps_col = h.ch[1].prefix.p;
     s.diag = first ? h.diag.p + (a0 - h.a0) * h.nb() : nullptr;
     s.accumulate = first ? 0 : 1;
-    launch_samespin<M>(s, h.stream, h.norbs <= 32);
+    launch_samespin<M>(s, h.stream);
 }
 
 size_t mixed_smem(const Handle& h, const SellTable& t, int M) {
@@ -776,7 +929,7 @@ void launch_mixed(Handle& h, const Ptrs& Cb, uint32_t b0, uint32_t b1, const MPt
     m.nb = static_cast<uint32_t>(h.nb());
     m.nparts = (m.nb + kMxBlock * MxR<M>::value - 1) / (kMxBlock * MxR<M>::value);
     m.alpha = h.ch[0].strings.p;
-    m.beta = h.ch[1].strings.p;
+    m.beta_prefix = h.ch[1].prefix.p;
     m.sa_flat = h.ch[0].flat[0].p;
     m.sa_off = h.ch[0].offset[0].p;
     m.sa_len = h.ch[0].len[0].p;
@@ -810,31 +963,179 @@ void launch_mixed(Handle& h, const Ptrs& Cb, uint32_t b0, uint32_t b1, const MPt
     CUDA_LAUNCH_CHECK();
 }
 
-// Scratch for M vectors: C^T / sigma^T blocks and ring buffers.
+// Scatter plan for block-rank g (rows [blk[g], blk[g+1])): output windows
+// whose D fits the capacity, and per window and alpha block the CTA items.
+// D capacity: DETCI_MIXED_DBYTES if set (tests force several windows), else
+// 60% of the free device memory at the first sigma (release_sigma_scratch
+// re-plans after the Davidson solvers allocate their subspace).
+const std::vector<std::unique_ptr<ScatterWindow>>& scatter_windows(Handle& h, int g, int P) {
+    const SellTable& t = scatter_table(h);
+    (void)t;
+    if (h.scatter_plan.size() != static_cast<size_t>(P)) {
+        h.scatter_plan.clear();
+        h.scatter_plan.resize(P);
+    }
+    auto& wins = h.scatter_plan[g];
+    if (!wins.empty()) return wins;
+    const uint64_t ldd = static_cast<uint64_t>(h.nslices) * kWarp;
+    const uint64_t* off = h.h_sa_off.data();
+    const uint32_t* flat = h.h_sa_flat.data();
+    if (h.dcap_rows == 0) {
+        size_t fr = 0, tot = 0;
+        CUDA_CHECK(cudaMemGetInfo(&fr, &tot));
+        uint64_t bytes = static_cast<uint64_t>(0.6 * static_cast<double>(fr));
+        if (const char* e = std::getenv("DETCI_MIXED_DBYTES")) bytes = std::strtoull(e, nullptr, 10);
+        uint64_t maxlen = 1;
+        for (size_t i = 0; i < h.na(); ++i) maxlen = std::max<uint64_t>(maxlen, off[i + 1] - off[i]);
+        h.dcap_rows = std::max<uint64_t>(bytes / (ldd * 8), maxlen);
+    }
+    const uint64_t r0 = h.blk[g], r1 = h.blk[g + 1];
+    uint64_t i = r0;
+    while (i < r1) {
+        auto w = std::make_unique<ScatterWindow>();
+        w->i_lo = i;
+        while (i < r1 && (i == w->i_lo || off[i + 1] - off[w->i_lo] <= h.dcap_rows)) ++i;
+        w->i_hi = i;
+        w->d_base = off[w->i_lo];
+        w->d_rows = off[w->i_hi] - w->d_base;
+        std::vector<uint2> items;
+        w->item_off.assign(P + 1, 0);
+        for (int b = 0; b < P; ++b) {
+            w->item_off[b] = items.size();
+            for (uint64_t ja = h.blk[b]; ja < h.blk[b + 1]; ++ja) {
+                const uint32_t* f = flat + off[ja];
+                const uint32_t* e = flat + off[ja + 1];
+                const uint32_t p_lo = static_cast<uint32_t>(std::lower_bound(f, e, static_cast<uint32_t>(w->i_lo)) - f);
+                const uint32_t p_hi = static_cast<uint32_t>(std::lower_bound(f, e, static_cast<uint32_t>(w->i_hi)) - f);
+                for (uint32_t p = p_lo; p < p_hi; p += kScatterK) {
+                    const uint32_t cnt = std::min<uint32_t>(kScatterK, p_hi - p);
+                    items.push_back(make_uint2(static_cast<uint32_t>(ja), p | cnt << 24));
+                }
+            }
+        }
+        w->item_off[P] = items.size();
+        w->items.alloc(std::max<size_t>(items.size(), 1));
+        if (!items.empty())
+            CUDA_CHECK(cudaMemcpy(w->items.p, items.data(), items.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+        wins.push_back(std::move(w));
+    }
+    uint64_t need = 0;
+    for (auto& w : wins) need = std::max(need, w->d_rows);
+    if (h.dbuf.n < need * ldd) h.dbuf.alloc(need * ldd);
+    return wins;
+}
+
+// Mixed term through the scatter kernel for block-rank g, held alpha block
+// b = rows [b0, b1) of Cs in Cb, outputs rows [a0, a1) of y_loc.
+void launch_mixed_scatter(Handle& h, int g, int P, int b, const double* Cb, uint32_t b0, uint32_t b1,
+                          double* y_loc, uint64_t a0) {
+    const SellTable& t = scatter_table(h);
+    const auto& wins = scatter_windows(h, g, P);
+    const uint32_t ldd = h.nslices * kWarp;
+    const uint32_t vpitch = scatter_vpitch(h.norbs);
+    const size_t smem = (static_cast<size_t>(kScatterK) * vpitch + ((t.seg_cols + 1) & ~1u)) * sizeof(double);
+    static size_t configured = 0;
+    if (smem > configured) {
+        CUDA_CHECK(cudaFuncSetAttribute(k_mixed_scatter<kScatterK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+        configured = smem;
+    }
+    for (const auto& w : wins) {
+        const uint64_t i0 = w->item_off[b], i1 = w->item_off[b + 1];
+        if (i1 == i0) continue;
+        ScatterArgs a{};
+        a.C = Cb;
+        a.ldc = h.nb();
+        a.c_row0 = b0;
+        a.items = w->items.p + i0;
+        a.nparts = (ldd + kMxBlock - 1) / kMxBlock;
+        a.nslices = h.nslices;
+        a.nb = static_cast<uint32_t>(h.nb());
+        a.seg_cols = t.seg_cols;
+        a.nseg = t.nseg;
+        a.vpitch = vpitch;
+        a.alpha = h.ch[0].strings.p;
+        a.sa_flat = h.ch[0].flat[0].p;
+        a.sa_off = h.ch[0].offset[0].p;
+        a.tpos = h.tpos.p;
+        a.sell = t.sell.p;
+        a.sell_off = t.off.p;
+        a.sell_len = t.len.p;
+        a.eri = h.d_eri.p;
+        a.norbs = h.norbs;
+        a.D = h.dbuf.p;
+        a.d_base = w->d_base;
+        a.ldd = ldd;
+        const uint64_t grid = (i1 - i0) * a.nparts;
+        if (grid >= (1ull << 31)) fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: scatter grid too large");
+        k_mixed_scatter<kScatterK><<<static_cast<unsigned>(grid), kMxBlock, smem, h.stream>>>(a);
+        CUDA_LAUNCH_CHECK();
+
+        ReduceArgs r{};
+        r.D = h.dbuf.p;
+        r.d_base = w->d_base;
+        r.ldd = ldd;
+        r.nb = a.nb;
+        r.nparts = (a.nb + kRedBlock - 1) / kRedBlock;
+        r.i_lo = static_cast<uint32_t>(w->i_lo);
+        r.j0 = b0;
+        r.j1 = b1;
+        r.sa_flat = a.sa_flat;
+        r.sa_off = a.sa_off;
+        r.sa_len = h.ch[0].len[0].p;
+        r.alpha = a.alpha;
+        r.beta_prefix = h.ch[1].prefix.p;
+        r.perm = h.sell_perm.p;
+        r.Y = y_loc;
+        r.ldy = h.nb();
+        r.y_row0 = static_cast<uint32_t>(a0);
+        const uint64_t rgrid = (w->i_hi - w->i_lo) * r.nparts;
+        k_mixed_reduce<<<static_cast<unsigned>(rgrid), kRedBlock, 0, h.stream>>>(r);
+        CUDA_LAUNCH_CHECK();
+    }
+}
+
+// Scratch for M vectors: Cs^T / sigma^T blocks, the eps-signed Cs (the
+// whole vector for virtual blocks, whose ring reads other blocks before
+// their own prologue ran) and ring buffers.
 void ensure_scratch(Handle& h, int M, int P) {
     const size_t block = static_cast<size_t>(h.max_blk) * h.nb();
     if (h.ct.n < M * block) {
         h.ct.alloc(M * block);
         h.yt.alloc(M * block);
     }
+    const size_t xs = M * (h.vblocks > 1 ? h.na() * h.nb() : block);
+    if (h.xs.n < xs) h.xs.alloc(xs);
     if (P > 1 && h.ring[0].n < M * block) {
         h.ring[0].alloc(M * block);
         h.ring[1].alloc(M * block);
     }
 }
 
-// The beta term for rows [a0, a1): transpose, same-spin kernel on C^T with
-// the alpha strings as spectators, result in h.yt (M x [nb][nloc]).
+// eps prologue for rows [a0, a1): Cs (row-major, if xs_loc) and Cs^T (h.ct).
 template <int M>
-void beta_term(Handle& h, const Ptrs& x_loc, uint64_t a0, uint64_t a1, PhaseTimer& tm) {
+void eps_prologue(Handle& h, const Ptrs& x_loc, const MPtrs& xs_loc, bool transpose, uint64_t a0,
+                  uint64_t a1) {
     const uint32_t nloc = static_cast<uint32_t>(a1 - a0), nb = static_cast<uint32_t>(h.nb());
     const size_t block = static_cast<size_t>(h.max_blk) * h.nb();
-    const int id = tm.begin(1);
+    if (nloc == 0 || nb == 0) return;
     dim3 tb(kTile, 8), tg((nb + kTile - 1) / kTile, (nloc + kTile - 1) / kTile);
+    for (int v = 0; v < M; ++v) {
+        k_eps_transpose<<<tg, tb, 0, h.stream>>>(x_loc[v], nb, xs_loc[v], transpose ? h.ct.p + v * block : nullptr,
+                                                 nloc, nloc, nb, h.ch[0].strings.p + a0, h.ch[1].prefix.p);
+        CUDA_LAUNCH_CHECK();
+    }
+}
+
+// The beta term for rows [a0, a1): same-spin kernel on Cs^T (h.ct, written
+// by the prologue), raw result in h.yt (M x [nb][nloc]); eps is applied by
+// the combine.
+template <int M>
+void beta_term(Handle& h, uint64_t a0, uint64_t a1) {
+    const uint32_t nloc = static_cast<uint32_t>(a1 - a0), nb = static_cast<uint32_t>(h.nb());
+    const size_t block = static_cast<size_t>(h.max_blk) * h.nb();
     SameSpinArgs s{};
     for (int v = 0; v < M; ++v) {
-        k_transpose<<<tg, tb, 0, h.stream>>>(x_loc[v], nb, h.ct.p + v * block, nloc, nloc, nb);
-        CUDA_LAUNCH_CHECK();
         s.C[v] = h.ct.p + v * block;
         s.Y[v] = h.yt.p + v * block;
     }
@@ -846,44 +1147,49 @@ void beta_term(Handle& h, const Ptrs& x_loc, uint64_t a0, uint64_t a1, PhaseTime
     s.row0 = 0;
     s.nrows = nb;
     s.ncols = nloc;
-    s.spec = h.ch[0].strings.p + a0;
     s.J = h.ch[0].J.p + a0;
     s.ldj = h.na();
     fill_lists(s, h.ch[1]);
     s.accumulate = 0;
-    launch_samespin<M>(s, h.stream, h.norbs <= 32);
-    tm.end(id);
+    launch_samespin<M>(s, h.stream);
 }
 
 template <int M>
 void combine(Handle& h, const MPtrs& y_loc, uint64_t a0, uint64_t a1, PhaseTimer& tm) {
     const uint32_t nloc = static_cast<uint32_t>(a1 - a0), nb = static_cast<uint32_t>(h.nb());
     const size_t block = static_cast<size_t>(h.max_blk) * h.nb();
+    if (nloc == 0 || nb == 0) return;
     const int id = tm.begin(3);
     dim3 tb(kTile, 8), tg((nb + kTile - 1) / kTile, (nloc + kTile - 1) / kTile);
     for (int v = 0; v < M; ++v) {
-        k_transpose_add<<<tg, tb, 0, h.stream>>>(h.yt.p + v * block, nloc, y_loc[v], nb, nloc, nb);
+        k_transpose_add_eps<<<tg, tb, 0, h.stream>>>(h.yt.p + v * block, nloc, y_loc[v], nb, nloc, nb,
+                                                     h.ch[0].strings.p + a0, h.ch[1].prefix.p);
         CUDA_LAUNCH_CHECK();
     }
     tm.end(id);
 }
 
-// One block-rank's sigma with the C ring.  `fetch(s, held, dst, block)`
+// One block-rank's sigma with the Cs ring.  `fetch(s, held, dst, block)`
 // enqueues on h.comm_stream the transfer that makes alpha block `block`
 // resident in dst (M consecutive block-sized slabs) for step s + 1 (NCCL
 // send/recv, or a device copy for virtual blocks).
 template <int M, class Fetch>
-void sigma_ring(Handle& h, int g, int P, const Ptrs& x_loc, const MPtrs& y_loc, PhaseTimer& tm, Fetch&& fetch) {
+void sigma_ring(Handle& h, int g, int P, const Ptrs& x_loc, const MPtrs& xs_loc, const MPtrs& y_loc,
+                PhaseTimer& tm, Fetch&& fetch) {
     const uint64_t a0 = h.blk[g], a1 = h.blk[g + 1];
     const size_t block = static_cast<size_t>(h.max_blk) * h.nb();
     cudaEvent_t* done_compute = h.ev;      // [0..1]
     cudaEvent_t* done_comm = h.ev + 2;     // [2..3]
-    // x and the ring buffers are produced / last read on the compute stream:
-    // the comm stream must not send or overwrite them before that work ends.
+    int id = tm.begin(1);
+    eps_prologue<M>(h, x_loc, xs_loc, true, a0, a1);
+    // Cs and the ring buffers are produced / last read on the compute
+    // stream: the comm stream must not send or overwrite them before that.
     CUDA_CHECK(cudaEventRecord(h.ev[4], h.stream));
     CUDA_CHECK(cudaStreamWaitEvent(h.comm_stream, h.ev[4], 0));
-    beta_term<M>(h, x_loc, a0, a1, tm);
-    Ptrs held = x_loc;
+    beta_term<M>(h, a0, a1);
+    tm.end(id);
+    Ptrs held{};
+    for (int v = 0; v < M; ++v) held[v] = xs_loc[v];
     for (int s = 0; s < P; ++s) {
         const int b = (g + s) % P;
         if (s + 1 < P) {
@@ -893,11 +1199,14 @@ void sigma_ring(Handle& h, int g, int P, const Ptrs& x_loc, const MPtrs& y_loc, 
             CUDA_CHECK(cudaEventRecord(done_comm[s % 2], h.comm_stream));
         }
         const uint32_t b0 = static_cast<uint32_t>(h.blk[b]), b1 = static_cast<uint32_t>(h.blk[b + 1]);
-        int id = tm.begin(0);
+        id = tm.begin(0);
         launch_alpha<M>(h, held, b0, b1, x_loc, y_loc, a0, a1, s == 0);
         tm.end(id);
         id = tm.begin(2);
-        launch_mixed<M>(h, held, b0, b1, y_loc, a0, a1);
+        if (M == 1 && mixed_scatter_enabled())
+            launch_mixed_scatter(h, g, P, b, held[0], b0, b1, y_loc[0], a0);
+        else
+            launch_mixed<M>(h, held, b0, b1, y_loc, a0, a1);
         tm.end(id);
         CUDA_CHECK(cudaEventRecord(done_compute[s % 2], h.stream));
         if (s + 1 < P) {
@@ -916,7 +1225,9 @@ void sigma_schedule_m(Handle& h, const Ptrs& dx, const MPtrs& dy, PhaseTimer& tm
     ensure_scratch(h, M, P);
     if (h.world > 1) {
         const int g = h.rank;
-        sigma_ring<M>(h, g, P, dx, dy, tm, [&](int s, const Ptrs& held, double* dst, int next) {
+        MPtrs xs{};
+        for (int v = 0; v < M; ++v) xs[v] = h.xs.p + v * block;
+        sigma_ring<M>(h, g, P, dx, xs, dy, tm, [&](int s, const Ptrs& held, double* dst, int next) {
             const int cur = (g + s) % P;
             const size_t send_n = (h.blk[cur + 1] - h.blk[cur]) * nb;
             const size_t recv_n = (h.blk[next + 1] - h.blk[next]) * nb;
@@ -929,23 +1240,31 @@ void sigma_schedule_m(Handle& h, const Ptrs& dx, const MPtrs& dy, PhaseTimer& tm
         });
     } else if (P > 1) {
         // Virtual blocks: every block-rank's schedule runs in turn on this GPU;
-        // the ring transport is a device copy out of the full x.
+        // the ring transport is a device copy out of the whole Cs, which is
+        // signed up front (a real rank signs its own block in its prologue).
+        const size_t full = h.na() * nb;
+        MPtrs xs_all{};
+        for (int v = 0; v < M; ++v) xs_all[v] = h.xs.p + v * full;
+        eps_prologue<M>(h, dx, xs_all, false, 0, h.na());
         for (int g = 0; g < P; ++g) {
             Ptrs xg{};
-            MPtrs yg{};
+            MPtrs yg{}, xsg{};
             for (int v = 0; v < M; ++v) {
                 xg[v] = dx[v] + h.blk[g] * nb;
                 yg[v] = dy[v] + h.blk[g] * nb;
+                xsg[v] = xs_all[v] + h.blk[g] * nb;
             }
-            sigma_ring<M>(h, g, P, xg, yg, tm, [&](int, const Ptrs&, double* dst, int next) {
+            sigma_ring<M>(h, g, P, xg, xsg, yg, tm, [&](int, const Ptrs&, double* dst, int next) {
                 const size_t n = (h.blk[next + 1] - h.blk[next]) * nb;
                 for (int v = 0; v < M; ++v)
-                    CUDA_CHECK(cudaMemcpyAsync(dst + v * block, dx[v] + h.blk[next] * nb, n * sizeof(double),
+                    CUDA_CHECK(cudaMemcpyAsync(dst + v * block, xs_all[v] + h.blk[next] * nb, n * sizeof(double),
                                                cudaMemcpyDeviceToDevice, h.comm_stream));
             });
         }
     } else {
-        sigma_ring<M>(h, 0, 1, dx, dy, tm, [](int, const Ptrs&, double*, int) {});
+        MPtrs xs{};
+        for (int v = 0; v < M; ++v) xs[v] = h.xs.p + v * block;
+        sigma_ring<M>(h, 0, 1, dx, xs, dy, tm, [](int, const Ptrs&, double*, int) {});
     }
 }
 

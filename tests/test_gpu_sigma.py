@@ -185,3 +185,48 @@ def test_segmented_virtual_blocks(monkeypatch):
     d = np.load(GOLDEN / "synthetic_s12.npz")
     with gpu_basis(ints, s, s, virtual_blocks=3, weighted_partition=True) as b:
         assert rel_diff(detci.matvec(b, synth.random_vector(len(s) ** 2, 11)), d["sigma11"]) <= 1e-12
+
+
+@pytest.mark.parametrize("kernel", ["row", "grouped"])
+def test_samespin_kernel_variants(kernel, monkeypatch):
+    """Both same-spin kernels (DETCI_SAMESPIN=row: one row per CTA; default:
+    8 rows per CTA) against the reference fixtures, the C1 reference rows and
+    virtual blocks."""
+    monkeypatch.setenv("DETCI_SAMESPIN", kernel)
+    for name in ("h6_ring", "chain8"):
+        ints, d = load_fixture(name)
+        with gpu_basis(ints, d["alpha"], d["beta"]) as b:
+            assert rel_diff(detci.matvec(b, d["x11"]), d["sigma11"]) <= 1e-12
+    rows = np.load(GOLDEN / "rows_C1.npz")
+    ints, a, bb = synth.synthetic_system("C1")
+    r = rows["rows"].astype(np.int64)
+    for blocks in (1, 3):
+        with gpu_basis(ints, a, bb, virtual_blocks=blocks) as b:
+            x = synth.random_vector(b.dimension(), 11)
+            assert rel_diff(detci.matvec(b, x).reshape(len(a), -1)[r], rows["sigma_rows"]) <= 1e-12
+
+
+@pytest.mark.parametrize("mixed,dbytes", [("gather", None), ("scatter", None), ("scatter", "3000000"),
+                                          ("scatter", "1")])
+def test_mixed_kernel_variants(mixed, dbytes, monkeypatch):
+    """Mixed term through the gather kernel (DETCI_MIXED=gather) and the
+    default scatter kernel + deterministic D reduction, with the D buffer
+    forced into several output windows (DETCI_MIXED_DBYTES; "1" = one alpha
+    row per window), against the reference rows at C1, the fixtures and
+    virtual blocks; bitwise run-to-run determinism."""
+    monkeypatch.setenv("DETCI_MIXED", mixed)
+    if dbytes:
+        monkeypatch.setenv("DETCI_MIXED_DBYTES", dbytes)
+    for name in ("h4_chain", "chain8"):
+        ints, d = load_fixture(name)
+        with gpu_basis(ints, d["alpha"], d["beta"]) as b:
+            assert rel_diff(detci.matvec(b, d["x11"]), d["sigma11"]) <= 1e-12
+    rows = np.load(GOLDEN / "rows_C1.npz")
+    ints, a, bb = synth.synthetic_system("C1")
+    r = rows["rows"].astype(np.int64)
+    for blocks in ((1, 3) if dbytes != "1" else (2,)):
+        with gpu_basis(ints, a, bb, virtual_blocks=blocks, weighted_partition=True) as b:
+            x = synth.random_vector(b.dimension(), 11)
+            y = detci.matvec(b, x)
+            assert rel_diff(y.reshape(len(a), -1)[r], rows["sigma_rows"]) <= 1e-12
+            assert np.array_equal(y, detci.matvec(b, x))
