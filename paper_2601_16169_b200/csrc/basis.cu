@@ -330,8 +330,8 @@ void build_pair_tables(Handle& h, int c) {
 //    cuts shared-memory wavefronts per element step from 9.2 to 5.6.
 //  * format 2 (scatter kernel, k_mixed_scatter): the same slots, segments
 //    and schedule, but the entry carries cd and the beta sign separately
-//    (encode_scatter_entry) because the kernel reads V[k][cd] for kScatterK
-//    output rows per C gather; the schedule weights V-bank conflicts double.
+//    (encode_scatter_entry) because the kernel reads V[k][cd] for K output
+//    rows per C gather; the schedule weights V-bank conflicts 8x.
 void build_mixed_sell(Handle& h, SellTable& st, int M, int format) {
     ChannelTables& b = h.ch[1];
     const uint32_t nb = static_cast<uint32_t>(b.n);
@@ -346,7 +346,16 @@ void build_mixed_sell(Handle& h, SellTable& st, int M, int format) {
     uint32_t cap = 32766;   // 18-bit byte offsets
     if (const char* e = std::getenv("DETCI_MIXED_MAX_SEG")) cap = std::max(2, std::atoi(e)) & ~1u;
     const uint32_t wdbl = (2 * nn + 1) & ~1u;
-    const uint32_t budget = format == 2 ? kScatterSmem / 8 - kScatterK * scatter_vpitch(n)
+    if (format == 2) {
+        // K = 16 output rows per CTA when that costs no extra row segments
+        auto nseg_for = [&](int K) {
+            const int64_t room = static_cast<int64_t>(kScatterSmem / 8) - K * static_cast<int64_t>(scatter_vpitch(n));
+            const uint32_t seg = std::min<uint32_t>(cap, static_cast<uint32_t>(std::max<int64_t>(room, 2) / M) & ~1u);
+            return (nb + seg - 1) / seg;
+        };
+        st.kmax = nseg_for(16) == nseg_for(8) ? 16 : 8;
+    }
+    const uint32_t budget = format == 2 ? kScatterSmem / 8 - st.kmax * scatter_vpitch(n)
                                         : 220u * 1024 / 8 - 2 * wdbl;   // doubles for C stages
     const uint32_t single_seg = std::min<uint32_t>(cap, (budget / M) & ~1u);
     const uint32_t double_seg = std::min<uint32_t>(std::min<uint32_t>(16000, cap), (budget / 2 / M) & ~1u);
@@ -360,7 +369,9 @@ void build_mixed_sell(Handle& h, SellTable& st, int M, int format) {
     st.nseg = (nb + max_seg - 1) / max_seg;
     if (st.nseg > 16) fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: more than 16 column segments");
     if (2 * nn >= (1u << 14)) fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: +-W index exceeds 14 bits");
-    const int wv = format == 2 ? 2 : 1;   // weight of a V/W bank conflict in the schedule
+    // weight of a V/W bank conflict in the schedule: the scatter kernel reads
+    // V once per output row (~8 per C gather on average)
+    const int wv = format == 2 ? 8 : 1;
     st.seg_cols = (nb + st.nseg - 1) / st.nseg;
     if (static_cast<uint64_t>(st.seg_cols) * 8 >= (1u << 18))
         fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: row segment exceeds the 18-bit entry offset");

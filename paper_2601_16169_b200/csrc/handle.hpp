@@ -23,9 +23,11 @@
 
 namespace detci_gpu {
 
-// Scatter formulation of the mixed term (sigma.cu k_mixed_scatter): output
-// alpha rows per CTA, shared-memory budget, V-table row pitch (doubles).
-constexpr int kScatterK = 8;
+// Scatter formulation of the mixed term (sigma.cu k_mixed_scatter): largest
+// number of output alpha rows per CTA (K classes 16, 8, 4, 2, 1), shared-memory
+// budget, V-table row pitch (doubles).
+constexpr int kScatterKMax = 16;
+constexpr int kScatterClasses = 5;
 constexpr uint32_t kScatterSmem = 226u * 1024;
 inline uint32_t scatter_vpitch(int n) { return static_cast<uint32_t>((n * n + 1) & ~1); }
 // DETCI_MIXED=gather selects the gather kernel (k_mixed) for M = 1.
@@ -83,17 +85,20 @@ struct SellTable {
     uint32_t seg_cols = 0, nseg = 0;
     bool double_buffer = true;         // C stages double-buffered (else one)
     int format = 1;                    // 1 gather (k_mixed), 2 scatter (k_mixed_scatter)
+    int kmax = 0;                      // format 2: largest K class (16 or 8)
     bool built = false;
 };
 
 // One output window of the scatter mixed term: alpha rows [i_lo, i_hi) of
 // this rank, whose D rows (one per (ia, position of ja in ia's singles list))
-// are sa_off[ia] - d_base; per alpha block b the CTA items (ja, kbeg | cnt <<
-// 24) with ja in the block and outputs ia_k in the window.
+// are sa_off[ia] - d_base; per alpha block b and K class c (K = 16 >> c) the
+// CTA items (ja, kbeg | K << 24) with ja in the block and outputs ia_k in the
+// window: each ja's list range is cut into chunks of kmax, the remainder
+// into its binary decomposition, so no CTA pads V rows.
 struct ScatterWindow {
     uint64_t i_lo = 0, i_hi = 0, d_base = 0, d_rows = 0;
     DevBuf<uint2> items;
-    std::vector<uint64_t> item_off;    // per block, size P + 1
+    std::vector<uint64_t> item_off;    // [b * kScatterClasses + c], size P * classes + 1
 };
 
 struct Handle {

@@ -999,21 +999,32 @@ const std::vector<std::unique_ptr<ScatterWindow>>& scatter_windows(Handle& h, in
         w->d_base = off[w->i_lo];
         w->d_rows = off[w->i_hi] - w->d_base;
         std::vector<uint2> items;
-        w->item_off.assign(P + 1, 0);
+        std::vector<std::vector<uint2>> cls(kScatterClasses);
+        w->item_off.assign(static_cast<size_t>(P) * kScatterClasses + 1, 0);
+        const uint32_t kmax = static_cast<uint32_t>(t.kmax);
         for (int b = 0; b < P; ++b) {
-            w->item_off[b] = items.size();
+            for (auto& c : cls) c.clear();
             for (uint64_t ja = h.blk[b]; ja < h.blk[b + 1]; ++ja) {
                 const uint32_t* f = flat + off[ja];
                 const uint32_t* e = flat + off[ja + 1];
-                const uint32_t p_lo = static_cast<uint32_t>(std::lower_bound(f, e, static_cast<uint32_t>(w->i_lo)) - f);
+                uint32_t p = static_cast<uint32_t>(std::lower_bound(f, e, static_cast<uint32_t>(w->i_lo)) - f);
                 const uint32_t p_hi = static_cast<uint32_t>(std::lower_bound(f, e, static_cast<uint32_t>(w->i_hi)) - f);
-                for (uint32_t p = p_lo; p < p_hi; p += kScatterK) {
-                    const uint32_t cnt = std::min<uint32_t>(kScatterK, p_hi - p);
-                    items.push_back(make_uint2(static_cast<uint32_t>(ja), p | cnt << 24));
+                for (int c = 0; c < kScatterClasses; ++c) {
+                    const uint32_t K = 16u >> c;
+                    if (K > kmax) continue;
+                    while (p_hi - p >= K) {
+                        cls[c].push_back(make_uint2(static_cast<uint32_t>(ja), p | K << 24));
+                        p += K;
+                        if (K < kmax) break;   // the remainder takes each smaller K at most once
+                    }
                 }
             }
+            for (int c = 0; c < kScatterClasses; ++c) {
+                w->item_off[static_cast<size_t>(b) * kScatterClasses + c] = items.size();
+                items.insert(items.end(), cls[c].begin(), cls[c].end());
+            }
         }
-        w->item_off[P] = items.size();
+        w->item_off[static_cast<size_t>(P) * kScatterClasses] = items.size();
         w->items.alloc(std::max<size_t>(items.size(), 1));
         if (!items.empty())
             CUDA_CHECK(cudaMemcpy(w->items.p, items.data(), items.size() * sizeof(uint2), cudaMemcpyHostToDevice));
@@ -1025,6 +1036,19 @@ const std::vector<std::unique_ptr<ScatterWindow>>& scatter_windows(Handle& h, in
     return wins;
 }
 
+template <int K>
+void launch_scatter_k(const ScatterArgs& a, uint64_t grid, uint32_t vpitch, size_t cbytes, cudaStream_t st) {
+    const size_t smem = static_cast<size_t>(K) * vpitch * sizeof(double) + cbytes;
+    static size_t configured = 0;
+    if (smem > configured) {
+        CUDA_CHECK(cudaFuncSetAttribute(k_mixed_scatter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+        configured = smem;
+    }
+    k_mixed_scatter<K><<<static_cast<unsigned>(grid), kMxBlock, smem, st>>>(a);
+    CUDA_LAUNCH_CHECK();
+}
+
 // Mixed term through the scatter kernel for block-rank g, held alpha block
 // b = rows [b0, b1) of Cs in Cb, outputs rows [a0, a1) of y_loc.
 void launch_mixed_scatter(Handle& h, int g, int P, int b, const double* Cb, uint32_t b0, uint32_t b1,
@@ -1033,21 +1057,14 @@ void launch_mixed_scatter(Handle& h, int g, int P, int b, const double* Cb, uint
     const auto& wins = scatter_windows(h, g, P);
     const uint32_t ldd = h.nslices * kWarp;
     const uint32_t vpitch = scatter_vpitch(h.norbs);
-    const size_t smem = (static_cast<size_t>(kScatterK) * vpitch + ((t.seg_cols + 1) & ~1u)) * sizeof(double);
-    static size_t configured = 0;
-    if (smem > configured) {
-        CUDA_CHECK(cudaFuncSetAttribute(k_mixed_scatter<kScatterK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem)));
-        configured = smem;
-    }
+    const size_t cbytes = ((t.seg_cols + 1) & ~1u) * sizeof(double);
     for (const auto& w : wins) {
-        const uint64_t i0 = w->item_off[b], i1 = w->item_off[b + 1];
-        if (i1 == i0) continue;
+        const size_t base = static_cast<size_t>(b) * kScatterClasses;
+        if (w->item_off[base + kScatterClasses] == w->item_off[base]) continue;
         ScatterArgs a{};
         a.C = Cb;
         a.ldc = h.nb();
         a.c_row0 = b0;
-        a.items = w->items.p + i0;
         a.nparts = (ldd + kMxBlock - 1) / kMxBlock;
         a.nslices = h.nslices;
         a.nb = static_cast<uint32_t>(h.nb());
@@ -1066,10 +1083,20 @@ void launch_mixed_scatter(Handle& h, int g, int P, int b, const double* Cb, uint
         a.D = h.dbuf.p;
         a.d_base = w->d_base;
         a.ldd = ldd;
-        const uint64_t grid = (i1 - i0) * a.nparts;
-        if (grid >= (1ull << 31)) fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: scatter grid too large");
-        k_mixed_scatter<kScatterK><<<static_cast<unsigned>(grid), kMxBlock, smem, h.stream>>>(a);
-        CUDA_LAUNCH_CHECK();
+        for (int c = 0; c < kScatterClasses; ++c) {
+            const uint64_t i0 = w->item_off[base + c], i1 = w->item_off[base + c + 1];
+            if (i1 == i0) continue;
+            a.items = w->items.p + i0;
+            const uint64_t grid = (i1 - i0) * a.nparts;
+            if (grid >= (1ull << 31)) fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: scatter grid too large");
+            switch (c) {
+                case 0: launch_scatter_k<16>(a, grid, vpitch, cbytes, h.stream); break;
+                case 1: launch_scatter_k<8>(a, grid, vpitch, cbytes, h.stream); break;
+                case 2: launch_scatter_k<4>(a, grid, vpitch, cbytes, h.stream); break;
+                case 3: launch_scatter_k<2>(a, grid, vpitch, cbytes, h.stream); break;
+                default: launch_scatter_k<1>(a, grid, vpitch, cbytes, h.stream); break;
+            }
+        }
 
         ReduceArgs r{};
         r.D = h.dbuf.p;

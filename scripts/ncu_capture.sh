@@ -10,6 +10,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   python bench.py --config $CFG --steps 2 --warmup 3 --no-davidson --no-cpu-baseline > gpurun_out/launches_bench_${CFG}_${TAG}.json 2>&1
 # 2. full capture of every sigma kernel once (skip the warm-up launches)
 timeout 1200 ncu --set full --clock-control none --import-source on \
-  -k regex:"k_mixed|k_samespin|k_transpose" -c 6 \
+  -k regex:"k_mixed|k_samespin|k_eps|k_transpose" -c 10 \
   -o gpurun_out/full_${CFG}_${TAG} python scripts/profile_sigma.py $CFG 1 > gpurun_out/full_${CFG}_${TAG}.log 2>&1
 tail -2 gpurun_out/full_${CFG}_${TAG}.log
