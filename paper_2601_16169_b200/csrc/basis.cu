@@ -353,7 +353,8 @@ void build_mixed_sell(Handle& h, SellTable& st, int M, int format) {
             const uint32_t seg = std::min<uint32_t>(cap, static_cast<uint32_t>(std::max<int64_t>(room, 2) / M) & ~1u);
             return (nb + seg - 1) / seg;
         };
-        st.kmax = nseg_for(16) == nseg_for(8) ? 16 : 8;
+        // (M = 2 keeps K <= 8: 2 x K accumulators per thread)
+        st.kmax = (M == 1 && nseg_for(16) == nseg_for(8)) ? 16 : 8;
     }
     const uint32_t budget = format == 2 ? kScatterSmem / 8 - st.kmax * scatter_vpitch(n)
                                         : 220u * 1024 / 8 - 2 * wdbl;   // doubles for C stages
@@ -608,11 +609,11 @@ const SellTable& mixed_table(Handle& h, int M) {
     return t;
 }
 
-const SellTable& scatter_table(Handle& h) {
-    SellTable& t = h.sell_scatter;
+const SellTable& scatter_table(Handle& h, int M) {
+    SellTable& t = h.sell_scatter[M == 2 ? 1 : 0];
     if (!t.built) {
-        build_mixed_sell(h, t, 1, 2);
-        build_scatter_tpos(h);
+        build_mixed_sell(h, t, M == 2 ? 2 : 1, 2);
+        if (!h.tpos.p) build_scatter_tpos(h);
     }
     return t;
 }
@@ -633,6 +634,7 @@ void build_scatter_tpos(Handle& h) {
 void release_sigma_scratch(Handle& h) {
     h.dbuf.reset();
     h.dcap_rows = 0;
+    h.dplan_m = 0;
     h.scatter_plan.clear();
 }
 
@@ -647,7 +649,7 @@ void release_basis(Handle& h) {
         t.pab.reset();
         t.J.reset();
     }
-    for (SellTable* tp : {&h.sell_m[0], &h.sell_m[1], &h.sell_m[2], &h.sell_scatter}) {
+    for (SellTable* tp : {&h.sell_m[0], &h.sell_m[1], &h.sell_m[2], &h.sell_scatter[0], &h.sell_scatter[1]}) {
         SellTable& t = *tp;
         t.sell.reset();
         t.off.reset();
@@ -687,7 +689,7 @@ void build_device_basis(Handle& h) {
                                        " bytes, budget is " + std::to_string(budget) + " bytes");
 
     for (int c = 0; c < 2; ++c) build_pair_tables(h, c);
-    if (mixed_scatter_enabled()) scatter_table(h);
+    if (mixed_scatter_enabled()) scatter_table(h, 1);
     else build_mixed_sell(h, h.sell_m[0], 1, 1);
     build_diag(h);
     const size_t scratch = static_cast<size_t>(h.max_blk) * h.nb();

@@ -97,8 +97,8 @@ struct SellTable {
 // into its binary decomposition, so no CTA pads V rows.
 struct ScatterWindow {
     uint64_t i_lo = 0, i_hi = 0, d_base = 0, d_rows = 0;
-    DevBuf<uint2> items;
-    std::vector<uint64_t> item_off;    // [b * kScatterClasses + c], size P * classes + 1
+    DevBuf<uint2> items[2];            // [0] kmax 16, [1] kmax 8 (built on demand)
+    std::vector<uint64_t> item_off[2]; // [b * kScatterClasses + c], size P * classes + 1
 };
 
 struct Handle {
@@ -122,7 +122,7 @@ struct Handle {
     // segmentation per vector count M in {1, 2, 4} (the staged C rows of M
     // vectors share the CTA's shared memory), built on first use
     SellTable sell_m[3];
-    SellTable sell_scatter;            // format 2, M = 1
+    SellTable sell_scatter[2];         // format 2, M = 1, 2
     DevBuf<uint32_t> sell_perm;        // slot -> beta string (degree-sorted)
     // scatter mixed term: tpos[sa_off[ja] + k] = position of ja in the
     // singles list of its k-th single ia; host copies of the alpha singles;
@@ -132,7 +132,8 @@ struct Handle {
     std::vector<uint64_t> h_sa_off;
     std::vector<std::vector<std::unique_ptr<ScatterWindow>>> scatter_plan;
     DevBuf<double> dbuf;               // D partials of the current window
-    uint64_t dcap_rows = 0;            // D rows that fit (set with the plan)
+    uint64_t dcap_rows = 0;            // D rows per vector that fit (set with the plan)
+    int dplan_m = 0;                   // vectors per pass the plan reserved D for
     uint32_t nslices = 0;
 
     // alpha-block partition: P = world (NCCL) or vblocks (virtual)
@@ -167,7 +168,7 @@ void plan_partition(uint64_t na, uint64_t nb, const uint32_t* sa, const uint32_t
                     const uint32_t* sb, const uint32_t* db, int P, int weighted, uint64_t* blk);
 void build_device_basis(Handle& h);
 const SellTable& mixed_table(Handle& h, int M);   // M in {1, 2, 4}
-const SellTable& scatter_table(Handle& h);
+const SellTable& scatter_table(Handle& h, int M);   // M in {1, 2}
 void release_basis(Handle& h);
 void build_scatter_tpos(Handle& h);
 // Drop the scatter D buffer and windows (re-planned against the free memory

@@ -553,7 +553,7 @@ k_mixed(const MixedArgs a) {
 // is deterministic without atomics.
 // ---------------------------------------------------------------------------
 struct ScatterArgs {
-    const double* C;            // Cs row ja at C + (ja - c_row0) * ldc
+    const double* C[2];         // Cs_v row ja at C[v] + (ja - c_row0) * ldc
     size_t ldc;
     uint32_t c_row0;
     const uint2* items;         // (ja, kbeg | cnt << 24)
@@ -567,17 +567,19 @@ struct ScatterArgs {
     const uint32_t* sell_len;
     const double* eri;
     int norbs;
-    double* D;                  // D row (sa_off[ia] + pos - d_base), ldd slots
+    double* D[2];               // D_v row (sa_off[ia] + pos - d_base), ldd slots
     uint64_t d_base;
     uint32_t ldd;
 };
 
-template <int K>
+// M = 1 or 2 vectors share the V gathers (the multi-root block's pairs):
+// an element then costs (M + K) / (M K) gathers per FMA.
+template <int K, int M>
 __global__ void __launch_bounds__(kMxBlock, 1)
 k_mixed_scatter(const ScatterArgs a) {
     extern __shared__ double smem[];
     double* const vsub = smem;                      // K rows of vpitch
-    double* const cseg = smem + K * a.vpitch;       // Cs[ja, segment]
+    double* const cseg = smem + K * a.vpitch;       // Cs_v[ja, segment], v < M
     __shared__ uint64_t s_vrow[K];                  // eri row offset | sign << 63
     __shared__ uint64_t s_drow[K];                  // D row of output k
 
@@ -587,6 +589,7 @@ k_mixed_scatter(const ScatterArgs a) {
     const uint64_t oja = a.sa_off[ja];
     const int n = a.norbs, nn = n * n;
     const uint32_t tid = threadIdx.x, lane = tid % kWarp;
+    const uint32_t segpad = (a.seg_cols + 1) & ~1u;
 
     if (tid < K) {
         uint64_t vr = ~0ull, dr = 0;
@@ -616,20 +619,41 @@ k_mixed_scatter(const ScatterArgs a) {
     const uint32_t slot = part * kMxBlock + tid;
     const uint32_t sl = slot / kWarp;
     const bool active = sl < a.nslices;
-    double acc[K];
+    double acc[M][K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) acc[k] = 0.0;
+    for (int v = 0; v < M; ++v)
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc[v][k] = 0.0;
     const char* vb = reinterpret_cast<const char*>(vsub);
     const char* cb = reinterpret_cast<const char*>(cseg);
-    const uint32_t vstride = a.vpitch * 8;
-    const double* crow = a.C + static_cast<size_t>(ja - a.c_row0) * a.ldc;
+    const uint32_t vstride = a.vpitch * 8, cstride = segpad * 8;
+    const size_t crow = static_cast<size_t>(ja - a.c_row0) * a.ldc;
+
+    auto element = [&](uint32_t e) {
+        const char* cp = cb + (e & 0x3ffffu);
+        double c[M];
+#pragma unroll
+        for (int v = 0; v < M; ++v)
+            c[v] = xor_sign(*reinterpret_cast<const double*>(cp + v * cstride), e & 0x80000000u);
+        const char* vp = vb + ((e >> 15) & 0x7ff8u);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const double w = *reinterpret_cast<const double*>(vp + k * vstride);
+#pragma unroll
+            for (int v = 0; v < M; ++v) acc[v][k] = fma(w, c[v], acc[v][k]);
+        }
+    };
 
 #pragma unroll 1
     for (uint32_t g = 0; g < a.nseg; ++g) {
         if (g > 0) __syncthreads();   // previous segment consumed
         const uint32_t segw = min(a.seg_cols, a.nb - g * a.seg_cols);
-        const double* src = crow + static_cast<size_t>(g) * a.seg_cols;
-        for (uint32_t c = tid; c < segw; c += kMxBlock) cp_async8(cseg + c, src + c);
+#pragma unroll
+        for (int v = 0; v < M; ++v) {
+            const double* src = a.C[v] + crow + static_cast<size_t>(g) * a.seg_cols;
+            double* dst = cseg + v * segpad;
+            for (uint32_t c = tid; c < segw; c += kMxBlock) cp_async8(dst + c, src + c);
+        }
         cp_async_commit();
         cp_async_wait_all();
         __syncthreads();
@@ -643,28 +667,17 @@ k_mixed_scatter(const ScatterArgs a) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) e[u] = __ldg(ent + static_cast<size_t>(t + u) * kWarp);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const double c = xor_sign(*reinterpret_cast<const double*>(cb + (e[u] & 0x3ffffu)), e[u] & 0x80000000u);
-                const char* v = vb + ((e[u] >> 15) & 0x7ff8u);
-#pragma unroll
-                for (int k = 0; k < K; ++k)
-                    acc[k] = fma(*reinterpret_cast<const double*>(v + k * vstride), c, acc[k]);
-            }
+            for (int u = 0; u < 4; ++u) element(e[u]);
         }
 #pragma unroll 1
-        for (; t < L; ++t) {
-            const uint32_t e0 = __ldg(ent + static_cast<size_t>(t) * kWarp);
-            const double c = xor_sign(*reinterpret_cast<const double*>(cb + (e0 & 0x3ffffu)), e0 & 0x80000000u);
-            const char* v = vb + ((e0 >> 15) & 0x7ff8u);
-#pragma unroll
-            for (int k = 0; k < K; ++k)
-                acc[k] = fma(*reinterpret_cast<const double*>(v + k * vstride), c, acc[k]);
-        }
+        for (; t < L; ++t) element(__ldg(ent + static_cast<size_t>(t) * kWarp));
     }
     if (!active) return;
 #pragma unroll
     for (int k = 0; k < K; ++k)
-        if (k < static_cast<int>(cnt)) a.D[s_drow[k] * a.ldd + slot] = acc[k];
+        if (k < static_cast<int>(cnt))
+#pragma unroll
+            for (int v = 0; v < M; ++v) a.D[v][s_drow[k] * a.ldd + slot] = acc[v][k];
 }
 
 // y[ia, ib] += eps(A_ia, B_ib) sum_{pos in [lo, hi)} D[sa_off[ia] + pos - d_base, slot]
@@ -964,44 +977,52 @@ void launch_mixed(Handle& h, const Ptrs& Cb, uint32_t b0, uint32_t b1, const MPt
 }
 
 // Scatter plan for block-rank g (rows [blk[g], blk[g+1])): output windows
-// whose D fits the capacity, and per window and alpha block the CTA items.
-// D capacity: DETCI_MIXED_DBYTES if set (tests force several windows), else
-// 60% of the free device memory at the first sigma (release_sigma_scratch
-// re-plans after the Davidson solvers allocate their subspace).
-const std::vector<std::unique_ptr<ScatterWindow>>& scatter_windows(Handle& h, int g, int P) {
-    const SellTable& t = scatter_table(h);
-    (void)t;
+// whose D fits the capacity, and per window, K grid (kmax 16 or 8) and alpha
+// block the CTA items.  D capacity: DETCI_MIXED_DBYTES if set (tests force
+// several windows), else 60% of the free device memory at the first sigma,
+// shared by the M vectors of a pass (release_sigma_scratch re-plans after
+// the Davidson solvers allocate their subspace, and a pass with more vectors
+// than the plan reserved for re-plans).
+const std::vector<std::unique_ptr<ScatterWindow>>& scatter_windows(Handle& h, int g, int P, int M, int kmax) {
+    const uint64_t ldd = static_cast<uint64_t>(h.nslices) * kWarp;
+    if (h.dplan_m != 0 && h.dplan_m < M) release_sigma_scratch(h);
     if (h.scatter_plan.size() != static_cast<size_t>(P)) {
         h.scatter_plan.clear();
         h.scatter_plan.resize(P);
     }
-    auto& wins = h.scatter_plan[g];
-    if (!wins.empty()) return wins;
-    const uint64_t ldd = static_cast<uint64_t>(h.nslices) * kWarp;
     const uint64_t* off = h.h_sa_off.data();
     const uint32_t* flat = h.h_sa_flat.data();
     if (h.dcap_rows == 0) {
         size_t fr = 0, tot = 0;
         CUDA_CHECK(cudaMemGetInfo(&fr, &tot));
-        uint64_t bytes = static_cast<uint64_t>(0.6 * static_cast<double>(fr));
+        uint64_t bytes = static_cast<uint64_t>(0.6 * static_cast<double>(fr + h.dbuf.bytes()));
         if (const char* e = std::getenv("DETCI_MIXED_DBYTES")) bytes = std::strtoull(e, nullptr, 10);
+        h.dbuf.reset();
         uint64_t maxlen = 1;
         for (size_t i = 0; i < h.na(); ++i) maxlen = std::max<uint64_t>(maxlen, off[i + 1] - off[i]);
-        h.dcap_rows = std::max<uint64_t>(bytes / (ldd * 8), maxlen);
+        h.dcap_rows = std::max<uint64_t>(bytes / (ldd * 8 * M), maxlen);
+        h.dplan_m = M;
     }
-    const uint64_t r0 = h.blk[g], r1 = h.blk[g + 1];
-    uint64_t i = r0;
-    while (i < r1) {
-        auto w = std::make_unique<ScatterWindow>();
-        w->i_lo = i;
-        while (i < r1 && (i == w->i_lo || off[i + 1] - off[w->i_lo] <= h.dcap_rows)) ++i;
-        w->i_hi = i;
-        w->d_base = off[w->i_lo];
-        w->d_rows = off[w->i_hi] - w->d_base;
+    auto& wins = h.scatter_plan[g];
+    if (wins.empty()) {
+        const uint64_t r0 = h.blk[g], r1 = h.blk[g + 1];
+        uint64_t i = r0;
+        while (i < r1) {
+            auto w = std::make_unique<ScatterWindow>();
+            w->i_lo = i;
+            while (i < r1 && (i == w->i_lo || off[i + 1] - off[w->i_lo] <= h.dcap_rows)) ++i;
+            w->i_hi = i;
+            w->d_base = off[w->i_lo];
+            w->d_rows = off[w->i_hi] - w->d_base;
+            wins.push_back(std::move(w));
+        }
+    }
+    const int ki = kmax == 16 ? 0 : 1;
+    for (auto& w : wins) {
+        if (!w->item_off[ki].empty()) continue;
         std::vector<uint2> items;
         std::vector<std::vector<uint2>> cls(kScatterClasses);
-        w->item_off.assign(static_cast<size_t>(P) * kScatterClasses + 1, 0);
-        const uint32_t kmax = static_cast<uint32_t>(t.kmax);
+        w->item_off[ki].assign(static_cast<size_t>(P) * kScatterClasses + 1, 0);
         for (int b = 0; b < P; ++b) {
             for (auto& c : cls) c.clear();
             for (uint64_t ja = h.blk[b]; ja < h.blk[b + 1]; ++ja) {
@@ -1011,58 +1032,63 @@ const std::vector<std::unique_ptr<ScatterWindow>>& scatter_windows(Handle& h, in
                 const uint32_t p_hi = static_cast<uint32_t>(std::lower_bound(f, e, static_cast<uint32_t>(w->i_hi)) - f);
                 for (int c = 0; c < kScatterClasses; ++c) {
                     const uint32_t K = 16u >> c;
-                    if (K > kmax) continue;
+                    if (K > static_cast<uint32_t>(kmax)) continue;
                     while (p_hi - p >= K) {
                         cls[c].push_back(make_uint2(static_cast<uint32_t>(ja), p | K << 24));
                         p += K;
-                        if (K < kmax) break;   // the remainder takes each smaller K at most once
+                        if (K < static_cast<uint32_t>(kmax)) break;   // remainder: each smaller K at most once
                     }
                 }
             }
             for (int c = 0; c < kScatterClasses; ++c) {
-                w->item_off[static_cast<size_t>(b) * kScatterClasses + c] = items.size();
+                w->item_off[ki][static_cast<size_t>(b) * kScatterClasses + c] = items.size();
                 items.insert(items.end(), cls[c].begin(), cls[c].end());
             }
         }
-        w->item_off[static_cast<size_t>(P) * kScatterClasses] = items.size();
-        w->items.alloc(std::max<size_t>(items.size(), 1));
+        w->item_off[ki][static_cast<size_t>(P) * kScatterClasses] = items.size();
+        w->items[ki].alloc(std::max<size_t>(items.size(), 1));
         if (!items.empty())
-            CUDA_CHECK(cudaMemcpy(w->items.p, items.data(), items.size() * sizeof(uint2), cudaMemcpyHostToDevice));
-        wins.push_back(std::move(w));
+            CUDA_CHECK(cudaMemcpy(w->items[ki].p, items.data(), items.size() * sizeof(uint2), cudaMemcpyHostToDevice));
     }
     uint64_t need = 0;
     for (auto& w : wins) need = std::max(need, w->d_rows);
-    if (h.dbuf.n < need * ldd) h.dbuf.alloc(need * ldd);
+    if (h.dbuf.n < need * ldd * M) h.dbuf.alloc(need * ldd * M);
     return wins;
 }
 
-template <int K>
+template <int K, int M>
 void launch_scatter_k(const ScatterArgs& a, uint64_t grid, uint32_t vpitch, size_t cbytes, cudaStream_t st) {
-    const size_t smem = static_cast<size_t>(K) * vpitch * sizeof(double) + cbytes;
+    const size_t smem = static_cast<size_t>(K) * vpitch * sizeof(double) + M * cbytes;
     static size_t configured = 0;
     if (smem > configured) {
-        CUDA_CHECK(cudaFuncSetAttribute(k_mixed_scatter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CUDA_CHECK(cudaFuncSetAttribute(k_mixed_scatter<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
         configured = smem;
     }
-    k_mixed_scatter<K><<<static_cast<unsigned>(grid), kMxBlock, smem, st>>>(a);
+    k_mixed_scatter<K, M><<<static_cast<unsigned>(grid), kMxBlock, smem, st>>>(a);
     CUDA_LAUNCH_CHECK();
 }
 
 // Mixed term through the scatter kernel for block-rank g, held alpha block
 // b = rows [b0, b1) of Cs in Cb, outputs rows [a0, a1) of y_loc.
-void launch_mixed_scatter(Handle& h, int g, int P, int b, const double* Cb, uint32_t b0, uint32_t b1,
-                          double* y_loc, uint64_t a0) {
-    const SellTable& t = scatter_table(h);
-    const auto& wins = scatter_windows(h, g, P);
+template <int M>
+void launch_mixed_scatter(Handle& h, int g, int P, int b, const Ptrs& Cb, uint32_t b0, uint32_t b1,
+                          const MPtrs& y_loc, uint64_t a0) {
+    const SellTable& t = scatter_table(h, M);
+    const auto& wins = scatter_windows(h, g, P, M, t.kmax);
+    const int ki = t.kmax == 16 ? 0 : 1;
     const uint32_t ldd = h.nslices * kWarp;
     const uint32_t vpitch = scatter_vpitch(h.norbs);
     const size_t cbytes = ((t.seg_cols + 1) & ~1u) * sizeof(double);
     for (const auto& w : wins) {
         const size_t base = static_cast<size_t>(b) * kScatterClasses;
-        if (w->item_off[base + kScatterClasses] == w->item_off[base]) continue;
+        const auto& io = w->item_off[ki];
+        if (io[base + kScatterClasses] == io[base]) continue;
         ScatterArgs a{};
-        a.C = Cb;
+        for (int v = 0; v < M; ++v) {
+            a.C[v] = Cb[v];
+            a.D[v] = h.dbuf.p + static_cast<size_t>(v) * w->d_rows * ldd;
+        }
         a.ldc = h.nb();
         a.c_row0 = b0;
         a.nparts = (ldd + kMxBlock - 1) / kMxBlock;
@@ -1080,45 +1106,45 @@ void launch_mixed_scatter(Handle& h, int g, int P, int b, const double* Cb, uint
         a.sell_len = t.len.p;
         a.eri = h.d_eri.p;
         a.norbs = h.norbs;
-        a.D = h.dbuf.p;
         a.d_base = w->d_base;
         a.ldd = ldd;
         for (int c = 0; c < kScatterClasses; ++c) {
-            const uint64_t i0 = w->item_off[base + c], i1 = w->item_off[base + c + 1];
+            const uint64_t i0 = io[base + c], i1 = io[base + c + 1];
             if (i1 == i0) continue;
-            a.items = w->items.p + i0;
+            a.items = w->items[ki].p + i0;
             const uint64_t grid = (i1 - i0) * a.nparts;
             if (grid >= (1ull << 31)) fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: scatter grid too large");
             switch (c) {
-                case 0: launch_scatter_k<16>(a, grid, vpitch, cbytes, h.stream); break;
-                case 1: launch_scatter_k<8>(a, grid, vpitch, cbytes, h.stream); break;
-                case 2: launch_scatter_k<4>(a, grid, vpitch, cbytes, h.stream); break;
-                case 3: launch_scatter_k<2>(a, grid, vpitch, cbytes, h.stream); break;
-                default: launch_scatter_k<1>(a, grid, vpitch, cbytes, h.stream); break;
+                case 0: launch_scatter_k<16, 1>(a, grid, vpitch, cbytes, h.stream); break;  // kmax 16 => M == 1
+                case 1: launch_scatter_k<8, M>(a, grid, vpitch, cbytes, h.stream); break;
+                case 2: launch_scatter_k<4, M>(a, grid, vpitch, cbytes, h.stream); break;
+                case 3: launch_scatter_k<2, M>(a, grid, vpitch, cbytes, h.stream); break;
+                default: launch_scatter_k<1, M>(a, grid, vpitch, cbytes, h.stream); break;
             }
         }
-
-        ReduceArgs r{};
-        r.D = h.dbuf.p;
-        r.d_base = w->d_base;
-        r.ldd = ldd;
-        r.nb = a.nb;
-        r.nparts = (a.nb + kRedBlock - 1) / kRedBlock;
-        r.i_lo = static_cast<uint32_t>(w->i_lo);
-        r.j0 = b0;
-        r.j1 = b1;
-        r.sa_flat = a.sa_flat;
-        r.sa_off = a.sa_off;
-        r.sa_len = h.ch[0].len[0].p;
-        r.alpha = a.alpha;
-        r.beta_prefix = h.ch[1].prefix.p;
-        r.perm = h.sell_perm.p;
-        r.Y = y_loc;
-        r.ldy = h.nb();
-        r.y_row0 = static_cast<uint32_t>(a0);
-        const uint64_t rgrid = (w->i_hi - w->i_lo) * r.nparts;
-        k_mixed_reduce<<<static_cast<unsigned>(rgrid), kRedBlock, 0, h.stream>>>(r);
-        CUDA_LAUNCH_CHECK();
+        for (int v = 0; v < M; ++v) {
+            ReduceArgs r{};
+            r.D = a.D[v];
+            r.d_base = w->d_base;
+            r.ldd = ldd;
+            r.nb = a.nb;
+            r.nparts = (a.nb + kRedBlock - 1) / kRedBlock;
+            r.i_lo = static_cast<uint32_t>(w->i_lo);
+            r.j0 = b0;
+            r.j1 = b1;
+            r.sa_flat = a.sa_flat;
+            r.sa_off = a.sa_off;
+            r.sa_len = h.ch[0].len[0].p;
+            r.alpha = a.alpha;
+            r.beta_prefix = h.ch[1].prefix.p;
+            r.perm = h.sell_perm.p;
+            r.Y = y_loc[v];
+            r.ldy = h.nb();
+            r.y_row0 = static_cast<uint32_t>(a0);
+            const uint64_t rgrid = (w->i_hi - w->i_lo) * r.nparts;
+            k_mixed_reduce<<<static_cast<unsigned>(rgrid), kRedBlock, 0, h.stream>>>(r);
+            CUDA_LAUNCH_CHECK();
+        }
     }
 }
 
@@ -1230,8 +1256,8 @@ void sigma_ring(Handle& h, int g, int P, const Ptrs& x_loc, const MPtrs& xs_loc,
         launch_alpha<M>(h, held, b0, b1, x_loc, y_loc, a0, a1, s == 0);
         tm.end(id);
         id = tm.begin(2);
-        if (M == 1 && mixed_scatter_enabled())
-            launch_mixed_scatter(h, g, P, b, held[0], b0, b1, y_loc[0], a0);
+        if (M <= 2 && mixed_scatter_enabled())
+            launch_mixed_scatter<M == 2 ? 2 : 1>(h, g, P, b, held, b0, b1, y_loc, a0);
         else
             launch_mixed<M>(h, held, b0, b1, y_loc, a0, a1);
         tm.end(id);
@@ -1321,9 +1347,9 @@ void sigma_block(Handle& h, const double* const* dx, double* const* dy, int m) {
     while (i < m) {
         Ptrs x{};
         MPtrs y{};
-        // pairs: M = 2 shares the W gather and SELL stream (-6..7% per vector
-        // at C2/C3); M = 4 shrinks the staged row segments 4x and loses
-        // (measured 1.35-1.6x slower per vector), so it is not used
+        // pairs: M = 2 shares the V gathers and SELL stream; M = 4 shrinks
+        // the staged row segments 4x and loses (measured 1.35-1.6x slower
+        // per vector with the gather kernel), so it is not used
         const int take = m - i >= 2 ? 2 : 1;
         for (int v = 0; v < take; ++v) {
             x[v] = dx[i + v];
