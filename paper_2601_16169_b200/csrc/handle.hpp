@@ -93,8 +93,9 @@ struct SellTable {
 // this rank, whose D rows (one per (ia, position of ja in ia's singles list))
 // are sa_off[ia] - d_base; per alpha block b and K class c (K = 16 >> c) the
 // CTA items (ja, kbeg | K << 24) with ja in the block and outputs ia_k in the
-// window: each ja's list range is cut into chunks of kmax, the remainder
-// into its binary decomposition, so no CTA pads V rows.
+// window: each ja's list range is cut into chunks of kmax and one remainder
+// CTA (zero V rows up to its class) or, DETCI_SCATTER_REM=binary, the
+// remainder's binary decomposition.
 struct ScatterWindow {
     uint64_t i_lo = 0, i_hi = 0, d_base = 0, d_rows = 0;
     DevBuf<uint2> items[2];            // [0] kmax 16, [1] kmax 8 (built on demand)

@@ -103,7 +103,7 @@ def main():
              "wf/LDS | issue % | occ % | FP64 pipe % | tensor % | regs | top stalls |",
              "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     summary = json.loads((PROF / "ncu_summary.json").read_text()) if (PROF / "ncu_summary.json").exists() else {}
-    cfg_sum = summary.setdefault(cfg, {})
+    cfg_sum = summary[cfg] = {}   # this capture replaces the config's entry
     for k in kernels:
         f = lambda key, fmt="{:.1f}": fmt.format(k[key]) if key in k else "-"  # noqa: E731
         stalls = ", ".join(f"{s} {v:.1f}" for v, s in k["top_stalls"])
