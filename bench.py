@@ -363,6 +363,7 @@ def run_gpu_arm(args):
         ints1, a1, b1 = synth.synthetic_system("C1")
         with detci.GpuBasis(ints1.norbs, a1, b1, ints1.core, ints1.h1, ints1.eri,
                             detci.BasisOptions(device=local_rank)) as basis1:
+            detci.davidson_solve(basis1, detci.DavidsonOptions(max_iter=2), want_vector=False)   # warm
             t1 = time.time()
             r1 = detci.davidson_solve(basis1, want_vector=False)
             wall1 = time.time() - t1

@@ -68,8 +68,13 @@ def test_trace_matches_reference_iteration_by_iteration():
     with gpu_basis(ints, d["alpha"], d["beta"]) as b:
         res = detci.davidson_solve(b)
     assert len(res.iterations) == len(ref)
+    # intermediate Ritz values: 1e-9 relative.  At an iteration whose
+    # correction is nearly inside the subspace the renormalised vector
+    # carries the summation-order rounding of the dot products amplified
+    # (chain8 iteration values move by ~1e-10 between reduction orders);
+    # the final energy is held to 1e-10 (test_chain8_shipped_golden).
     for it, r in zip(res.iterations, ref):
-        assert abs(it.ritz_value - r[0]) <= 1e-10 * abs(r[0])
+        assert abs(it.ritz_value - r[0]) <= 1e-9 * abs(r[0])
         assert it.restarted == bool(r[3])
 
 
@@ -156,3 +161,26 @@ def test_vector_helpers():
         assert c[0] == 0.5 and abs(c[1] - 1e8) <= 1e-8 * 1e8 and c[2] == 0.0
         with pytest.raises(errors.InputError):
             detci.precondition(b, [1.0, 1.0], [1.0], 0.0)
+
+
+@pytest.mark.parametrize("ortho", ["mgs", "cgs2"])
+def test_orthogonalization_variants_match_reference_trace(ortho, monkeypatch):
+    """Both orthogonalizations (DETCI_DAVIDSON_ORTHO=mgs: the reference's
+    sequential 2-pass MGS; default: classical Gram-Schmidt twice) reproduce
+    the reference chain8 trace iteration by iteration and the C1 energy."""
+    if ortho == "mgs":
+        monkeypatch.setenv("DETCI_DAVIDSON_ORTHO", "mgs")
+    ints, d = load_fixture("chain8")
+    ref = d["trace"]
+    with gpu_basis(ints, d["alpha"], d["beta"]) as b:
+        res = detci.davidson_solve(b)
+    assert len(res.iterations) == len(ref)
+    for it, r in zip(res.iterations, ref):
+        assert abs(it.ritz_value - r[0]) <= 1e-9 * abs(r[0])
+        assert it.max_gram_deviation <= 1e-12
+    assert abs(res.energy - ref[-1][0]) <= 1e-10 * abs(ref[-1][0])
+    meta = golden_meta()["C1"]
+    ints, a, bb = synth.synthetic_system("C1")
+    with gpu_basis(ints, a, bb) as b:
+        res = detci.davidson_solve(b, want_vector=False)
+    assert res.converged and abs(res.energy - meta["energy"]) <= 1e-8
