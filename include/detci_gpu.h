@@ -25,6 +25,9 @@
  *                                   LinearOperator apply_h (davidson.hpp:28,
  *                                   run.cpp:96-103)
  *   detci_gpu_davidson              davidson_solve (davidson.hpp:85-86)
+ *   detci_gpu_build_stored, _stored_arrays, _set_operator, _release_stored
+ *                                   build_stored_matrix / stored_matvec
+ *                                   (matvec.hpp:73-90), Method::Stored
  *   detci_gpu_inner_product, _orthonormalize, _precondition
  *                                   davidson.hpp:67-81 vector helpers
  *   detci_gpu_last_error            what() of the detci::Error thrown
@@ -222,6 +225,24 @@ int detci_gpu_davidson_roots(detci_gpu_handle* h, const detci_dav_block_opts* op
 /* m vectors through one blocked sigma: dx[i], dy[i] device pointers of the
  * local length (the multi-root Davidson's new block). */
 int detci_gpu_sigma_block(detci_gpu_handle* h, const double* const* dx, double* const* dy, int m);
+
+/* ---- stored-matrix method (Method::Stored) ------------
+ * build_stored_matrix (matvec.cpp:240-316): CSR of H in HBM with the
+ * reference's row layout -- row I = ia*nb + ib holds the diagonal, the alpha
+ * singles u doubles (ascending ja), the beta singles u doubles (ascending
+ * jb), then alpha singles x beta singles (ja-major) -- so row_offset and col
+ * are identical to the reference StoredMatrix.  Budget: required = nnz*12 +
+ * (dim+1)*8 bytes against memory_budget_bytes (0 = free device memory), else
+ * DETCI_GPU_E_CAPACITY with the reference message; dim > 2^32-1 is
+ * DETCI_GPU_E_CAPACITY too (matvec.cpp:245-246).  Single GPU only.
+ * set_operator(h, 1) makes every sigma call (sigma, sigma_device, the
+ * Davidson solvers) the stored SpMV (stored_matvec, matvec.cpp:318-332);
+ * set_operator(h, 0) returns to the matrix-free sigma. */
+int detci_gpu_build_stored(detci_gpu_handle* h, uint64_t memory_budget_bytes, uint64_t* nnz);
+int detci_gpu_stored_arrays(const detci_gpu_handle* h, uint64_t* row_offset /* dim+1 */,
+                            uint32_t* col /* nnz */, double* value /* nnz */);
+int detci_gpu_set_operator(detci_gpu_handle* h, int kind);   /* 0 matrix-free, 1 stored */
+int detci_gpu_release_stored(detci_gpu_handle* h);
 
 /* davidson.hpp:67-81 helpers on host arrays of length n (single GPU). */
 int detci_gpu_inner_product(detci_gpu_handle* h, const double* x, const double* y, uint64_t n,

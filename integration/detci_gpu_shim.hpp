@@ -4,6 +4,10 @@
 // keeping the reference signatures:
 //
 //   build_basis_gpu(const detci::Basis&)          device copy of a host Basis
+//   build_basis_gpu(alpha, beta, IntegralTable, BasisOptions)
+//                                                 build_basis (basis.hpp:85-86)
+//                                                 with tables + diag built on
+//                                                 the device
 //   matvec(DeviceBasis, x, y, MatvecTimings*)     matvec.hpp:64-65 (plan and
 //                                                 workers are scheduling-only
 //                                                 in the reference and have no
@@ -14,6 +18,7 @@
 // INTEGRATION.md shows the run.cpp hook (Method::Gpu) that uses these.
 #pragma once
 
+#include <chrono>
 #include <cstdint>
 #include <memory>
 #include <span>
@@ -24,6 +29,7 @@
 #include <detci/davidson.hpp>
 #include <detci/error.hpp>
 #include <detci/matvec.hpp>
+#include <detci/slater_condon.hpp>
 
 #include "../include/detci_gpu.h"
 
@@ -64,33 +70,16 @@ struct DeviceOptions {
 
 class DeviceBasis {
 public:
+    /// Device copy of a host Basis built by the reference build_basis.
     explicit DeviceBasis(const Basis& basis, const DeviceOptions& o = {}) {
-        detci_gpu_desc d{o.device, o.rank, o.world_size, o.nccl_id, o.virtual_blocks,
-                         o.weighted_partition ? 1 : 0, o.memory_budget_bytes};
-        rethrow(detci_gpu_create(&d, &h_), nullptr);
-        try {
-            const int n = basis.norbs;
-            const auto a = channel_masks(basis.alpha_strings, n);
-            const auto b = channel_masks(basis.beta_strings, n);
-            rethrow(detci_gpu_set_strings(h_, n, a.data(), a.size(), b.data(), b.size()), h_);
-            const std::size_t nn = static_cast<std::size_t>(n);
-            std::vector<double> h1(nn * nn), eri(nn * nn * nn * nn);
-            for (int p = 0; p < n; ++p)
-                for (int q = 0; q < n; ++q) h1[p * nn + q] = basis.integrals.one_electron(p, q);
-            for (int p = 0; p < n; ++p)
-                for (int q = 0; q < n; ++q)
-                    for (int r = 0; r < n; ++r)
-                        for (int s = 0; s < n; ++s)
-                            eri[((p * nn + q) * nn + r) * nn + s] = basis.integrals.two_electron(p, q, r, s);
-            rethrow(detci_gpu_set_integrals(h_, basis.integrals.core_energy(), h1.data(), eri.data()), h_);
-            rethrow(detci_gpu_build_basis(h_), h_);
-            std::uint64_t nb = 0;
-            rethrow(detci_gpu_local_rows(h_, &row_begin_, &row_end_, &nb), h_);
-            local_dim_ = (row_end_ - row_begin_) * nb;
-        } catch (...) {
-            detci_gpu_destroy(h_);
-            throw;
-        }
+        init(basis.norbs, channel_masks(basis.alpha_strings, basis.norbs),
+             channel_masks(basis.beta_strings, basis.norbs), basis.integrals, o);
+    }
+    /// Device basis straight from the string lists and integrals (the
+    /// host never builds tables, cache or diagonal).
+    DeviceBasis(int norbs, const std::vector<std::uint64_t>& a, const std::vector<std::uint64_t>& b,
+                const IntegralTable& table, const DeviceOptions& o = {}) {
+        init(norbs, a, b, table, o);
     }
     DeviceBasis(const DeviceBasis&) = delete;
     DeviceBasis& operator=(const DeviceBasis&) = delete;
@@ -98,8 +87,38 @@ public:
 
     detci_gpu_handle* handle() const { return h_; }
     std::size_t local_dimension() const { return local_dim_; }
+    std::uint64_t row_begin() const { return row_begin_; }
+    std::uint64_t row_end() const { return row_end_; }
 
 private:
+    void init(int n, const std::vector<std::uint64_t>& a, const std::vector<std::uint64_t>& b,
+              const IntegralTable& table, const DeviceOptions& o) {
+        detci_gpu_desc d{o.device, o.rank, o.world_size, o.nccl_id, o.virtual_blocks,
+                         o.weighted_partition ? 1 : 0, o.memory_budget_bytes};
+        rethrow(detci_gpu_create(&d, &h_), nullptr);
+        try {
+            rethrow(detci_gpu_set_strings(h_, n, a.data(), a.size(), b.data(), b.size()), h_);
+            const std::size_t nn = static_cast<std::size_t>(n);
+            std::vector<double> h1(nn * nn), eri(nn * nn * nn * nn);
+            for (int p = 0; p < n; ++p)
+                for (int q = 0; q < n; ++q) h1[p * nn + q] = table.one_electron(p, q);
+            for (int p = 0; p < n; ++p)
+                for (int q = 0; q < n; ++q)
+                    for (int r = 0; r < n; ++r)
+                        for (int s = 0; s < n; ++s)
+                            eri[((p * nn + q) * nn + r) * nn + s] = table.two_electron(p, q, r, s);
+            rethrow(detci_gpu_set_integrals(h_, table.core_energy(), h1.data(), eri.data()), h_);
+            rethrow(detci_gpu_build_basis(h_), h_);
+            std::uint64_t nb = 0;
+            rethrow(detci_gpu_local_rows(h_, &row_begin_, &row_end_, &nb), h_);
+            local_dim_ = (row_end_ - row_begin_) * nb;
+        } catch (...) {
+            detci_gpu_destroy(h_);
+            h_ = nullptr;
+            throw;
+        }
+    }
+
     detci_gpu_handle* h_ = nullptr;
     std::uint64_t row_begin_ = 0, row_end_ = 0;
     std::size_t local_dim_ = 0;
@@ -107,6 +126,62 @@ private:
 
 inline std::unique_ptr<DeviceBasis> build_basis_gpu(const Basis& basis, const DeviceOptions& o = {}) {
     return std::make_unique<DeviceBasis>(basis, o);
+}
+
+/// build_basis (basis.hpp:85-86, basis.cpp:78-148)
+/// end to end on the device.  The helper lists and the diagonal are built in
+/// HBM and copied back into a host Basis with the reference's field layout
+/// (strings repacked at the same bit_length, integrals, J/K, the four
+/// FlatExcitationTables, diag); the determinant cache is left empty, which the
+/// reference treats as "compute on the fly" (basis.hpp:63-70), and the
+/// budget check on it does not apply.  Errors follow build_basis: too many
+/// spin-orbitals, empty lists, bad popcounts and duplicates are InputError.
+struct GpuBuiltBasis {
+    std::unique_ptr<DeviceBasis> device;
+    Basis host;
+};
+
+inline GpuBuiltBasis build_basis_gpu(std::vector<BitString> alpha, std::vector<BitString> beta, IntegralTable table,
+                                     const BasisOptions& opts = {}, const DeviceOptions& o = {}) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const int n = table.norbs();
+    if (2 * n > kMaxKernelBits)
+        throw InputError("build_basis: " + std::to_string(2 * n) + " spin-orbitals exceed the kernel limit of " +
+                         std::to_string(kMaxKernelBits));
+    GpuBuiltBasis out;
+    out.device = std::make_unique<DeviceBasis>(n, channel_masks(alpha, n), channel_masks(beta, n), table, o);
+    detci_gpu_handle* h = out.device->handle();
+    Basis& B = out.host;
+    B.norbs = n;
+    const int bit_length = opts.bit_length != 0 ? opts.bit_length : (2 * n <= 64 ? 2 * n : 20);
+    B.channel_packing = make_packing(n, bit_length);
+    B.det_packing = make_packing(2 * n, bit_length);
+    B.alpha_strings.reserve(alpha.size());
+    B.beta_strings.reserve(beta.size());
+    for (const BitString& s : alpha) B.alpha_strings.push_back(repack(s, bit_length));
+    for (const BitString& s : beta) B.beta_strings.push_back(repack(s, bit_length));
+    B.n_elec_alpha = static_cast<int>(occupied_list(B.alpha_strings.front()).size());
+    B.n_elec_beta = static_cast<int>(occupied_list(B.beta_strings.front()).size());
+    B.integrals = std::move(table);
+    B.jk = build_direct_exchange(B.integrals);
+    FlatExcitationTable* tabs[2][2] = {{&B.singles_a, &B.doubles_a}, {&B.singles_b, &B.doubles_b}};
+    for (int ch = 0; ch < 2; ++ch)
+        for (int kind = 0; kind < 2; ++kind) {
+            std::uint64_t nflat = 0;
+            rethrow(detci_gpu_helper_size(h, ch, kind, &nflat), h);
+            FlatExcitationTable& t = *tabs[ch][kind];
+            const std::size_t ns = ch == 0 ? B.alpha_strings.size() : B.beta_strings.size();
+            std::vector<std::uint64_t> off(ns);
+            t.flat.resize(nflat);
+            t.len.resize(ns);
+            rethrow(detci_gpu_get_helpers(h, ch, kind, t.flat.data(), off.data(), t.len.data()), h);
+            t.offset.assign(off.begin(), off.end());
+        }
+    B.diag.resize(out.device->local_dimension());
+    rethrow(detci_gpu_diag(h, B.diag.data()), h);
+    B.stats.connectivity_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return out;
 }
 
 inline void matvec(const DeviceBasis& db, std::span<const double> x, std::span<double> y,

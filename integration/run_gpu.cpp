@@ -5,12 +5,17 @@
 //
 //   run_gpu <fcidump> [<det-list>]
 //
-// Prints three GROUND_ENERGY lines:
+// Prints GPU_BUILD (the device build_basis against the reference one) and
+// four GROUND_ENERGY lines:
 //   reference   davidson_solve over the reference matvec (CPU)
 //   mixed       the reference davidson_solve over the device sigma through
 //               detci::LinearOperator (SURVEY.md 7.2.7 "mixed oracle")
 //   device      the device-resident Davidson (detci_gpu_davidson)
+//   gpu_built   the reference davidson_solve over build_basis_gpu's basis
+//               (tables and diagonal built on the device)
+#include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <fstream>
 #include <random>
@@ -46,7 +51,33 @@ int main(int argc, char** argv) {
             alpha = full_channel_strings(table.norbs(), na);
             beta = full_channel_strings(table.norbs(), nb);
         }
+        const IntegralTable table_copy = table;
+        const std::vector<BitString> alpha_copy = alpha, beta_copy = beta;
+        auto tb0 = std::chrono::steady_clock::now();
         const Basis basis = build_basis(std::move(alpha), std::move(beta), std::move(table));
+        const double t_host = std::chrono::duration<double>(std::chrono::steady_clock::now() - tb0).count();
+        tb0 = std::chrono::steady_clock::now();
+        gpu::GpuBuiltBasis built = gpu::build_basis_gpu(alpha_copy, beta_copy, table_copy);
+        const double t_dev = std::chrono::duration<double>(std::chrono::steady_clock::now() - tb0).count();
+        // the device-built host Basis against the reference one: helper lists
+        // byte-identical, diagonal within 1e-12
+        bool tables_equal = true;
+        const FlatExcitationTable* ra[4] = {&basis.singles_a, &basis.doubles_a, &basis.singles_b, &basis.doubles_b};
+        const FlatExcitationTable* ga[4] = {&built.host.singles_a, &built.host.doubles_a, &built.host.singles_b,
+                                            &built.host.doubles_b};
+        for (int i = 0; i < 4; ++i)
+            tables_equal = tables_equal && ra[i]->flat == ga[i]->flat && ra[i]->offset == ga[i]->offset &&
+                           ra[i]->len == ga[i]->len;
+        double diag_worst = 0.0;
+        for (std::size_t i = 0; i < basis.diag.size(); ++i)
+            diag_worst = std::max(diag_worst, std::abs(basis.diag[i] - built.host.diag[i]) /
+                                                  std::max(1.0, std::abs(basis.diag[i])));
+        const bool same_shape = built.host.dimension() == basis.dimension() && built.host.norbs == basis.norbs &&
+                                built.host.n_elec_alpha == basis.n_elec_alpha &&
+                                built.host.channel_packing.bit_length == basis.channel_packing.bit_length &&
+                                built.host.det_packing.nwords == basis.det_packing.nwords;
+        std::printf("GPU_BUILD tables_equal %d diag_max_rel %.3e shape %d host_s %.4f device_s %.4f\n",
+                    tables_equal ? 1 : 0, diag_worst, same_shape ? 1 : 0, t_host, t_dev);
         const DecompositionPlan plan = plan_decomposition(1, 1, 1, 1, basis);
         const auto dev = gpu::build_basis_gpu(basis);
 
@@ -67,10 +98,13 @@ int main(int argc, char** argv) {
             [&](std::span<const double> in, std::span<double> out) { matvec(basis, plan, in, out); }, basis.diag);
         const DavidsonResult mixed = davidson_solve(gpu::linear_operator(*dev), basis.diag);
         const DavidsonResult device = gpu::davidson_solve(*dev);
+        // the reference solver over the GPU-built basis (its diag and sigma)
+        const DavidsonResult gbuilt = davidson_solve(gpu::linear_operator(*built.device), built.host.diag);
         std::printf("GROUND_ENERGY reference %.12e %zu\n", ref.energy, ref.trace.iterations.size());
         std::printf("GROUND_ENERGY mixed %.12e %zu\n", mixed.energy, mixed.trace.iterations.size());
         std::printf("GROUND_ENERGY device %.12e %zu\n", device.energy, device.trace.iterations.size());
-        return ref.converged && mixed.converged && device.converged ? 0 : 2;
+        std::printf("GROUND_ENERGY gpu_built %.12e %zu\n", gbuilt.energy, gbuilt.trace.iterations.size());
+        return ref.converged && mixed.converged && device.converged && gbuilt.converged ? 0 : 2;
     } catch (const Error& e) {
         std::fprintf(stderr, "error: %s\n", e.what());
         return 1;

@@ -86,6 +86,10 @@ class RefLib:
         L.ref_davidson_operator.argtypes = [self.APPLY, vp, dp, C.c_uint64, C.c_double, C.c_int, C.c_int, dp,
                                             C.POINTER(C.c_int), C.POINTER(C.c_int), dp, C.c_int]
         L.ref_brute_force_hij.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, dp]
+        L.ref_stored_build.argtypes = [vp, C.c_uint64, C.c_int, C.POINTER(vp), u64p]
+        L.ref_stored_free.argtypes = [vp]
+        L.ref_stored_arrays.argtypes = [vp, u64p, u32p, dp]
+        L.ref_stored_matvec.argtypes = [vp, dp, dp, C.c_int]
 
     def check(self, code):
         if code:
@@ -258,6 +262,30 @@ class RefBasis:
                                                  _p(trace, C.c_double), max_iter, C.byref(sec)))
         return {"energy": e.value, "iterations": it.value, "status": st.value, "trace": trace[: it.value],
                 "eigenvector": vec, "seconds": sec.value}
+
+    def stored_matrix(self, budget=8 << 30, workers=0):
+        """Reference build_stored_matrix: (row_offset, col, value) and an
+        apply function running the reference stored_matvec."""
+        m, nnz = vp(), C.c_uint64()
+        self.ref.check(self.ref.lib.ref_stored_build(self.h, budget, workers, C.byref(m), C.byref(nnz)))
+        try:
+            ro = np.zeros(self.dim() + 1, dtype=np.uint64)
+            col = np.zeros(nnz.value, dtype=np.uint32)
+            val = np.zeros(nnz.value, dtype=np.float64)
+            self.ref.check(self.ref.lib.ref_stored_arrays(m, _p(ro, C.c_uint64), _p(col, C.c_uint32),
+                                                          _p(val, C.c_double)))
+            def apply(x):
+                x = np.ascontiguousarray(x, dtype=np.float64)
+                y = np.zeros_like(x)
+                self.ref.check(self.ref.lib.ref_stored_matvec(m, _p(x, C.c_double), _p(y, C.c_double), workers))
+                return y
+            return ro, col, val, apply, m
+        except Exception:
+            self.ref.lib.ref_stored_free(m)
+            raise
+
+    def stored_free(self, m):
+        self.ref.lib.ref_stored_free(m)
 
     def dense_hamiltonian(self, cap=4000):
         out = np.zeros((self.dim(), self.dim()))

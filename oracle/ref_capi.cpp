@@ -482,4 +482,32 @@ int ref_brute_force_hij(void* tp, std::uint64_t bra_a, std::uint64_t bra_b, std:
     })
 }
 
+// Reference StoredMatrix (build_stored_matrix, matvec.cpp:240-316): build,
+// copy out, stored_matvec (matvec.cpp:318-332).
+int ref_stored_build(void* bp, std::uint64_t budget, int workers, void** out, std::uint64_t* nnz) {
+    GUARD({
+        auto* m = new StoredMatrix(build_stored_matrix(*static_cast<Basis*>(bp), budget, workers));
+        *nnz = m->nonzero_count();
+        *out = m;
+    })
+}
+
+void ref_stored_free(void* m) { delete static_cast<StoredMatrix*>(m); }
+
+int ref_stored_arrays(void* mp, std::uint64_t* row_offset, std::uint32_t* col, double* value) {
+    GUARD({
+        const auto* m = static_cast<StoredMatrix*>(mp);
+        for (std::size_t i = 0; i < m->row_offset.size(); ++i) row_offset[i] = m->row_offset[i];
+        std::copy(m->col.begin(), m->col.end(), col);
+        std::copy(m->value.begin(), m->value.end(), value);
+    })
+}
+
+int ref_stored_matvec(void* mp, const double* x, double* y, int workers) {
+    GUARD({
+        const auto* m = static_cast<StoredMatrix*>(mp);
+        stored_matvec(*m, std::span<const double>(x, m->dimension), std::span<double>(y, m->dimension), workers);
+    })
+}
+
 } // extern "C"

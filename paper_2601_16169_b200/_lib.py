@@ -127,6 +127,10 @@ SIGNATURES = {
     "detci_gpu_davidson": (C.c_int, [vp, C.POINTER(DavOpts), C.POINTER(DavResult), TRACE_CB, vp]),
     "detci_gpu_davidson_roots": (C.c_int, [vp, C.POINTER(DavBlockOpts), C.POINTER(DavBlockResult)]),
     "detci_gpu_sigma_block": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.c_int]),
+    "detci_gpu_build_stored": (C.c_int, [vp, C.c_uint64, u64p]),
+    "detci_gpu_stored_arrays": (C.c_int, [vp, u64p, u32p, dp]),
+    "detci_gpu_set_operator": (C.c_int, [vp, C.c_int]),
+    "detci_gpu_release_stored": (C.c_int, [vp]),
     "detci_gpu_inner_product": (C.c_int, [vp, dp, dp, C.c_uint64, dp]),
     "detci_gpu_orthonormalize": (C.c_int, [vp, dp, C.c_int, C.c_uint64, dp, dp, C.POINTER(C.c_int)]),
     "detci_gpu_precondition": (C.c_int, [vp, dp, dp, C.c_uint64, C.c_double, dp]),

@@ -657,6 +657,7 @@ void release_basis(Handle& h) {
         t.built = false;
     }
     h.sell_perm.reset();
+    release_stored(h);
     h.tpos.reset();
     h.h_sa_flat.clear();
     h.h_sa_off.clear();

@@ -435,6 +435,45 @@ int detci_gpu_sigma_block(detci_gpu_handle* hh, const double* const* dx, double*
     });
 }
 
+int detci_gpu_build_stored(detci_gpu_handle* hh, uint64_t memory_budget_bytes, uint64_t* nnz) {
+    return guarded(hh, [&] {
+        require(hh != nullptr, DETCI_GPU_E_INPUT, "build_stored_matrix: null handle");
+        activate(hh->h);
+        build_stored(hh->h, memory_budget_bytes, nnz);
+    });
+}
+
+int detci_gpu_stored_arrays(const detci_gpu_handle* hh, uint64_t* row_offset, uint32_t* col, double* value) {
+    return guarded(const_cast<detci_gpu_handle*>(hh), [&] {
+        require(hh != nullptr, DETCI_GPU_E_INPUT, "stored_arrays: null handle");
+        const Handle& h = hh->h;
+        require(h.st_off.p != nullptr, DETCI_GPU_E_INPUT, "stored_arrays: matrix not built");
+        activate(const_cast<Handle&>(h));
+        const uint64_t dim = h.na() * h.nb();
+        if (row_offset) CUDA_CHECK(cudaMemcpy(row_offset, h.st_off.p, (dim + 1) * 8, cudaMemcpyDeviceToHost));
+        if (col) CUDA_CHECK(cudaMemcpy(col, h.st_col.p, h.st_nnz * 4, cudaMemcpyDeviceToHost));
+        if (value) CUDA_CHECK(cudaMemcpy(value, h.st_val.p, h.st_nnz * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+int detci_gpu_set_operator(detci_gpu_handle* hh, int kind) {
+    return guarded(hh, [&] {
+        require(hh != nullptr, DETCI_GPU_E_INPUT, "set_operator: null handle");
+        require(kind == 0 || kind == 1, DETCI_GPU_E_CONFIG, "set_operator: kind must be 0 or 1");
+        require(kind == 0 || hh->h.st_off.p != nullptr, DETCI_GPU_E_INPUT,
+                "set_operator: build the stored matrix first");
+        hh->h.use_stored = kind == 1;
+    });
+}
+
+int detci_gpu_release_stored(detci_gpu_handle* hh) {
+    return guarded(hh, [&] {
+        require(hh != nullptr, DETCI_GPU_E_INPUT, "release_stored: null handle");
+        activate(hh->h);
+        release_stored(hh->h);
+    });
+}
+
 int detci_gpu_inner_product(detci_gpu_handle* hh, const double* x, const double* y, uint64_t n,
                             double* out) {
     return guarded(hh, [&] {

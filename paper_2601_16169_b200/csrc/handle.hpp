@@ -152,6 +152,14 @@ struct Handle {
     DevBuf<double> red;                // reduction partials
     DevBuf<unsigned int> red_count;
 
+    // stored-matrix method (stored.cu): CSR of H, used by every sigma call
+    // while use_stored is set (detci_gpu_set_operator)
+    DevBuf<uint64_t> st_off;
+    DevBuf<uint32_t> st_col;
+    DevBuf<double> st_val;
+    uint64_t st_nnz = 0;
+    bool use_stored = false;
+
     cudaStream_t stream = nullptr, comm_stream = nullptr;
     cudaEvent_t ev[16] = {};
     ncclComm_t nccl = nullptr;
@@ -182,6 +190,11 @@ void sigma_enqueue(Handle& h, const double* dx, double* dy);  // no host sync
 // m vectors through one blocked pass (element evaluations shared across
 // vectors where the kernels support it); synchronous.
 void sigma_block(Handle& h, const double* const* dx, double* const* dy, int m);
+
+// stored.cu
+void build_stored(Handle& h, uint64_t budget, uint64_t* nnz);
+void release_stored(Handle& h);
+void stored_spmv(Handle& h, const double* dx, double* dy);   // enqueued on h.stream
 
 // davidson.cu
 struct DavidsonOutcome {

@@ -1338,6 +1338,12 @@ void sigma_schedule_m(Handle& h, const Ptrs& dx, const MPtrs& dy, PhaseTimer& tm
 }
 
 void sigma_schedule(Handle& h, const double* dx, double* dy, PhaseTimer& tm) {
+    if (h.use_stored) {   // Method::Stored (run.cpp:87-95): CSR SpMV
+        const int id = tm.begin(0);
+        stored_spmv(h, dx, dy);
+        tm.end(id);
+        return;
+    }
     Ptrs x{};
     MPtrs y{};
     x[0] = dx;
@@ -1359,6 +1365,11 @@ void sigma_block(Handle& h, const double* const* dx, double* const* dy, int m) {
         for (int j = 0; j < m; ++j)
             if (dx[i] == dy[j]) fail(DETCI_GPU_E_INPUT, "sigma: x and y must not alias");
     PhaseTimer tm(h, false);
+    if (h.use_stored) {
+        for (int i = 0; i < m; ++i) stored_spmv(h, dx[i], dy[i]);
+        CUDA_CHECK(cudaStreamSynchronize(h.stream));
+        return;
+    }
     int i = 0;
     while (i < m) {
         Ptrs x{};

@@ -194,6 +194,57 @@ class GpuBasis:
         return lambda x, y: matvec(self, x, y)
 
 
+class StoredMatrix:
+    """StoredMatrix (matvec.hpp:73-80) held in HBM by the basis's handle:
+    the reference CSR layout (row_offset, col, value)."""
+
+    def __init__(self, basis: GpuBasis, nnz: int):
+        self.basis = basis
+        self.dimension = basis.dimension()
+        self._nnz = nnz
+
+    def nonzero_count(self) -> int:
+        return self._nnz
+
+    def arrays(self):
+        """(row_offset u64[dim+1], col u32[nnz], value f64[nnz]) copied to the host."""
+        ro = np.zeros(self.dimension + 1, dtype=np.uint64)
+        col = np.zeros(self._nnz, dtype=np.uint32)
+        val = np.zeros(self._nnz, dtype=np.float64)
+        self.basis._check(self.basis._lib.detci_gpu_stored_arrays(
+            self.basis.handle, _ptr(ro, C.c_uint64), _ptr(col, C.c_uint32), _ptr(val, C.c_double)))
+        return ro, col, val
+
+    def use(self, on: bool = True) -> None:
+        """Method::Stored: every sigma (matvec, davidson_solve) uses the SpMV."""
+        self.basis._check(self.basis._lib.detci_gpu_set_operator(self.basis.handle, 1 if on else 0))
+
+    def release(self) -> None:
+        self.basis._check(self.basis._lib.detci_gpu_release_stored(self.basis.handle))
+
+
+def build_stored_matrix(basis: GpuBasis, memory_budget_bytes: int = 8 << 30) -> StoredMatrix:
+    """build_stored_matrix (matvec.hpp:84-86) on the device; CapacityError
+    over the budget (0 = free device memory) as matvec.cpp:262-269."""
+    nnz = C.c_uint64()
+    basis._check(basis._lib.detci_gpu_build_stored(basis.handle, int(memory_budget_bytes), C.byref(nnz)))
+    return StoredMatrix(basis, nnz.value)
+
+
+def stored_matvec(m: StoredMatrix, x: np.ndarray, y: Optional[np.ndarray] = None) -> np.ndarray:
+    """stored_matvec (matvec.hpp:89-90): y = H x from the stored values;
+    length mismatch -> InputError (matvec.cpp:320-321)."""
+    x = _f64(x)
+    if x.size != m.dimension or (y is not None and y.size != m.dimension):
+        raise InputError("stored_matvec: vector length does not match matrix dimension")
+    lib, h = m.basis._lib, m.basis.handle
+    m.basis._check(lib.detci_gpu_set_operator(h, 1))
+    try:
+        return matvec(m.basis, x, y)
+    finally:
+        m.basis._check(lib.detci_gpu_set_operator(h, 0))
+
+
 def build_basis(alpha: Sequence[int], beta: Sequence[int], integrals, opts: BasisOptions = BasisOptions()) -> GpuBasis:
     """build_basis (basis.hpp:85-86).  `integrals` exposes norbs, core, h1 (n^2), eri (n^4)."""
     return GpuBasis(integrals.norbs, alpha, beta, integrals.core, integrals.h1, integrals.eri, opts)

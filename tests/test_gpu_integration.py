@@ -24,7 +24,9 @@ def test_reference_pipeline_with_device_sigma(name):
     sig = [l for l in out.stdout.splitlines() if l.startswith("SIGMA_MAX_REL_DIFF")][0]
     assert float(sig.split()[1]) <= 1e-12
     e_ref = float(lines["reference"][0])
-    for k in ("mixed", "device"):
+    gb = [l.split() for l in out.stdout.splitlines() if l.startswith("GPU_BUILD")][0]
+    assert gb[2] == "1" and float(gb[4]) <= 1e-12 and gb[6] == "1", gb   # tables, diag, shape
+    for k in ("mixed", "device", "gpu_built"):
         assert abs(float(lines[k][0]) - e_ref) <= 1e-10 * abs(e_ref), (k, lines)
     if name == "chain8":
         assert lines["reference"][0] == "-2.420193979007e+00"
