@@ -367,11 +367,42 @@ def run_gpu_arm(args):
             t1 = time.time()
             r1 = detci.davidson_solve(basis1, want_vector=False)
             wall1 = time.time() - t1
+            # stored-matrix method at C1 (Method::Stored):
+            # CSR build and SpMV on device buffers; the SpMV is HBM-bound at
+            # 12 B per nonzero + 24 B per row
+            stored_c1 = None
+            if args.stored:
+                try:
+                    tb = time.time()
+                    sm = detci.build_stored_matrix(basis1, 0)
+                    build_st = time.time() - tb
+                    d1 = basis1.dimension()
+                    sx = torch.from_numpy(synth.random_vector(d1, 11)).cuda()
+                    sy = torch.empty_like(sx)
+                    sm.use(True)
+                    tms = []
+                    for _ in range(6):
+                        tmc = _lib.Timings()
+                        assert lib.detci_gpu_sigma_device(basis1.handle, sx.data_ptr(), sy.data_ptr(), C.byref(tmc)) == 0
+                        tms.append(tmc.total_seconds)
+                    tfree = _lib.Timings()
+                    sm.use(False)
+                    assert lib.detci_gpu_sigma_device(basis1.handle, sx.data_ptr(), sy.data_ptr(), C.byref(tfree)) == 0
+                    t_sp = float(np.median(tms[1:]))
+                    bytes_sp = 12.0 * sm.nonzero_count() + 24.0 * d1
+                    stored_c1 = {"nnz": sm.nonzero_count(), "build_seconds": build_st, "spmv_seconds": t_sp,
+                                 "spmv_GBps": bytes_sp / t_sp / 1e9, "spmv_frac_of_hbm": bytes_sp / t_sp / 1e9 / peak,
+                                 "matrix_free_sigma_seconds": tfree.total_seconds}
+                    sm.release()
+                    del sx, sy
+                except Exception as e:   # noqa: BLE001 -- reported, not fatal
+                    stored_c1 = {"error": str(e)}
         ref_e = None
         gpath = ROOT / "tests" / "golden" / "golden.json"
         if gpath.exists():
             ref_e = json.loads(gpath.read_text()).get("C1", {}).get("energy")
         dav_c1 = {"status": r1.status, "iterations": len(r1.iterations), "seconds": wall1, "energy": r1.energy,
+                  "stored_matrix": stored_c1,
                   "reference_energy": ref_e, "abs_err_vs_reference": abs(r1.energy - ref_e) if ref_e else None,
                   "reference_seconds_8core_container": json.loads(gpath.read_text()).get("C1", {}).get("davidson_seconds")
                   if gpath.exists() else None}
@@ -431,6 +462,7 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=8.0, help="target CPU seconds per reference sample")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-davidson", dest="davidson", action="store_false")
+    ap.add_argument("--no-stored", dest="stored", action="store_false", help="skip the C1 stored-matrix leg")
     ap.add_argument("--block", type=int, default=4, help="vectors in the blocked-sigma measurement (0 = skip)")
     ap.add_argument("--davidson-iters", type=int, default=30,
                     help="Davidson iterations timed for s/iter (reference defaults otherwise)")
