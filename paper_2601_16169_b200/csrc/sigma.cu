@@ -215,12 +215,13 @@ k_samespin(const SameSpinArgs a, uint32_t chunk0) {
 // similar paces, so Cs[ja, chunk] lines fetched by one warp are re-read by
 // the others from L1 (simulated 45-59% L1 hits at C2) instead of L2, which
 // bounds the one-row-per-CTA kernel (84.6% L2 throughput, 98% L2 hits).
-constexpr int kGW = 8;        // warps = rows per CTA
 constexpr int kGStage = 32;   // entries staged per warp
 
-template <bool kTail, int M>
-__global__ void __launch_bounds__(kGW * kWarp, 4)
+// GW warps = output rows per CTA (8 or 16; 1024 threads per SM either way)
+template <bool kTail, int M, int GW>
+__global__ void __launch_bounds__(GW * kWarp, 32 / GW)
 k_samespin_g(const SameSpinArgs a, uint32_t chunk0, uint32_t ngroups) {
+    constexpr int kGW = GW;
     constexpr int R = SSR<M>::value;
     __shared__ uint32_t s_ja[kGW][kGStage];
     __shared__ double s_v[kGW][kGStage];
@@ -606,6 +607,19 @@ k_mixed_scatter(const ScatterArgs a) {
         s_vrow[tid] = vr;
         s_drow[tid] = dr;
     }
+    // the first Cs segment streams in (cp.async) under the V build
+    const size_t crow = static_cast<size_t>(ja - a.c_row0) * a.ldc;
+    auto stage = [&](uint32_t g) {
+        const uint32_t segw = min(a.seg_cols, a.nb - g * a.seg_cols);
+#pragma unroll
+        for (int v = 0; v < M; ++v) {
+            const double* src = a.C[v] + crow + static_cast<size_t>(g) * a.seg_cols;
+            double* dst = cseg + v * segpad;
+            for (uint32_t c = tid; c < segw; c += kMxBlock) cp_async8(dst + c, src + c);
+        }
+        cp_async_commit();
+    };
+    stage(0);
     __syncthreads();
     for (uint32_t t = tid; t < static_cast<uint32_t>(K * nn); t += kMxBlock) {
         const uint32_t k = t / nn, cd = t - k * nn;
@@ -627,7 +641,6 @@ k_mixed_scatter(const ScatterArgs a) {
     const char* vb = reinterpret_cast<const char*>(vsub);
     const char* cb = reinterpret_cast<const char*>(cseg);
     const uint32_t vstride = a.vpitch * 8, cstride = segpad * 8;
-    const size_t crow = static_cast<size_t>(ja - a.c_row0) * a.ldc;
 
     auto element = [&](uint32_t e) {
         const char* cp = cb + (e & 0x3ffffu);
@@ -646,15 +659,10 @@ k_mixed_scatter(const ScatterArgs a) {
 
 #pragma unroll 1
     for (uint32_t g = 0; g < a.nseg; ++g) {
-        if (g > 0) __syncthreads();   // previous segment consumed
-        const uint32_t segw = min(a.seg_cols, a.nb - g * a.seg_cols);
-#pragma unroll
-        for (int v = 0; v < M; ++v) {
-            const double* src = a.C[v] + crow + static_cast<size_t>(g) * a.seg_cols;
-            double* dst = cseg + v * segpad;
-            for (uint32_t c = tid; c < segw; c += kMxBlock) cp_async8(dst + c, src + c);
+        if (g > 0) {
+            __syncthreads();   // previous segment consumed
+            stage(g);
         }
-        cp_async_commit();
         cp_async_wait_all();
         __syncthreads();
         if (!active) continue;
@@ -843,28 +851,40 @@ bool grouped_samespin() {
     return !(e && std::string(e) == "row");
 }
 
+template <int M, int GW>
+void launch_samespin_g(const SameSpinArgs& s, cudaStream_t st) {
+    constexpr uint32_t kChunk = kWarp * SSR<M>::value;
+    const uint64_t full = s.ncols / kChunk;
+    const bool tail = s.ncols % kChunk != 0;
+    const uint32_t ngroups = (s.nrows + GW - 1) / GW;
+    static bool configured = false;
+    if (!configured) {  // favour L1 over shared memory (the kernel uses <= 32 KB)
+        CUDA_CHECK(cudaFuncSetAttribute(k_samespin_g<false, M, GW>, cudaFuncAttributePreferredSharedMemoryCarveout, 10));
+        CUDA_CHECK(cudaFuncSetAttribute(k_samespin_g<true, M, GW>, cudaFuncAttributePreferredSharedMemoryCarveout, 10));
+        configured = true;
+    }
+    if (full) {
+        k_samespin_g<false, M, GW><<<static_cast<unsigned>(full * ngroups), GW * kWarp, 0, st>>>(s, 0, ngroups);
+        CUDA_LAUNCH_CHECK();
+    }
+    if (tail) {
+        k_samespin_g<true, M, GW><<<ngroups, GW * kWarp, 0, st>>>(s, static_cast<uint32_t>(full), ngroups);
+        CUDA_LAUNCH_CHECK();
+    }
+}
+
+// DETCI_SAMESPIN_ROWS=16: 16 rows per grouped CTA (default 8).
+int samespin_group_rows() {
+    const char* e = std::getenv("DETCI_SAMESPIN_ROWS");
+    return (e && std::string(e) == "16") ? 16 : 8;
+}
+
 template <int M>
 void launch_samespin(const SameSpinArgs& s, cudaStream_t st) {
     if (s.nrows == 0 || s.ncols == 0) return;
     if (grouped_samespin()) {
-        constexpr uint32_t kChunk = kWarp * SSR<M>::value;
-        const uint64_t full = s.ncols / kChunk;
-        const bool tail = s.ncols % kChunk != 0;
-        const uint32_t ngroups = (s.nrows + kGW - 1) / kGW;
-        static bool configured = false;
-        if (!configured) {  // favour L1 over shared memory (the kernel uses ~16 KB)
-            CUDA_CHECK(cudaFuncSetAttribute(k_samespin_g<false, M>, cudaFuncAttributePreferredSharedMemoryCarveout, 10));
-            CUDA_CHECK(cudaFuncSetAttribute(k_samespin_g<true, M>, cudaFuncAttributePreferredSharedMemoryCarveout, 10));
-            configured = true;
-        }
-        if (full) {
-            k_samespin_g<false, M><<<static_cast<unsigned>(full * ngroups), kGW * kWarp, 0, st>>>(s, 0, ngroups);
-            CUDA_LAUNCH_CHECK();
-        }
-        if (tail) {
-            k_samespin_g<true, M><<<ngroups, kGW * kWarp, 0, st>>>(s, static_cast<uint32_t>(full), ngroups);
-            CUDA_LAUNCH_CHECK();
-        }
+        if (samespin_group_rows() == 16) launch_samespin_g<M, 16>(s, st);
+        else launch_samespin_g<M, 8>(s, st);
         return;
     }
     constexpr uint32_t kChunk = kSSBlock * SSR<M>::value;
