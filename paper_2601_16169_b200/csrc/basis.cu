@@ -347,16 +347,22 @@ void build_mixed_sell(Handle& h, SellTable& st, int M, int format) {
     if (const char* e = std::getenv("DETCI_MIXED_MAX_SEG")) cap = std::max(2, std::atoi(e)) & ~1u;
     const uint32_t wdbl = (2 * nn + 1) & ~1u;
     if (format == 2) {
-        // K = 16 output rows per CTA when that costs no extra row segments
+        // The largest K (output rows per CTA) whose K V rows leave room for
+        // a Cs segment of >= 2048 columns per vector and that costs no more
+        // row segments than K/2 (M = 2 starts at 8: 2 x K accumulators per
+        // thread).  Large norbs shrink K (n = 64: 32 KB per V row).
+        const int64_t vp = scatter_vpitch(n);
+        auto room = [&](int K) { return static_cast<int64_t>(kScatterSmem / 8) - K * vp; };
         auto nseg_for = [&](int K) {
-            const int64_t room = static_cast<int64_t>(kScatterSmem / 8) - K * static_cast<int64_t>(scatter_vpitch(n));
-            const uint32_t seg = std::min<uint32_t>(cap, static_cast<uint32_t>(std::max<int64_t>(room, 2) / M) & ~1u);
+            const uint32_t seg = std::min<uint32_t>(cap, static_cast<uint32_t>(std::max<int64_t>(room(K), 2) / M) & ~1u);
             return (nb + seg - 1) / seg;
         };
-        // (M = 2 keeps K <= 8: 2 x K accumulators per thread)
-        st.kmax = (M == 1 && nseg_for(16) == nseg_for(8)) ? 16 : 8;
+        int K = M == 1 ? 16 : 8;
+        while (K > 1 && (room(K) < 2048 * M || nseg_for(K) > nseg_for(K / 2))) K /= 2;
+        if (room(K) < 64 * M) fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: V rows do not fit shared memory");
+        st.kmax = K;
     }
-    const uint32_t budget = format == 2 ? kScatterSmem / 8 - st.kmax * scatter_vpitch(n)
+    const uint32_t budget = format == 2 ? static_cast<uint32_t>(kScatterSmem / 8 - st.kmax * scatter_vpitch(n))
                                         : 220u * 1024 / 8 - 2 * wdbl;   // doubles for C stages
     const uint32_t single_seg = std::min<uint32_t>(cap, (budget / M) & ~1u);
     const uint32_t double_seg = std::min<uint32_t>(std::min<uint32_t>(16000, cap), (budget / 2 / M) & ~1u);

@@ -98,8 +98,8 @@ struct SellTable {
 // remainder's binary decomposition.
 struct ScatterWindow {
     uint64_t i_lo = 0, i_hi = 0, d_base = 0, d_rows = 0;
-    DevBuf<uint2> items[2];            // [0] kmax 16, [1] kmax 8 (built on demand)
-    std::vector<uint64_t> item_off[2]; // [b * kScatterClasses + c], size P * classes + 1
+    DevBuf<uint2> items[kScatterClasses];            // by log2(kmax) (built on demand)
+    std::vector<uint64_t> item_off[kScatterClasses]; // [b * classes + c], size P * classes + 1
 };
 
 struct Handle {

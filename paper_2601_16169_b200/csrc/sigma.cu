@@ -1044,7 +1044,7 @@ const std::vector<std::unique_ptr<ScatterWindow>>& scatter_windows(Handle& h, in
             wins.push_back(std::move(w));
         }
     }
-    const int ki = kmax == 16 ? 0 : 1;
+    const int ki = __builtin_ctz(static_cast<unsigned>(kmax));   // items depend on kmax
     for (auto& w : wins) {
         if (!w->item_off[ki].empty()) continue;
         std::vector<uint2> items;
@@ -1112,7 +1112,7 @@ void launch_mixed_scatter(Handle& h, int g, int P, int b, const Ptrs& Cb, uint32
                           const MPtrs& y_loc, uint64_t a0) {
     const SellTable& t = scatter_table(h, M);
     const auto& wins = scatter_windows(h, g, P, M, t.kmax);
-    const int ki = t.kmax == 16 ? 0 : 1;
+    const int ki = __builtin_ctz(static_cast<unsigned>(t.kmax));
     const uint32_t ldd = h.nslices * kWarp;
     const uint32_t vpitch = scatter_vpitch(h.norbs);
     const size_t cbytes = ((t.seg_cols + 1) & ~1u) * sizeof(double);

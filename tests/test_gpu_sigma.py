@@ -233,3 +233,21 @@ def test_mixed_kernel_variants(mixed, dbytes, rem, monkeypatch):
             y = detci.matvec(b, x)
             assert rel_diff(y.reshape(len(a), -1)[r], rows["sigma_rows"]) <= 1e-12
             assert np.array_equal(y, detci.matvec(b, x))
+
+
+@pytest.mark.parametrize("norbs,nel,count", [(40, 3, 160), (52, 2, 120), (64, 2, 150)])
+def test_large_norbs_scatter_classes(norbs, nel, count):
+    """Wide orbital spaces shrink the scatter kernel's K (a V row is 8 n^2
+    bytes: 32 KB at n = 64) and the gather kernel's W; sigma against the C
+    oracle, single vectors and pairs."""
+    from oracle.bindings import Oracle
+
+    ints = synth.synthetic_integrals(norbs, 2 * nel)
+    s = synth.synthetic_strings(norbs, nel, count)
+    o = Oracle().system(ints, s, s, threads=8)
+    x = synth.random_vector(len(s) ** 2, 5)
+    ref = o.matvec(x)
+    with gpu_basis(ints, s, s) as b:
+        assert rel_diff(detci.matvec(b, x), ref) <= 1e-12
+        Y = detci.matvec_block(b, np.stack([x, -x]))
+        assert rel_diff(Y[0], ref) <= 1e-12 and rel_diff(Y[1], -ref) <= 1e-12
