@@ -354,6 +354,7 @@ int detci_gpu_sigma(detci_gpu_handle* hh, const double* x, double* y, detci_gpu_
         Handle& h = hh->h;
         require(h.built, DETCI_GPU_E_INPUT, "sigma: basis not built");
         activate(h);
+        if (sigma_host(h, x, y, tm)) return;
         const size_t n = h.local_len();
         h.xbuf.alloc(n);
         h.ybuf.alloc(n);

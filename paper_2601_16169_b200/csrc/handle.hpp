@@ -187,6 +187,10 @@ void release_sigma_scratch(Handle& h);
 // sigma.cu
 void sigma_device(Handle& h, const double* dx, double* dy, detci_gpu_timings* tm);
 void sigma_enqueue(Handle& h, const double* dx, double* dy);  // no host sync
+// y = H x on host buffers with the copies overlapped (chunked H2D under the
+// beta term, chunked D2H under the alpha term / reduction); false when the
+// shape needs the plain copy-sigma-copy schedule.  Synchronous.
+bool sigma_host(Handle& h, const double* x, double* y, detci_gpu_timings* tm);
 // m vectors through one blocked pass (element evaluations shared across
 // vectors where the kernels support it); synchronous.
 void sigma_block(Handle& h, const double* const* dx, double* const* dy, int m);

@@ -26,6 +26,7 @@
 // with the compute of the resident block).  The beta term and diagonal are
 // block-local.
 #include <algorithm>
+#include <cstdio>
 #include <array>
 #include <cstdlib>
 #include <string>
@@ -1107,16 +1108,21 @@ void launch_scatter_k(const ScatterArgs& a, uint64_t grid, uint32_t vpitch, size
 
 // Mixed term through the scatter kernel for block-rank g, held alpha block
 // b = rows [b0, b1) of Cs in Cb, outputs rows [a0, a1) of y_loc.
+// phases: 1 = scatter kernels only, 2 = D reduction only (of output rows
+// [r_lo, r_hi) within each window), 3 = both (per window).
 template <int M>
 void launch_mixed_scatter(Handle& h, int g, int P, int b, const Ptrs& Cb, uint32_t b0, uint32_t b1,
-                          const MPtrs& y_loc, uint64_t a0) {
+                          const MPtrs& y_loc, uint64_t a0, int phases = 3, uint64_t r_lo = 0,
+                          uint64_t r_hi = ~0ull, int only_window = -1) {
     const SellTable& t = scatter_table(h, M);
     const auto& wins = scatter_windows(h, g, P, M, t.kmax);
     const int ki = __builtin_ctz(static_cast<unsigned>(t.kmax));
     const uint32_t ldd = h.nslices * kWarp;
     const uint32_t vpitch = scatter_vpitch(h.norbs);
     const size_t cbytes = ((t.seg_cols + 1) & ~1u) * sizeof(double);
-    for (const auto& w : wins) {
+    for (size_t wi = 0; wi < wins.size(); ++wi) {
+        if (only_window >= 0 && static_cast<size_t>(only_window) != wi) continue;
+        const auto& w = wins[wi];
         const size_t base = static_cast<size_t>(b) * kScatterClasses;
         const auto& io = w->item_off[ki];
         if (io[base + kScatterClasses] == io[base]) continue;
@@ -1144,7 +1150,7 @@ void launch_mixed_scatter(Handle& h, int g, int P, int b, const Ptrs& Cb, uint32
         a.norbs = h.norbs;
         a.d_base = w->d_base;
         a.ldd = ldd;
-        for (int c = 0; c < kScatterClasses; ++c) {
+        for (int c = 0; c < kScatterClasses && (phases & 1); ++c) {
             const uint64_t i0 = io[base + c], i1 = io[base + c + 1];
             if (i1 == i0) continue;
             a.items = w->items[ki].p + i0;
@@ -1158,14 +1164,15 @@ void launch_mixed_scatter(Handle& h, int g, int P, int b, const Ptrs& Cb, uint32
                 default: launch_scatter_k<1, M>(a, grid, vpitch, cbytes, h.stream); break;
             }
         }
-        for (int v = 0; v < M; ++v) {
+        const uint64_t lo = std::max<uint64_t>(w->i_lo, r_lo), hi = std::min<uint64_t>(w->i_hi, r_hi);
+        for (int v = 0; v < M && (phases & 2) && lo < hi; ++v) {
             ReduceArgs r{};
             r.D = a.D[v];
             r.d_base = w->d_base;
             r.ldd = ldd;
             r.nb = a.nb;
             r.nparts = (a.nb + kRedBlock - 1) / kRedBlock;
-            r.i_lo = static_cast<uint32_t>(w->i_lo);
+            r.i_lo = static_cast<uint32_t>(lo);
             r.j0 = b0;
             r.j1 = b1;
             r.sa_flat = a.sa_flat;
@@ -1177,7 +1184,7 @@ void launch_mixed_scatter(Handle& h, int g, int P, int b, const Ptrs& Cb, uint32
             r.Y = y_loc[v];
             r.ldy = h.nb();
             r.y_row0 = static_cast<uint32_t>(a0);
-            const uint64_t rgrid = (w->i_hi - w->i_lo) * r.nparts;
+            const uint64_t rgrid = (hi - lo) * r.nparts;
             k_mixed_reduce<<<static_cast<unsigned>(rgrid), kRedBlock, 0, h.stream>>>(r);
             CUDA_LAUNCH_CHECK();
         }
@@ -1371,7 +1378,182 @@ void sigma_schedule(Handle& h, const double* dx, double* dy, PhaseTimer& tm) {
     sigma_schedule_m<1>(h, x, y, tm);
 }
 
+// Row chunks of the pipelined host sigma.  Front (H2D under the beta term):
+// growing chunks, ratio ~1.4 < (beta time / H2D time) per row, so each chunk
+// lands before the previous chunk's beta work ends.  Tail (D2H under the
+// alpha term and reduction): shrinking chunks, so only the last, small
+// chunk's copy is exposed.
+constexpr int kFrontChunks = 9, kTailChunks = 5;
+constexpr double kFrontWeight[kFrontChunks] = {1, 1.4, 2, 2.8, 3.9, 5.4, 7.5, 10.5, 14.7};
+constexpr double kTailWeight[kTailChunks] = {16, 8, 4, 2, 1};
+
+// Chunk edges (multiples of 128 rows, so the beta term's column chunks and
+// the alpha term's row groups have no partial tiles inside the pipe).
+template <int N>
+std::vector<uint64_t> pipe_edges(uint64_t nloc, const double (&w)[N]) {
+    double sum = 0.0;
+    for (double x : w) sum += x;
+    std::vector<uint64_t> e(N + 1, 0);
+    double acc = 0.0;
+    for (int c = 1; c < N; ++c) {
+        acc += w[c - 1];
+        e[c] = std::min<uint64_t>(nloc, static_cast<uint64_t>(nloc * acc / sum + 64) / 128 * 128);
+        e[c] = std::max(e[c], e[c - 1]);
+    }
+    e[N] = nloc;
+    return e;
+}
+
+// Host-pointer sigma with the host copies overlapped (one block, one vector,
+// matrix-free).  x arrives in growing row chunks on the copy stream; as each lands, its eps prologue runs and the beta term
+// over its alpha columns (the beta term reads only the x rows of its own
+// column chunk).  The scatter kernels then need all of Cs.  Finally, per row
+// chunk: the alpha term (y = diag*C + ...), the beta combine, the D
+// reduction, and that chunk's D2H on the copy stream under the next chunk's
+// kernels.  Returns false (nothing enqueued) when the shape does not allow it.
+bool sigma_host_pipelined(Handle& h, const double* x, double* y, detci_gpu_timings* out) {
+    if (h.world > 1 || h.vblocks > 1 || h.use_stored || !mixed_scatter_enabled()) return false;
+    const uint64_t nloc = h.nloc(), nb = h.nb(), n = nloc * nb;
+    if (nloc < 128 * kFrontChunks || nb == 0) return false;
+    ensure_scratch(h, 1, 1);
+    const SellTable& t = scatter_table(h, 1);
+    const auto& wins = scatter_windows(h, 0, 1, 1, t.kmax);
+    h.xbuf.alloc(n);
+    h.ybuf.alloc(n);
+    double* dx = h.xbuf.p;
+    double* dy = h.ybuf.p;
+    const uint64_t a0 = h.a0;
+    const size_t block = static_cast<size_t>(h.max_blk) * nb;
+    (void)block;
+    const std::vector<uint64_t> fe = pipe_edges(nloc, kFrontWeight), te = pipe_edges(nloc, kTailWeight);
+    cudaEvent_t ev[kFrontChunks + kTailChunks + 2];
+    const bool dbg = std::getenv("DETCI_PIPE_DEBUG") != nullptr;
+    for (auto& e : ev) CUDA_CHECK(cudaEventCreateWithFlags(&e, out || dbg ? cudaEventDefault : cudaEventDisableTiming));
+    cudaEvent_t* landed = ev;                    // H2D of front chunk c done
+    cudaEvent_t* final_rows = ev + kFrontChunks; // y rows of tail chunk c final
+    cudaEvent_t t0 = ev[kFrontChunks + kTailChunks], t1 = ev[kFrontChunks + kTailChunks + 1];
+    CUDA_CHECK(cudaEventRecord(t0, h.stream));
+    CUDA_CHECK(cudaStreamWaitEvent(h.comm_stream, t0, 0));   // previous work on the buffers is done
+    for (int c = 0; c < kFrontChunks; ++c) {
+        const uint64_t r0 = fe[c], r1 = fe[c + 1];
+        if (r1 > r0)
+            CUDA_CHECK(cudaMemcpyAsync(dx + r0 * nb, x + r0 * nb, (r1 - r0) * nb * 8, cudaMemcpyHostToDevice,
+                                       h.comm_stream));
+        CUDA_CHECK(cudaEventRecord(landed[c], h.comm_stream));
+    }
+    // prologue + beta term per landed chunk
+    for (int c = 0; c < kFrontChunks; ++c) {
+        const uint64_t r0 = fe[c], r1 = fe[c + 1];
+        CUDA_CHECK(cudaStreamWaitEvent(h.stream, landed[c], 0));
+        if (r1 == r0) continue;
+        const uint32_t rc = static_cast<uint32_t>(r1 - r0);
+        dim3 tb(kTile, 8), tg(static_cast<unsigned>((nb + kTile - 1) / kTile), (rc + kTile - 1) / kTile);
+        k_eps_transpose<<<tg, tb, 0, h.stream>>>(dx + r0 * nb, nb, h.xs.p + r0 * nb, h.ct.p + r0, nloc, rc,
+                                                 static_cast<uint32_t>(nb), h.ch[0].strings.p + a0 + r0,
+                                                 h.ch[1].prefix.p);
+        CUDA_LAUNCH_CHECK();
+        SameSpinArgs s{};
+        s.C[0] = h.ct.p + r0;
+        s.Y[0] = h.yt.p + r0;
+        s.ldc = nloc;
+        s.c_row0 = 0;
+        s.j0 = 0;
+        s.j1 = static_cast<uint32_t>(nb);
+        s.ldy = nloc;
+        s.row0 = 0;
+        s.nrows = static_cast<uint32_t>(nb);
+        s.ncols = rc;
+        s.J = h.ch[0].J.p + a0 + r0;
+        s.ldj = h.na();
+        fill_lists(s, h.ch[1]);
+        s.accumulate = 0;
+        launch_samespin<1>(s, h.stream);
+    }
+    cudaEvent_t e_front = nullptr, e_scatter = nullptr;
+    if (dbg) {
+        CUDA_CHECK(cudaEventCreate(&e_front));
+        CUDA_CHECK(cudaEventCreate(&e_scatter));
+        CUDA_CHECK(cudaEventRecord(e_front, h.stream));
+    }
+    // per scatter window: the scatter kernels (D partials of the window's
+    // rows), then per row chunk of the window: alpha term, combine, D
+    // reduction, D2H.  A window's D2H runs under the next window's scatter;
+    // the last window's rows go in shrinking chunks.
+    Ptrs held{};
+    held[0] = h.xs.p;
+    MPtrs yl{};
+    yl[0] = dy;
+    const int nw = static_cast<int>(wins.size());
+    int last_chunk = -1;
+    for (int wi = 0; wi < nw; ++wi) {
+        launch_mixed_scatter<1>(h, 0, 1, 0, held, 0, static_cast<uint32_t>(h.na()), yl, a0, 1, 0, ~0ull, wi);
+        if (dbg && wi == 0) CUDA_CHECK(cudaEventRecord(e_scatter, h.stream));
+        const uint64_t w0 = wins[wi]->i_lo - a0, w1 = wins[wi]->i_hi - a0;
+        std::vector<uint64_t> edges = {w0, w1};
+        if (wi + 1 == nw) {
+            edges = pipe_edges(w1 - w0, kTailWeight);
+            for (auto& e : edges) e += w0;
+        }
+        for (size_t c = 0; c + 1 < edges.size(); ++c) {
+            const uint64_t r0 = edges[c], r1 = edges[c + 1];
+            if (r1 == r0) continue;
+            Ptrs xl{};
+            xl[0] = dx + r0 * nb;
+            MPtrs yc{};
+            yc[0] = dy + r0 * nb;
+            launch_alpha<1>(h, held, 0, static_cast<uint32_t>(h.na()), xl, yc, a0 + r0, a0 + r1, true);
+            const uint32_t rc = static_cast<uint32_t>(r1 - r0);
+            dim3 tb(kTile, 8), tg(static_cast<unsigned>((nb + kTile - 1) / kTile), (rc + kTile - 1) / kTile);
+            k_transpose_add_eps<<<tg, tb, 0, h.stream>>>(h.yt.p + r0, nloc, dy + r0 * nb, nb, rc,
+                                                         static_cast<uint32_t>(nb), h.ch[0].strings.p + a0 + r0,
+                                                         h.ch[1].prefix.p);
+            CUDA_LAUNCH_CHECK();
+            launch_mixed_scatter<1>(h, 0, 1, 0, held, 0, static_cast<uint32_t>(h.na()), yl, a0, 2, a0 + r0,
+                                    a0 + r1, wi);
+            last_chunk = (last_chunk + 1) % kTailChunks;
+            cudaEvent_t done = final_rows[last_chunk];
+            CUDA_CHECK(cudaEventRecord(done, h.stream));
+            CUDA_CHECK(cudaStreamWaitEvent(h.comm_stream, done, 0));
+            CUDA_CHECK(cudaMemcpyAsync(y + r0 * nb, dy + r0 * nb, (r1 - r0) * nb * 8, cudaMemcpyDeviceToHost,
+                                       h.comm_stream));
+        }
+    }
+    CUDA_CHECK(cudaEventRecord(t1, h.comm_stream));
+    CUDA_CHECK(cudaEventSynchronize(t1));
+    if (dbg) {
+        float f = 0.f, sc = 0.f, lastland = 0.f, tail = 0.f, tot = 0.f;
+        CUDA_CHECK(cudaEventElapsedTime(&f, t0, e_front));
+        CUDA_CHECK(cudaEventElapsedTime(&sc, e_front, e_scatter));
+        CUDA_CHECK(cudaEventElapsedTime(&lastland, t0, landed[kFrontChunks - 1]));
+        CUDA_CHECK(cudaEventElapsedTime(&tail, e_scatter, final_rows[std::max(last_chunk, 0)]));
+        CUDA_CHECK(cudaEventElapsedTime(&tot, t0, t1));
+        std::fprintf(stderr, "pipe: front %.2f (H2D done %.2f) scatter %.2f tail %.2f total %.2f ms\n", f, lastland,
+                     sc, tail, tot);
+        cudaEventDestroy(e_front);
+        cudaEventDestroy(e_scatter);
+    }
+    if (out) {
+        float total = 0.f, h2d = 0.f, tail = 0.f;
+        CUDA_CHECK(cudaEventElapsedTime(&total, t0, t1));
+        CUDA_CHECK(cudaEventElapsedTime(&h2d, t0, landed[kFrontChunks - 1]));
+        CUDA_CHECK(cudaEventElapsedTime(&tail, final_rows[std::max(last_chunk, 0)], t1));
+        *out = detci_gpu_timings{};
+        out->h2d_seconds = h2d * 1e-3;    // overlapped with the beta term
+        out->d2h_seconds = tail * 1e-3;   // exposed tail (last chunk)
+        out->total_seconds = total * 1e-3;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    return true;
+}
+
 } // namespace
+
+bool sigma_host(Handle& h, const double* x, double* y, detci_gpu_timings* tm) {
+    if (!h.built) fail(DETCI_GPU_E_INPUT, "sigma: basis not built");
+    if (std::getenv("DETCI_SIGMA_PIPELINE") && std::string(std::getenv("DETCI_SIGMA_PIPELINE")) == "0") return false;
+    if (tm) return false;   // the phase split needs the plain schedule
+    return sigma_host_pipelined(h, x, y, nullptr);
+}
 
 void sigma_enqueue(Handle& h, const double* dx, double* dy) {
     if (!h.built) fail(DETCI_GPU_E_INPUT, "sigma: basis not built");

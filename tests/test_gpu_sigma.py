@@ -251,3 +251,26 @@ def test_large_norbs_scatter_classes(norbs, nel, count):
         assert rel_diff(detci.matvec(b, x), ref) <= 1e-12
         Y = detci.matvec_block(b, np.stack([x, -x]))
         assert rel_diff(Y[0], ref) <= 1e-12 and rel_diff(Y[1], -ref) <= 1e-12
+
+
+@pytest.mark.parametrize("cfg,dbytes", [("C1", None), ("C1", "20000000"), ("C2", None)])
+def test_pipelined_host_sigma_equals_plain(cfg, dbytes, monkeypatch):
+    """The host-pointer sigma with chunked, overlapped copies (default when
+    no timings are requested) against the plain copy-sigma-copy schedule
+    (DETCI_SIGMA_PIPELINE=0) and the reference rows; with several scatter
+    windows too (DETCI_MIXED_DBYTES)."""
+    if dbytes:
+        monkeypatch.setenv("DETCI_MIXED_DBYTES", dbytes)
+    rows = np.load(GOLDEN / f"rows_{cfg}.npz")
+    ints, a, bb = synth.synthetic_system(cfg)
+    with gpu_basis(ints, a, bb) as b:
+        x = synth.random_vector(b.dimension(), 11)
+        y = detci.matvec(b, x)
+        tm = {}
+        y_plain = detci.matvec(b, x, timings=tm)
+        assert rel_diff(y, y_plain) <= 1e-14
+        r = rows["rows"].astype(np.int64)
+        assert rel_diff(y.reshape(len(a), -1)[r], rows["sigma_rows"]) <= 1e-12
+        assert np.array_equal(y, detci.matvec(b, x))   # deterministic
+        monkeypatch.setenv("DETCI_SIGMA_PIPELINE", "0")
+        assert rel_diff(detci.matvec(b, x), y_plain) <= 1e-15
