@@ -360,7 +360,7 @@ def run_gpu_arm(args):
     # sigma over vector pairs) on the same basis, a bounded number of
     # iterations; s/iter of the whole solver
     roots = None
-    if args.davidson and args.roots > 0:
+    if args.davidson and args.roots > 0 and world == 1:
         rr = detci.davidson_roots(basis, args.roots, max_iter=args.roots_iters, want_vectors=False)
         nit = max(1, len(rr.iterations))
         roots = {"nroots": args.roots, "status": rr.status, "iterations": len(rr.iterations),
