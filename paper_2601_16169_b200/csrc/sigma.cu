@@ -219,11 +219,15 @@ k_samespin(const SameSpinArgs a, uint32_t chunk0) {
 constexpr int kGStage = 32;   // entries staged per warp
 
 // GW warps = output rows per CTA (8 or 16; 1024 threads per SM either way)
-template <bool kTail, int M, int GW>
+// kV2 (M = 1, full chunks, 16-byte aligned rows): each lane owns two pairs
+// of adjacent columns and reads them with one 16-byte load each, halving
+// the load instructions per element.
+template <bool kTail, int M, int GW, bool kV2 = false>
 __global__ void __launch_bounds__(GW * kWarp, 32 / GW)
 k_samespin_g(const SameSpinArgs a, uint32_t chunk0, uint32_t ngroups) {
     constexpr int kGW = GW;
     constexpr int R = SSR<M>::value;
+    static_assert(!kV2 || (M == 1 && !kTail && R == 4), "kV2: one vector, full chunks");
     __shared__ uint32_t s_ja[kGW][kGStage];
     __shared__ double s_v[kGW][kGStage];
     __shared__ uint32_t s_ab[kGW][kGStage];
@@ -271,6 +275,40 @@ k_samespin_g(const SameSpinArgs a, uint32_t chunk0, uint32_t ngroups) {
                 if (kind == 0) sab[t] = a.pab[k0 + t];
             }
             __syncwarp();
+            if constexpr (kV2) {
+                // columns chunk*128 + q*64 + 2*lane + {0, 1}, q < 2
+                const uint32_t cb = chunk * (kWarp * R) + 2 * lane;
+                if (kind == 0) {
+#pragma unroll 2
+                    for (int e = 0; e < cnt; ++e) {
+                        const double* crow = a.C[0] + static_cast<size_t>(sja[e]) * a.ldc + cb;
+                        const uint32_t ab = sab[e];
+                        const double* jrow = a.J + static_cast<size_t>(ab & 0x7fffffffu) * a.ldj + cb;
+                        const double v = sv[e];
+                        const uint32_t jsign = ab & 0x80000000u;
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            const double2 j = __ldg(reinterpret_cast<const double2*>(jrow + q * 2 * kWarp));
+                            const double2 c = __ldg(reinterpret_cast<const double2*>(crow + q * 2 * kWarp));
+                            acc[2 * q][0] = fma(v + xor_sign(j.x, jsign), c.x, acc[2 * q][0]);
+                            acc[2 * q + 1][0] = fma(v + xor_sign(j.y, jsign), c.y, acc[2 * q + 1][0]);
+                        }
+                    }
+                } else {
+#pragma unroll 4
+                    for (int e = 0; e < cnt; ++e) {
+                        const double* crow = a.C[0] + static_cast<size_t>(sja[e]) * a.ldc + cb;
+                        const double v = sv[e];
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            const double2 c = __ldg(reinterpret_cast<const double2*>(crow + q * 2 * kWarp));
+                            acc[2 * q][0] = fma(v, c.x, acc[2 * q][0]);
+                            acc[2 * q + 1][0] = fma(v, c.y, acc[2 * q + 1][0]);
+                        }
+                    }
+                }
+                continue;
+            }
             if (kind == 0) {
 #pragma unroll 2
                 for (int e = 0; e < cnt; ++e) {
@@ -310,7 +348,7 @@ k_samespin_g(const SameSpinArgs a, uint32_t chunk0, uint32_t ngroups) {
     const uint64_t arow = a.eps_row ? a.eps_row[row] : 0;
 #pragma unroll
     for (int q = 0; q < R; ++q) {
-        const uint32_t c = col0 + q * kWarp;
+        const uint32_t c = kV2 ? chunk * (kWarp * R) + (q / 2) * 2 * kWarp + 2 * lane + (q % 2) : col0 + q * kWarp;
         if (kTail && c >= a.ncols) continue;
         samespin_store<M>(a, arow, r, c, acc[q]);
     }
@@ -852,6 +890,15 @@ bool grouped_samespin() {
     return !(e && std::string(e) == "row");
 }
 
+// DETCI_SAMESPIN_VEC=1: 16-byte loads in the grouped kernel.  Off by
+// default: measured level or slightly slower (C2 alpha 20.1 vs 19.8 ms, C3
+// 117.4 vs 116.3 ms), i.e. the kernel is bound by L1/L2 data, not by load
+// instructions.
+bool samespin_vec2() {
+    const char* e = std::getenv("DETCI_SAMESPIN_VEC");
+    return e && std::string(e) == "1";
+}
+
 template <int M, int GW>
 void launch_samespin_g(const SameSpinArgs& s, cudaStream_t st) {
     constexpr uint32_t kChunk = kWarp * SSR<M>::value;
@@ -862,9 +909,20 @@ void launch_samespin_g(const SameSpinArgs& s, cudaStream_t st) {
     if (!configured) {  // favour L1 over shared memory (the kernel uses <= 32 KB)
         CUDA_CHECK(cudaFuncSetAttribute(k_samespin_g<false, M, GW>, cudaFuncAttributePreferredSharedMemoryCarveout, 10));
         CUDA_CHECK(cudaFuncSetAttribute(k_samespin_g<true, M, GW>, cudaFuncAttributePreferredSharedMemoryCarveout, 10));
+        if constexpr (M == 1)
+            CUDA_CHECK(cudaFuncSetAttribute(k_samespin_g<false, 1, GW, true>,
+                                            cudaFuncAttributePreferredSharedMemoryCarveout, 10));
         configured = true;
     }
-    if (full) {
+    // 16-byte loads need even strides and 16-byte aligned bases
+    const bool v2 = M == 1 && samespin_vec2() && s.ldc % 2 == 0 && s.ldj % 2 == 0 &&
+                    reinterpret_cast<uintptr_t>(s.C[0]) % 16 == 0 && reinterpret_cast<uintptr_t>(s.J) % 16 == 0;
+    if (full && v2) {
+        if constexpr (M == 1) {
+            k_samespin_g<false, 1, GW, true><<<static_cast<unsigned>(full * ngroups), GW * kWarp, 0, st>>>(s, 0, ngroups);
+            CUDA_LAUNCH_CHECK();
+        }
+    } else if (full) {
         k_samespin_g<false, M, GW><<<static_cast<unsigned>(full * ngroups), GW * kWarp, 0, st>>>(s, 0, ngroups);
         CUDA_LAUNCH_CHECK();
     }
@@ -1423,8 +1481,6 @@ bool sigma_host_pipelined(Handle& h, const double* x, double* y, detci_gpu_timin
     double* dx = h.xbuf.p;
     double* dy = h.ybuf.p;
     const uint64_t a0 = h.a0;
-    const size_t block = static_cast<size_t>(h.max_blk) * nb;
-    (void)block;
     const std::vector<uint64_t> fe = pipe_edges(nloc, kFrontWeight), te = pipe_edges(nloc, kTailWeight);
     cudaEvent_t ev[kFrontChunks + kTailChunks + 2];
     const bool dbg = std::getenv("DETCI_PIPE_DEBUG") != nullptr;

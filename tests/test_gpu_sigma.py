@@ -187,12 +187,16 @@ def test_segmented_virtual_blocks(monkeypatch):
         assert rel_diff(detci.matvec(b, synth.random_vector(len(s) ** 2, 11)), d["sigma11"]) <= 1e-12
 
 
-@pytest.mark.parametrize("kernel", ["row", "grouped"])
+@pytest.mark.parametrize("kernel", ["row", "grouped", "grouped-vec2", "grouped16"])
 def test_samespin_kernel_variants(kernel, monkeypatch):
     """Both same-spin kernels (DETCI_SAMESPIN=row: one row per CTA; default:
     8 rows per CTA) against the reference fixtures, the C1 reference rows and
     virtual blocks."""
-    monkeypatch.setenv("DETCI_SAMESPIN", kernel)
+    monkeypatch.setenv("DETCI_SAMESPIN", "row" if kernel == "row" else "grouped")
+    if kernel == "grouped-vec2":   # 16-byte loads
+        monkeypatch.setenv("DETCI_SAMESPIN_VEC", "1")
+    if kernel == "grouped16":
+        monkeypatch.setenv("DETCI_SAMESPIN_ROWS", "16")
     for name in ("h6_ring", "chain8"):
         ints, d = load_fixture(name)
         with gpu_basis(ints, d["alpha"], d["beta"]) as b:
