@@ -672,6 +672,9 @@ void release_basis(Handle& h) {
     h.ct.reset();
     h.yt.reset();
     h.xs.reset();
+    h.cs_full.reset();
+    h.mix_t.reset();
+    h.mix_r.reset();
     h.ring[0].reset();
     h.ring[1].reset();
     h.xbuf.reset();

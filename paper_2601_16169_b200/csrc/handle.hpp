@@ -147,6 +147,8 @@ struct Handle {
     // sigma scratch
     DevBuf<double> ct, yt;             // nb * max_blk
     DevBuf<double> xs;                 // eps o C of the local block (ring payload)
+    DevBuf<double> cs_full;            // gather schedule (P > 1): the whole Cs
+    DevBuf<double> mix_t, mix_r;       // gather schedule: own / received mixed slabs
     DevBuf<double> ring[2];            // max_blk * nb
     DevBuf<double> xbuf, ybuf;         // host-pointer staging, local length
     DevBuf<double> red;                // reduction partials

@@ -610,6 +610,7 @@ struct ScatterArgs {
     double* D[2];               // D_v row (sa_off[ia] + pos - d_base), ldd slots
     uint64_t d_base;
     uint32_t ldd;
+    uint32_t slot0, slot_end;   // beta slots [slot0, slot_end) (multi-GPU column share)
 };
 
 // M = 1 or 2 vectors share the V gathers (the multi-root block's pairs):
@@ -669,9 +670,9 @@ k_mixed_scatter(const ScatterArgs a) {
         vsub[k * a.vpitch + cd] = v;
     }
 
-    const uint32_t slot = part * kMxBlock + tid;
+    const uint32_t slot = a.slot0 + part * kMxBlock + tid;
     const uint32_t sl = slot / kWarp;
-    const bool active = sl < a.nslices;
+    const bool active = sl < a.nslices && slot < a.slot_end;
     double acc[M][K];
 #pragma unroll
     for (int v = 0; v < M; ++v)
@@ -724,7 +725,7 @@ k_mixed_scatter(const ScatterArgs a) {
     for (int k = 0; k < K; ++k)
         if (k < static_cast<int>(cnt))
 #pragma unroll
-            for (int v = 0; v < M; ++v) a.D[v][s_drow[k] * a.ldd + slot] = acc[v][k];
+            for (int v = 0; v < M; ++v) a.D[v][s_drow[k] * a.ldd + (slot - a.slot0)] = acc[v][k];
 }
 
 // y[ia, ib] += eps(A_ia, B_ib) sum_{pos in [lo, hi)} D[sa_off[ia] + pos - d_base, slot]
@@ -741,9 +742,12 @@ struct ReduceArgs {
     const uint64_t* alpha;
     const uint64_t* beta_prefix;
     const uint32_t* perm;
-    double* Y;                  // row ia at Y + (ia - y_row0) * ldy
+    double* Y;                  // row ia at Y + (ia - y_row0) * ldy (accumulate, by perm)
     size_t ldy;
     uint32_t y_row0;
+    uint32_t slot0, slot_end;   // slots [slot0, slot_end); D column = slot - slot0
+    double* T;                  // if set: T[(ia - y_row0) * ldt + slot - slot0] = result (slot order)
+    size_t ldt;
 };
 
 constexpr int kRedBlock = 256;
@@ -752,17 +756,17 @@ __global__ void __launch_bounds__(kRedBlock)
 k_mixed_reduce(const ReduceArgs a) {
     __shared__ uint32_t s_rng[2];
     const uint32_t ia = a.i_lo + blockIdx.x / a.nparts;
-    const uint32_t slot = (blockIdx.x % a.nparts) * kRedBlock + threadIdx.x;
+    const uint32_t slot = a.slot0 + (blockIdx.x % a.nparts) * kRedBlock + threadIdx.x;
     const uint64_t o = a.sa_off[ia];
     if (threadIdx.x < 2) {
         const uint32_t* f = a.sa_flat + o;
         s_rng[threadIdx.x] = lower_bound_u32(f, a.sa_len[ia], threadIdx.x == 0 ? a.j0 : a.j1);
     }
     __syncthreads();
-    if (slot >= a.nb) return;
+    if (slot >= a.nb || slot >= a.slot_end) return;
     const uint32_t lo = s_rng[0], hi = s_rng[1];
-    if (lo == hi) return;
-    const double* d = a.D + (o + lo - a.d_base) * a.ldd + slot;
+    if (lo == hi && !a.T) return;
+    const double* d = a.D + (o + lo - a.d_base) * a.ldd + (slot - a.slot0);
     double s = 0.0;
     uint32_t p = lo;
 #pragma unroll 1
@@ -776,7 +780,17 @@ k_mixed_reduce(const ReduceArgs a) {
     for (; p < hi; ++p) s += __ldcs(d + static_cast<size_t>(p - lo) * a.ldd);
     const uint32_t ib = a.perm[slot];
     const uint32_t flip = static_cast<uint32_t>(__popcll(a.alpha[ia] & a.beta_prefix[ib]));
-    a.Y[static_cast<size_t>(ia - a.y_row0) * a.ldy + ib] += flip_sign(s, flip);
+    if (a.T) a.T[static_cast<size_t>(ia - a.y_row0) * a.ldt + (slot - a.slot0)] = flip_sign(s, flip);
+    else a.Y[static_cast<size_t>(ia - a.y_row0) * a.ldy + ib] += flip_sign(s, flip);
+}
+
+// y[r * ldy + perm[s]] += R[r * ldr + s], s < ns (perm already offset to the
+// source's first slot): the column-partitioned mixed term back into rows.
+__global__ void k_unpack_mixed(const double* __restrict__ R, size_t ldr, uint32_t ns, uint32_t rows,
+                               const uint32_t* __restrict__ perm, double* __restrict__ y, size_t ldy) {
+    const uint32_t r = blockIdx.y;
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x)
+        if (r < rows) y[static_cast<size_t>(r) * ldy + perm[s]] += R[static_cast<size_t>(r) * ldr + s];
 }
 
 // ---------------------------------------------------------------------------
@@ -1057,6 +1071,22 @@ void launch_mixed(Handle& h, const Ptrs& Cb, uint32_t b0, uint32_t b1, const MPt
 
 // Remainder policy of the scatter items: one padded CTA (default; measured
 // C2 mixed 63.7 vs 65.9 ms, C3 466 vs 477 ms) or DETCI_SCATTER_REM=binary.
+bool multi_ring();
+std::pair<uint32_t, uint32_t> mixed_slots(const Handle& h, int g, int P);
+
+// D row stride (slots): all slots, or under the multi-block gather schedule
+// the largest per-rank column share.
+uint32_t mixed_ldd(const Handle& h) {
+    const int P = std::max(h.world, h.vblocks);
+    if (P == 1 || multi_ring()) return h.nslices * kWarp;
+    uint32_t m = 0;
+    for (int g = 0; g < P; ++g) {
+        const auto [s0, s1] = mixed_slots(h, g, P);
+        m = std::max(m, s1 - s0);
+    }
+    return m;
+}
+
 bool scatter_pad_remainder() {
     const char* e = std::getenv("DETCI_SCATTER_REM");
     return !(e && std::string(e) == "binary");
@@ -1070,7 +1100,7 @@ bool scatter_pad_remainder() {
 // the Davidson solvers allocate their subspace, and a pass with more vectors
 // than the plan reserved for re-plans).
 const std::vector<std::unique_ptr<ScatterWindow>>& scatter_windows(Handle& h, int g, int P, int M, int kmax) {
-    const uint64_t ldd = static_cast<uint64_t>(h.nslices) * kWarp;
+    const uint64_t ldd = mixed_ldd(h);
     if (h.dplan_m != 0 && h.dplan_m < M) release_sigma_scratch(h);
     if (h.scatter_plan.size() != static_cast<size_t>(P)) {
         h.scatter_plan.clear();
@@ -1091,7 +1121,9 @@ const std::vector<std::unique_ptr<ScatterWindow>>& scatter_windows(Handle& h, in
     }
     auto& wins = h.scatter_plan[g];
     if (wins.empty()) {
-        const uint64_t r0 = h.blk[g], r1 = h.blk[g + 1];
+        // P == 1: all rows and all ja (also the gather schedule's column
+        // share on a multi-block handle)
+        const uint64_t r0 = P == 1 ? 0 : h.blk[g], r1 = P == 1 ? h.na() : h.blk[g + 1];
         uint64_t i = r0;
         while (i < r1) {
             auto w = std::make_unique<ScatterWindow>();
@@ -1111,7 +1143,8 @@ const std::vector<std::unique_ptr<ScatterWindow>>& scatter_windows(Handle& h, in
         w->item_off[ki].assign(static_cast<size_t>(P) * kScatterClasses + 1, 0);
         for (int b = 0; b < P; ++b) {
             for (auto& c : cls) c.clear();
-            for (uint64_t ja = h.blk[b]; ja < h.blk[b + 1]; ++ja) {
+            const uint64_t j0 = P == 1 ? 0 : h.blk[b], j1 = P == 1 ? h.na() : h.blk[b + 1];
+            for (uint64_t ja = j0; ja < j1; ++ja) {
                 const uint32_t* f = flat + off[ja];
                 const uint32_t* e = flat + off[ja + 1];
                 uint32_t p = static_cast<uint32_t>(std::lower_bound(f, e, static_cast<uint32_t>(w->i_lo)) - f);
@@ -1164,6 +1197,15 @@ void launch_scatter_k(const ScatterArgs& a, uint64_t grid, uint32_t vpitch, size
     CUDA_LAUNCH_CHECK();
 }
 
+// Where the mixed term goes: beta slots [slot0, slot_end) and, if T is set,
+// overwrite T[v][(ia - a0) * ldt + slot - slot0] (slot order) instead of
+// accumulating into y[ia][perm[slot]].
+struct MixedTarget {
+    uint32_t slot0 = 0, slot_end = 0xffffffffu;
+    double* T[kMaxM] = {};
+    size_t ldt = 0;
+};
+
 // Mixed term through the scatter kernel for block-rank g, held alpha block
 // b = rows [b0, b1) of Cs in Cb, outputs rows [a0, a1) of y_loc.
 // phases: 1 = scatter kernels only, 2 = D reduction only (of output rows
@@ -1171,11 +1213,11 @@ void launch_scatter_k(const ScatterArgs& a, uint64_t grid, uint32_t vpitch, size
 template <int M>
 void launch_mixed_scatter(Handle& h, int g, int P, int b, const Ptrs& Cb, uint32_t b0, uint32_t b1,
                           const MPtrs& y_loc, uint64_t a0, int phases = 3, uint64_t r_lo = 0,
-                          uint64_t r_hi = ~0ull, int only_window = -1) {
+                          uint64_t r_hi = ~0ull, int only_window = -1, const MixedTarget& tgt = MixedTarget{}) {
     const SellTable& t = scatter_table(h, M);
     const auto& wins = scatter_windows(h, g, P, M, t.kmax);
     const int ki = __builtin_ctz(static_cast<unsigned>(t.kmax));
-    const uint32_t ldd = h.nslices * kWarp;
+    const uint32_t ldd = mixed_ldd(h);
     const uint32_t vpitch = scatter_vpitch(h.norbs);
     const size_t cbytes = ((t.seg_cols + 1) & ~1u) * sizeof(double);
     for (size_t wi = 0; wi < wins.size(); ++wi) {
@@ -1191,7 +1233,6 @@ void launch_mixed_scatter(Handle& h, int g, int P, int b, const Ptrs& Cb, uint32
         }
         a.ldc = h.nb();
         a.c_row0 = b0;
-        a.nparts = (ldd + kMxBlock - 1) / kMxBlock;
         a.nslices = h.nslices;
         a.nb = static_cast<uint32_t>(h.nb());
         a.seg_cols = t.seg_cols;
@@ -1208,6 +1249,11 @@ void launch_mixed_scatter(Handle& h, int g, int P, int b, const Ptrs& Cb, uint32
         a.norbs = h.norbs;
         a.d_base = w->d_base;
         a.ldd = ldd;
+        a.slot0 = tgt.slot0;
+        a.slot_end = std::min<uint32_t>(tgt.slot_end, h.nslices * kWarp);
+        if (a.slot_end <= a.slot0) return;   // empty column share (more ranks than slices)
+        if (a.slot_end - a.slot0 > ldd) fail(DETCI_GPU_E_CUDA, "mixed term: slot share exceeds the D stride");
+        a.nparts = (a.slot_end - a.slot0 + kMxBlock - 1) / kMxBlock;
         for (int c = 0; c < kScatterClasses && (phases & 1); ++c) {
             const uint64_t i0 = io[base + c], i1 = io[base + c + 1];
             if (i1 == i0) continue;
@@ -1229,7 +1275,11 @@ void launch_mixed_scatter(Handle& h, int g, int P, int b, const Ptrs& Cb, uint32
             r.d_base = w->d_base;
             r.ldd = ldd;
             r.nb = a.nb;
-            r.nparts = (a.nb + kRedBlock - 1) / kRedBlock;
+            r.slot0 = a.slot0;
+            r.slot_end = std::min<uint32_t>(a.slot_end, a.nb);
+            r.nparts = (r.slot_end - r.slot0 + kRedBlock - 1) / kRedBlock;
+            r.T = tgt.T[v];
+            r.ldt = tgt.ldt;
             r.i_lo = static_cast<uint32_t>(lo);
             r.j0 = b0;
             r.j1 = b1;
@@ -1371,8 +1421,213 @@ void sigma_ring(Handle& h, int g, int P, const Ptrs& x_loc, const MPtrs& xs_loc,
     combine<M>(h, y_loc, a0, a1, tm);
 }
 
+// ---------------------------------------------------------------------------
+// Multi-block "gather" schedule (default for P > 1; DETCI_MULTI=ring keeps the
+// ring).  The ring's mixed term restricts each CTA item (ja, K outputs) to
+// the outputs of one rank, i.e. to ~|S(ja)|/P rows, so items shrink to K of
+// 4-8 at P = 8 (1.2-1.6x the per-element cost, measured with virtual
+// blocks).  Here every rank holds the whole Cs (allgather, dim x 8 B, under
+// the beta term), runs the alpha term in one launch, and computes the mixed
+// term for ALL alpha rows but only its 1/P of the beta slots, with the full
+// K = 16 items; the resulting column slab is exchanged all-to-all (dim/P x
+// 8 B per rank) and unpacked into the local rows.
+// ---------------------------------------------------------------------------
+bool multi_ring() {
+    const char* e = std::getenv("DETCI_MULTI");
+    return e && std::string(e) == "ring";
+}
+
+// Beta slots of the mixed term owned by block-rank g (32-slot aligned).
+std::pair<uint32_t, uint32_t> mixed_slots(const Handle& h, int g, int P) {
+    const uint64_t total = static_cast<uint64_t>(h.nslices) * kWarp;
+    auto at = [&](int k) { return static_cast<uint32_t>(k == P ? total : total * k / P / kWarp * kWarp); };
+    return {at(g), at(g + 1)};
+}
+
+// Scratch of the gather schedule: the whole Cs (M vectors), this rank's
+// column slab T (na x ns_g) and the received slabs R (nloc x ns_g' each).
+void ensure_gather_scratch(Handle& h, int M, int P) {
+    const size_t na = h.na(), nb = h.nb();
+    const size_t full = na * nb;
+    if (h.world > 1 && h.cs_full.n < M * full) h.cs_full.alloc(M * full);
+    size_t tmax = 0;
+    for (int g = 0; g < P; ++g) {
+        const auto [s0, s1] = mixed_slots(h, g, P);
+        tmax = std::max<size_t>(tmax, s1 - s0);
+    }
+    const size_t t = (h.world > 1 ? na * tmax : full + na * kWarp * static_cast<size_t>(P));
+    if (h.mix_t.n < M * t) h.mix_t.alloc(M * t);
+    if (h.world > 1) {
+        const size_t r = static_cast<size_t>(h.max_blk) * (nb + kWarp * static_cast<size_t>(P));
+        if (h.mix_r.n < M * r) h.mix_r.alloc(M * r);
+    }
+}
+
+// Unpack a column slab of slots [s0, s0 + ns): only slots < nb are real
+// (the last slice is padded to 32).
+template <int M>
+void unpack_slab(Handle& h, const double* R, size_t ldr, uint32_t ns, uint64_t rows, uint32_t s0, double* y) {
+    ns = static_cast<uint32_t>(std::min<uint64_t>(ns, h.nb() > s0 ? h.nb() - s0 : 0));
+    if (rows == 0 || ns == 0) return;
+    for (uint64_t r0 = 0; r0 < rows; r0 += 65535) {
+        const uint32_t rr = static_cast<uint32_t>(std::min<uint64_t>(65535, rows - r0));
+        dim3 grid((ns + 255) / 256, rr);
+        k_unpack_mixed<<<grid, 256, 0, h.stream>>>(R + r0 * ldr, ldr, ns, rr, h.sell_perm.p + s0, y + r0 * h.nb(),
+                                                   h.nb());
+        CUDA_LAUNCH_CHECK();
+    }
+}
+
+// Mixed term of block-rank g, column-partitioned: all alpha rows (Cs whole
+// in Cfull), beta slots of g, result (eps applied) into T (na x ldt, slot
+// order).
+template <int M>
+void mixed_columns(Handle& h, int g, int P, const Ptrs& Cfull, double* const* T, size_t ldt) {
+    const auto [s0, s1] = mixed_slots(h, g, P);
+    MixedTarget tgt;
+    tgt.slot0 = s0;
+    tgt.slot_end = s1;
+    tgt.ldt = ldt;
+    for (int v = 0; v < M; ++v) tgt.T[v] = T[v];
+    MPtrs none{};
+    launch_mixed_scatter<M>(h, 0, 1, 0, Cfull, 0, static_cast<uint32_t>(h.na()), none, 0, 3, 0, ~0ull, -1, tgt);
+}
+
+// One rank (world > 1) of the gather schedule over NCCL.
+template <int M>
+void sigma_gather_rank(Handle& h, const Ptrs& x_loc, const MPtrs& y_loc, PhaseTimer& tm) {
+    const int g = h.rank, P = h.world;
+    const uint64_t a0 = h.blk[g], a1 = h.blk[g + 1], nloc = a1 - a0;
+    const size_t na = h.na(), nb = h.nb(), full = na * nb;
+    Ptrs cf{};
+    MPtrs cfw{};
+    for (int v = 0; v < M; ++v) {
+        cf[v] = h.cs_full.p + v * full;
+        cfw[v] = h.cs_full.p + v * full + a0 * nb;
+    }
+    int id = tm.begin(1);
+    eps_prologue<M>(h, x_loc, cfw, true, a0, a1);   // own rows of Cs, and Cs^T
+    CUDA_CHECK(cudaEventRecord(h.ev[4], h.stream));
+    CUDA_CHECK(cudaStreamWaitEvent(h.comm_stream, h.ev[4], 0));
+    // allgather of the P row blocks (in-place broadcasts from each owner)
+    if (ncclGroupStart() != ncclSuccess) fail(DETCI_GPU_E_CUDA, "ncclGroupStart");
+    for (int v = 0; v < M; ++v)
+        for (int b = 0; b < P; ++b) {
+            double* blk = h.cs_full.p + v * full + h.blk[b] * nb;
+            const size_t n = (h.blk[b + 1] - h.blk[b]) * nb;
+            if (n && ncclBroadcast(blk, blk, n, ncclDouble, b, h.nccl, h.comm_stream) != ncclSuccess)
+                fail(DETCI_GPU_E_CUDA, "ncclBroadcast (Cs allgather)");
+        }
+    if (ncclGroupEnd() != ncclSuccess) fail(DETCI_GPU_E_CUDA, "ncclGroupEnd (Cs allgather)");
+    CUDA_CHECK(cudaEventRecord(h.ev[5], h.comm_stream));
+    beta_term<M>(h, a0, a1);                        // local, under the allgather
+    tm.end(id);
+    CUDA_CHECK(cudaStreamWaitEvent(h.stream, h.ev[5], 0));
+    id = tm.begin(0);
+    launch_alpha<M>(h, cf, 0, static_cast<uint32_t>(na), x_loc, y_loc, a0, a1, true);
+    tm.end(id);
+    id = tm.begin(2);
+    const auto [s0, s1] = mixed_slots(h, g, P);
+    const size_t ns = s1 - s0;
+    double* T[kMaxM] = {};
+    for (int v = 0; v < M; ++v) T[v] = h.mix_t.p + v * na * ns;
+    mixed_columns<M>(h, g, P, cf, T, ns);
+    // all-to-all of the slab: rows of rank b go to b; slabs from every rank
+    // land in R (source-major, nloc x ns_src each)
+    CUDA_CHECK(cudaEventRecord(h.ev[6], h.stream));
+    CUDA_CHECK(cudaStreamWaitEvent(h.comm_stream, h.ev[6], 0));
+    const size_t rstride = static_cast<size_t>(h.max_blk) * (nb + kWarp * static_cast<size_t>(P));
+    std::vector<size_t> roff(P + 1, 0);
+    for (int b = 0; b < P; ++b) {
+        const auto [t0, t1] = mixed_slots(h, b, P);
+        roff[b + 1] = roff[b] + nloc * (t1 - t0);
+    }
+    if (ncclGroupStart() != ncclSuccess) fail(DETCI_GPU_E_CUDA, "ncclGroupStart");
+    for (int v = 0; v < M; ++v)
+        for (int b = 0; b < P; ++b) {
+            const auto [t0, t1] = mixed_slots(h, b, P);
+            const size_t send_n = (h.blk[b + 1] - h.blk[b]) * ns, recv_n = nloc * (t1 - t0);
+            double* src = T[v] + h.blk[b] * ns;
+            double* dst = h.mix_r.p + v * rstride + roff[b];
+            if (b == g) {
+                if (send_n)
+                    CUDA_CHECK(cudaMemcpyAsync(dst, src, send_n * 8, cudaMemcpyDeviceToDevice, h.comm_stream));
+                continue;
+            }
+            if (send_n && ncclSend(src, send_n, ncclDouble, b, h.nccl, h.comm_stream) != ncclSuccess)
+                fail(DETCI_GPU_E_CUDA, "ncclSend (mixed slab)");
+            if (recv_n && ncclRecv(dst, recv_n, ncclDouble, b, h.nccl, h.comm_stream) != ncclSuccess)
+                fail(DETCI_GPU_E_CUDA, "ncclRecv (mixed slab)");
+        }
+    if (ncclGroupEnd() != ncclSuccess) fail(DETCI_GPU_E_CUDA, "ncclGroupEnd (mixed slab)");
+    CUDA_CHECK(cudaEventRecord(h.ev[7], h.comm_stream));
+    CUDA_CHECK(cudaStreamWaitEvent(h.stream, h.ev[7], 0));
+    for (int v = 0; v < M; ++v)
+        for (int b = 0; b < P; ++b) {
+            const auto [t0, t1] = mixed_slots(h, b, P);
+            unpack_slab<M>(h, h.mix_r.p + v * rstride + roff[b], t1 - t0, t1 - t0, nloc, t0, y_loc[v]);
+        }
+    tm.end(id);
+    combine<M>(h, y_loc, a0, a1, tm);
+}
+
+// The gather schedule emulated on one GPU (virtual blocks): every rank's
+// work in turn; the allgather is the whole Cs signed up front, the
+// all-to-all is the column slabs of all ranks unpacked into the whole y.
+template <int M>
+void sigma_gather_virtual(Handle& h, const Ptrs& dx, const MPtrs& dy, PhaseTimer& tm) {
+    const int P = h.vblocks;
+    const size_t na = h.na(), nb = h.nb(), full = na * nb;
+    const size_t tstride = full + na * kWarp * static_cast<size_t>(P);
+    Ptrs cf{};
+    MPtrs cfw{};
+    for (int v = 0; v < M; ++v) {
+        cf[v] = h.xs.p + v * full;
+        cfw[v] = h.xs.p + v * full;
+    }
+    eps_prologue<M>(h, dx, cfw, false, 0, na);
+    for (int g = 0; g < P; ++g) {
+        const uint64_t a0 = h.blk[g], a1 = h.blk[g + 1];
+        Ptrs xg{};
+        MPtrs yg{}, cg{};
+        for (int v = 0; v < M; ++v) {
+            xg[v] = dx[v] + a0 * nb;
+            yg[v] = dy[v] + a0 * nb;
+            cg[v] = h.xs.p + v * full + a0 * nb;
+        }
+        int id = tm.begin(1);
+        eps_prologue<M>(h, xg, cg, true, a0, a1);
+        beta_term<M>(h, a0, a1);
+        tm.end(id);
+        id = tm.begin(0);
+        launch_alpha<M>(h, cf, 0, static_cast<uint32_t>(na), xg, yg, a0, a1, true);
+        tm.end(id);
+        combine<M>(h, yg, a0, a1, tm);
+    }
+    const int id = tm.begin(2);
+    size_t toff = 0;
+    for (int g = 0; g < P; ++g) {
+        const auto [s0, s1] = mixed_slots(h, g, P);
+        const size_t ns = s1 - s0;
+        double* T[kMaxM] = {};
+        for (int v = 0; v < M; ++v) T[v] = h.mix_t.p + v * tstride + toff;
+        mixed_columns<M>(h, g, P, cf, T, ns);
+        for (int v = 0; v < M; ++v) unpack_slab<M>(h, T[v], ns, static_cast<uint32_t>(ns), na, s0, dy[v]);
+        toff += na * ns;
+    }
+    tm.end(id);
+}
+
 template <int M>
 void sigma_schedule_m(Handle& h, const Ptrs& dx, const MPtrs& dy, PhaseTimer& tm) {
+    const int Pm = std::max(h.world, h.vblocks);
+    if (Pm > 1 && M <= 2 && mixed_scatter_enabled() && !multi_ring()) {
+        ensure_scratch(h, M, 1);
+        ensure_gather_scratch(h, M, Pm);
+        if (h.world > 1) sigma_gather_rank<M>(h, dx, dy, tm);
+        else sigma_gather_virtual<M>(h, dx, dy, tm);
+        return;
+    }
     const size_t nb = h.nb();
     const int P = std::max(h.world, h.vblocks);
     const size_t block = static_cast<size_t>(h.max_blk) * nb;

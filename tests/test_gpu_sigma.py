@@ -278,3 +278,28 @@ def test_pipelined_host_sigma_equals_plain(cfg, dbytes, monkeypatch):
         assert np.array_equal(y, detci.matvec(b, x))   # deterministic
         monkeypatch.setenv("DETCI_SIGMA_PIPELINE", "0")
         assert rel_diff(detci.matvec(b, x), y_plain) <= 1e-15
+
+
+@pytest.mark.parametrize("multi", ["gather", "ring"])
+@pytest.mark.parametrize("blocks", [2, 3, 8])
+def test_multi_block_schedules(multi, blocks, monkeypatch):
+    """Both multi-GPU schedules on virtual alpha blocks: the gather schedule
+    (default: Cs allgather, alpha term in one launch, mixed term split by
+    beta-slot columns and exchanged all-to-all) and the Cs ring
+    (DETCI_MULTI=ring), single vectors and pairs, against the reference rows
+    at C1 and the single-block sigma."""
+    if multi == "ring":
+        monkeypatch.setenv("DETCI_MULTI", "ring")
+    rows = np.load(GOLDEN / "rows_C1.npz")
+    ints, a, bb = synth.synthetic_system("C1")
+    r = rows["rows"].astype(np.int64)
+    x = synth.random_vector(len(a) * len(bb), 11)
+    with gpu_basis(ints, a, bb) as b1:
+        y1 = detci.matvec(b1, x)
+    with gpu_basis(ints, a, bb, virtual_blocks=blocks, weighted_partition=True) as b:
+        y = detci.matvec(b, x)
+        assert rel_diff(y.reshape(len(a), -1)[r], rows["sigma_rows"]) <= 1e-12
+        assert rel_diff(y, y1) <= 1e-12
+        Y = detci.matvec_block(b, np.stack([x, -0.5 * x, 2.0 * x]))
+        for i, sc in enumerate((1.0, -0.5, 2.0)):
+            assert rel_diff(Y[i], sc * y1) <= 1e-12
