@@ -128,3 +128,101 @@ def test_ring_decomposed_sigma_matches_full(world, weighted):
     assert err <= 1e-12
     assert abs(dot_dist - dot_full) <= 1e-12 * max(1.0, abs(dot_full))
     assert blk[0] == 0 and blk[-1] == 48 and len(blk) == world + 1
+
+
+def _gather_worker(rank, world, port, q):
+    """The gather schedule (sigma.cu:sigma_gather_rank): allgather of the C
+    row blocks; alpha-alpha, beta-beta and diagonal for the own rows with all
+    of C; the mixed term for ALL alpha rows but only the own share of beta
+    columns (32-aligned split as mixed_slots); the column slabs go
+    all-to-all (rows of rank b to b) and are added into the own rows."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ints, strs = _system()
+        sysm = Oracle().system(ints, strs, strs, threads=1)
+        tables = sysm.tables
+        ls = [tables[k][2] for k in ((0, 0), (0, 1), (1, 0), (1, 1))]
+        blk = [int(v) for v in detci.plan_partition(sysm.na, sysm.nb, *ls, world, True)]
+        na, nb = sysm.na, sysm.nb
+        alpha, beta, hij = sysm.alpha, sysm.beta, sysm.hij
+        sa, da, sb, db = (tables[k] for k in ((0, 0), (0, 1), (1, 0), (1, 1)))
+
+        def row(t, i):
+            f, o, l = t
+            return f[int(o[i]):int(o[i]) + int(l[i])]
+
+        x = synth.random_vector(na * nb, 5).reshape(na, nb)
+        a0, a1 = blk[rank], blk[rank + 1]
+        # allgather of the row blocks (padded to the largest block)
+        mb = max(blk[b + 1] - blk[b] for b in range(world))
+        mine = torch.zeros((mb, nb), dtype=torch.float64)
+        mine[:a1 - a0] = torch.from_numpy(x[a0:a1])
+        parts = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(parts, mine)
+        C = np.concatenate([parts[b][:blk[b + 1] - blk[b]].numpy() for b in range(world)])
+        assert np.array_equal(C, x)
+        y = np.zeros((a1 - a0, nb))
+        for ia in range(a0, a1):
+            for ib in range(nb):
+                acc = sysm.diag[ia * nb + ib] * C[ia, ib]
+                for ja in np.concatenate([row(sa, ia), row(da, ia)]):
+                    acc += hij(alpha[ia], beta[ib], alpha[ja], beta[ib]) * C[ja, ib]
+                for jb in np.concatenate([row(sb, ib), row(db, ib)]):
+                    acc += hij(alpha[ia], beta[ib], alpha[ia], beta[jb]) * C[ia, jb]
+                y[ia - a0, ib] = acc
+        # mixed term: all alpha rows, own beta-column share
+        total = (nb + 31) // 32 * 32
+        edge = [total if k == world else total * k // world // 32 * 32 for k in range(world + 1)]
+        c0, c1 = edge[rank], min(edge[rank + 1], nb)
+        slab = np.zeros((na, max(c1 - c0, 0)))
+        for ia in range(na):
+            for ib in range(c0, c1):
+                acc = 0.0
+                for ja in row(sa, ia):
+                    for jb in row(sb, ib):
+                        acc += hij(alpha[ia], beta[ib], alpha[ja], beta[jb]) * C[ja, jb]
+                slab[ia, ib - c0] = acc
+        send = [torch.from_numpy(np.ascontiguousarray(slab[blk[b]:blk[b + 1]])).reshape(-1) for b in range(world)]
+        widths = [max(min(edge[b + 1], nb) - edge[b], 0) for b in range(world)]
+        recv = [torch.empty((a1 - a0) * widths[b], dtype=torch.float64) for b in range(world)]
+        # point-to-point pairs, as the grouped ncclSend/ncclRecv of the slab
+        reqs = []
+        for b in range(world):
+            if b == rank:
+                recv[b].copy_(send[b])
+                continue
+            if send[b].numel():
+                reqs.append(dist.isend(send[b], b))
+            if recv[b].numel():
+                reqs.append(dist.irecv(recv[b], b))
+        for r in reqs:
+            r.wait()
+        for b in range(world):
+            if widths[b]:
+                y[:, edge[b]:edge[b] + widths[b]] += recv[b].numpy().reshape(a1 - a0, widths[b])
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (a0, a1, y))
+        if rank == 0:
+            full = np.zeros((na, nb))
+            for b0, b1, yl in gathered:
+                full[b0:b1] = yl
+            ref = sysm.matvec(x.ravel()).reshape(na, nb)
+            q.put(float(np.max(np.abs(full - ref) / np.maximum(1.0, np.abs(ref)))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gather_schedule_sigma_matches_full(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    assert q.get(timeout=10) <= 1e-12
