@@ -24,10 +24,10 @@
 namespace detci_gpu {
 
 // Scatter formulation of the mixed term (sigma.cu k_mixed_scatter): largest
-// number of output alpha rows per CTA (K classes 16, 8, 4, 2, 1), shared-memory
-// budget, V-table row pitch (doubles).
+// number of output alpha rows per pass (kmax is one of 16, 8, 4, 2, 1),
+// shared-memory budget, V-table row pitch (doubles).
 constexpr int kScatterKMax = 16;
-constexpr int kScatterClasses = 5;
+constexpr int kScatterClasses = 5;   // possible kmax values (item lists cached per kmax)
 constexpr uint32_t kScatterSmem = 226u * 1024;
 inline uint32_t scatter_vpitch(int n) { return static_cast<uint32_t>((n * n + 1) & ~1); }
 // DETCI_MIXED=gather selects the gather kernel (k_mixed) for M = 1.
@@ -91,15 +91,13 @@ struct SellTable {
 
 // One output window of the scatter mixed term: alpha rows [i_lo, i_hi) of
 // this rank, whose D rows (one per (ia, position of ja in ia's singles list))
-// are sa_off[ia] - d_base; per alpha block b and K class c (K = 16 >> c) the
-// CTA items (ja, kbeg | K << 24) with ja in the block and outputs ia_k in the
-// window: each ja's list range is cut into chunks of kmax and one remainder
-// CTA (zero V rows up to its class) or, DETCI_SCATTER_REM=binary, the
-// remainder's binary decomposition.
+// are sa_off[ia] - d_base; per alpha block b the CTA items (ja, kbeg | len <<
+// 20): the run of ja's singles list whose outputs ia_k lie in the window (the
+// CTA cuts it into passes of kmax rows and one padded remainder pass).
 struct ScatterWindow {
     uint64_t i_lo = 0, i_hi = 0, d_base = 0, d_rows = 0;
     DevBuf<uint2> items[kScatterClasses];            // by log2(kmax) (built on demand)
-    std::vector<uint64_t> item_off[kScatterClasses]; // [b * classes + c], size P * classes + 1
+    std::vector<uint64_t> item_off[kScatterClasses]; // per alpha block, size P + 1
 };
 
 struct Handle {

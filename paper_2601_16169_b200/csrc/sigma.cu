@@ -613,25 +613,31 @@ struct ScatterArgs {
     uint32_t slot0, slot_end;   // beta slots [slot0, slot_end) (multi-GPU column share)
 };
 
-// M = 1 or 2 vectors share the V gathers (the multi-root block's pairs):
-// an element then costs (M + K) / (M K) gathers per FMA.
+// One pass of the scatter CTA: K output rows ia_k = list(ja)[kbeg + k], k <
+// cnt (rows cnt..K-1 padded with zero V rows).  Builds V for the pass, runs
+// the row segments (reusing the staged row when it fits whole: `staged`),
+// and stores the partials.  M = 1 or 2 vectors share the V gathers (the
+// multi-root block's pairs): an element costs (M + K) / (M K) gathers per
+// FMA.
 template <int K, int M>
-__global__ void __launch_bounds__(kMxBlock, 1)
-k_mixed_scatter(const ScatterArgs a) {
-    extern __shared__ double smem[];
-    double* const vsub = smem;                      // K rows of vpitch
-    double* const cseg = smem + K * a.vpitch;       // Cs_v[ja, segment], v < M
-    __shared__ uint64_t s_vrow[K];                  // eri row offset | sign << 63
-    __shared__ uint64_t s_drow[K];                  // D row of output k
-
-    const uint32_t item = blockIdx.x / a.nparts, part = blockIdx.x % a.nparts;
-    const uint2 it = a.items[item];
-    const uint32_t ja = it.x, kbeg = it.y & 0xffffffu, cnt = it.y >> 24;
-    const uint64_t oja = a.sa_off[ja];
+__device__ __forceinline__ void scatter_pass(const ScatterArgs& a, double* vsub, double* cseg, uint64_t* s_vrow,
+                                             uint64_t* s_drow, uint32_t ja, uint64_t oja, uint32_t kbeg,
+                                             uint32_t cnt, bool staged, uint32_t part) {
     const int n = a.norbs, nn = n * n;
     const uint32_t tid = threadIdx.x, lane = tid % kWarp;
     const uint32_t segpad = (a.seg_cols + 1) & ~1u;
-
+    const size_t crow = static_cast<size_t>(ja - a.c_row0) * a.ldc;
+    auto stage = [&](uint32_t g) {
+        const uint32_t segw = min(a.seg_cols, a.nb - g * a.seg_cols);
+#pragma unroll
+        for (int v = 0; v < M; ++v) {
+            const double* src = a.C[v] + crow + static_cast<size_t>(g) * a.seg_cols;
+            double* dst = cseg + v * segpad;
+            for (uint32_t c = tid; c < segw; c += kMxBlock) cp_async8(dst + c, src + c);
+        }
+        cp_async_commit();
+    };
+    __syncthreads();   // the previous pass is done with V, the row tables and the segment
     if (tid < K) {
         uint64_t vr = ~0ull, dr = 0;
         if (tid < cnt) {
@@ -647,19 +653,7 @@ k_mixed_scatter(const ScatterArgs a) {
         s_vrow[tid] = vr;
         s_drow[tid] = dr;
     }
-    // the first Cs segment streams in (cp.async) under the V build
-    const size_t crow = static_cast<size_t>(ja - a.c_row0) * a.ldc;
-    auto stage = [&](uint32_t g) {
-        const uint32_t segw = min(a.seg_cols, a.nb - g * a.seg_cols);
-#pragma unroll
-        for (int v = 0; v < M; ++v) {
-            const double* src = a.C[v] + crow + static_cast<size_t>(g) * a.seg_cols;
-            double* dst = cseg + v * segpad;
-            for (uint32_t c = tid; c < segw; c += kMxBlock) cp_async8(dst + c, src + c);
-        }
-        cp_async_commit();
-    };
-    stage(0);
+    if (!staged) stage(0);   // streams in under the V build
     __syncthreads();
     for (uint32_t t = tid; t < static_cast<uint32_t>(K * nn); t += kMxBlock) {
         const uint32_t k = t / nn, cd = t - k * nn;
@@ -726,6 +720,49 @@ k_mixed_scatter(const ScatterArgs a) {
         if (k < static_cast<int>(cnt))
 #pragma unroll
             for (int v = 0; v < M; ++v) a.D[v][s_drow[k] * a.ldd + (slot - a.slot0)] = acc[v][k];
+}
+
+// CTA = (item = (ja, a run of len entries of its singles list), 1024 beta
+// slots).  The row Cs[ja, .] is staged once when it fits whole (nseg == 1)
+// and serves every pass: full passes of KMAX output rows, then one padded
+// remainder pass of the next power of two >= the rest.
+template <int KMAX, int M>
+__global__ void __launch_bounds__(kMxBlock, 1)
+k_mixed_scatter(const ScatterArgs a) {
+    extern __shared__ double smem[];
+    double* const vsub = smem;                      // KMAX rows of vpitch
+    double* const cseg = smem + KMAX * a.vpitch;    // Cs_v[ja, segment], v < M
+    __shared__ uint64_t s_vrow[KMAX];               // eri row offset | sign << 63
+    __shared__ uint64_t s_drow[KMAX];               // D row of output k
+
+    const uint32_t item = blockIdx.x / a.nparts, part = blockIdx.x % a.nparts;
+    const uint2 it = a.items[item];
+    const uint32_t ja = it.x, kbeg = it.y & 0xfffffu, len = it.y >> 20;
+    const uint64_t oja = a.sa_off[ja];
+    const bool whole = a.nseg == 1;
+    if (whole) {
+        const uint32_t segpad = (a.seg_cols + 1) & ~1u;
+        const size_t crow = static_cast<size_t>(ja - a.c_row0) * a.ldc;
+#pragma unroll
+        for (int v = 0; v < M; ++v) {
+            const double* src = a.C[v] + crow;
+            double* dst = cseg + v * segpad;
+            for (uint32_t c = threadIdx.x; c < a.nb; c += kMxBlock) cp_async8(dst + c, src + c);
+        }
+        cp_async_commit();
+    }
+    uint32_t p = kbeg;
+    const uint32_t end = kbeg + len;
+#pragma unroll 1
+    for (; p + KMAX <= end; p += KMAX)
+        scatter_pass<KMAX, M>(a, vsub, cseg, s_vrow, s_drow, ja, oja, p, KMAX, whole, part);
+    const uint32_t r = end - p;
+    if (r == 0) return;
+    if constexpr (KMAX > 8) { if (r > 8) { scatter_pass<16, M>(a, vsub, cseg, s_vrow, s_drow, ja, oja, p, r, whole, part); return; } }
+    if constexpr (KMAX > 4) { if (r > 4) { scatter_pass<8, M>(a, vsub, cseg, s_vrow, s_drow, ja, oja, p, r, whole, part); return; } }
+    if constexpr (KMAX > 2) { if (r > 2) { scatter_pass<4, M>(a, vsub, cseg, s_vrow, s_drow, ja, oja, p, r, whole, part); return; } }
+    if constexpr (KMAX > 1) { if (r > 1) { scatter_pass<2, M>(a, vsub, cseg, s_vrow, s_drow, ja, oja, p, r, whole, part); return; } }
+    scatter_pass<1, M>(a, vsub, cseg, s_vrow, s_drow, ja, oja, p, r, whole, part);
 }
 
 // y[ia, ib] += eps(A_ia, B_ib) sum_{pos in [lo, hi)} D[sa_off[ia] + pos - d_base, slot]
@@ -1069,8 +1106,7 @@ void launch_mixed(Handle& h, const Ptrs& Cb, uint32_t b0, uint32_t b1, const MPt
     CUDA_LAUNCH_CHECK();
 }
 
-// Remainder policy of the scatter items: one padded CTA (default; measured
-// C2 mixed 63.7 vs 65.9 ms, C3 466 vs 477 ms) or DETCI_SCATTER_REM=binary.
+
 bool multi_ring();
 std::pair<uint32_t, uint32_t> mixed_slots(const Handle& h, int g, int P);
 
@@ -1085,11 +1121,6 @@ uint32_t mixed_ldd(const Handle& h) {
         m = std::max(m, s1 - s0);
     }
     return m;
-}
-
-bool scatter_pad_remainder() {
-    const char* e = std::getenv("DETCI_SCATTER_REM");
-    return !(e && std::string(e) == "binary");
 }
 
 // Scatter plan for block-rank g (rows [blk[g], blk[g+1])): output windows
@@ -1138,42 +1169,26 @@ const std::vector<std::unique_ptr<ScatterWindow>>& scatter_windows(Handle& h, in
     const int ki = __builtin_ctz(static_cast<unsigned>(kmax));   // items depend on kmax
     for (auto& w : wins) {
         if (!w->item_off[ki].empty()) continue;
+        // one item per ja: the run of its (window-restricted) singles list;
+        // the CTA cuts it into passes of kmax and a padded remainder
         std::vector<uint2> items;
-        std::vector<std::vector<uint2>> cls(kScatterClasses);
-        w->item_off[ki].assign(static_cast<size_t>(P) * kScatterClasses + 1, 0);
+        w->item_off[ki].assign(static_cast<size_t>(P) + 1, 0);
         for (int b = 0; b < P; ++b) {
-            for (auto& c : cls) c.clear();
+            w->item_off[ki][b] = items.size();
             const uint64_t j0 = P == 1 ? 0 : h.blk[b], j1 = P == 1 ? h.na() : h.blk[b + 1];
             for (uint64_t ja = j0; ja < j1; ++ja) {
                 const uint32_t* f = flat + off[ja];
                 const uint32_t* e = flat + off[ja + 1];
-                uint32_t p = static_cast<uint32_t>(std::lower_bound(f, e, static_cast<uint32_t>(w->i_lo)) - f);
+                const uint32_t p_lo = static_cast<uint32_t>(std::lower_bound(f, e, static_cast<uint32_t>(w->i_lo)) - f);
                 const uint32_t p_hi = static_cast<uint32_t>(std::lower_bound(f, e, static_cast<uint32_t>(w->i_hi)) - f);
-                // full chunks of kmax; the remainder r goes to one CTA of the
-                // class K = next power of two >= r (zero V rows above r), or
-                // with DETCI_SCATTER_REM=binary to its binary decomposition
-                const bool pad = scatter_pad_remainder();
-                for (int c = 0; c < kScatterClasses; ++c) {
-                    const uint32_t K = 16u >> c;
-                    if (K > static_cast<uint32_t>(kmax)) continue;
-                    while (p_hi - p >= K) {
-                        cls[c].push_back(make_uint2(static_cast<uint32_t>(ja), p | K << 24));
-                        p += K;
-                        if (K < static_cast<uint32_t>(kmax)) break;   // remainder: each smaller K at most once
-                    }
-                    const uint32_t r = p_hi - p;
-                    if (pad && r > 0 && r < K && (c + 1 == kScatterClasses || r > (K >> 1))) {
-                        cls[c].push_back(make_uint2(static_cast<uint32_t>(ja), p | r << 24));
-                        p = p_hi;
-                    }
+                if (p_hi > p_lo) {
+                    if (p_hi - p_lo >= (1u << 12) || p_lo >= (1u << 20))
+                        fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: singles list too long for the item encoding");
+                    items.push_back(make_uint2(static_cast<uint32_t>(ja), p_lo | (p_hi - p_lo) << 20));
                 }
             }
-            for (int c = 0; c < kScatterClasses; ++c) {
-                w->item_off[ki][static_cast<size_t>(b) * kScatterClasses + c] = items.size();
-                items.insert(items.end(), cls[c].begin(), cls[c].end());
-            }
         }
-        w->item_off[ki][static_cast<size_t>(P) * kScatterClasses] = items.size();
+        w->item_off[ki][P] = items.size();
         w->items[ki].alloc(std::max<size_t>(items.size(), 1));
         if (!items.empty())
             CUDA_CHECK(cudaMemcpy(w->items[ki].p, items.data(), items.size() * sizeof(uint2), cudaMemcpyHostToDevice));
@@ -1184,16 +1199,16 @@ const std::vector<std::unique_ptr<ScatterWindow>>& scatter_windows(Handle& h, in
     return wins;
 }
 
-template <int K, int M>
+template <int KMAX, int M>
 void launch_scatter_k(const ScatterArgs& a, uint64_t grid, uint32_t vpitch, size_t cbytes, cudaStream_t st) {
-    const size_t smem = static_cast<size_t>(K) * vpitch * sizeof(double) + M * cbytes;
+    const size_t smem = static_cast<size_t>(KMAX) * vpitch * sizeof(double) + M * cbytes;
     static size_t configured = 0;
     if (smem > configured) {
-        CUDA_CHECK(cudaFuncSetAttribute(k_mixed_scatter<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CUDA_CHECK(cudaFuncSetAttribute(k_mixed_scatter<KMAX, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
         configured = smem;
     }
-    k_mixed_scatter<K, M><<<static_cast<unsigned>(grid), kMxBlock, smem, st>>>(a);
+    k_mixed_scatter<KMAX, M><<<static_cast<unsigned>(grid), kMxBlock, smem, st>>>(a);
     CUDA_LAUNCH_CHECK();
 }
 
@@ -1223,9 +1238,9 @@ void launch_mixed_scatter(Handle& h, int g, int P, int b, const Ptrs& Cb, uint32
     for (size_t wi = 0; wi < wins.size(); ++wi) {
         if (only_window >= 0 && static_cast<size_t>(only_window) != wi) continue;
         const auto& w = wins[wi];
-        const size_t base = static_cast<size_t>(b) * kScatterClasses;
         const auto& io = w->item_off[ki];
-        if (io[base + kScatterClasses] == io[base]) continue;
+        const uint64_t i0 = io[b], i1 = io[b + 1];
+        if (i1 == i0) continue;
         ScatterArgs a{};
         for (int v = 0; v < M; ++v) {
             a.C[v] = Cb[v];
@@ -1254,20 +1269,19 @@ void launch_mixed_scatter(Handle& h, int g, int P, int b, const Ptrs& Cb, uint32
         if (a.slot_end <= a.slot0) return;   // empty column share (more ranks than slices)
         if (a.slot_end - a.slot0 > ldd) fail(DETCI_GPU_E_CUDA, "mixed term: slot share exceeds the D stride");
         a.nparts = (a.slot_end - a.slot0 + kMxBlock - 1) / kMxBlock;
-        for (int c = 0; c < kScatterClasses && (phases & 1); ++c) {
-            const uint64_t i0 = io[base + c], i1 = io[base + c + 1];
-            if (i1 == i0) continue;
+        if (phases & 1) {
             a.items = w->items[ki].p + i0;
             const uint64_t grid = (i1 - i0) * a.nparts;
             if (grid >= (1ull << 31)) fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: scatter grid too large");
-            switch (c) {
-                case 0: launch_scatter_k<16, 1>(a, grid, vpitch, cbytes, h.stream); break;  // kmax 16 => M == 1
-                case 1: launch_scatter_k<8, M>(a, grid, vpitch, cbytes, h.stream); break;
-                case 2: launch_scatter_k<4, M>(a, grid, vpitch, cbytes, h.stream); break;
-                case 3: launch_scatter_k<2, M>(a, grid, vpitch, cbytes, h.stream); break;
+            switch (t.kmax) {
+                case 16: launch_scatter_k<16, 1>(a, grid, vpitch, cbytes, h.stream); break;   // kmax 16 => M == 1
+                case 8: launch_scatter_k<8, M>(a, grid, vpitch, cbytes, h.stream); break;
+                case 4: launch_scatter_k<4, M>(a, grid, vpitch, cbytes, h.stream); break;
+                case 2: launch_scatter_k<2, M>(a, grid, vpitch, cbytes, h.stream); break;
                 default: launch_scatter_k<1, M>(a, grid, vpitch, cbytes, h.stream); break;
             }
         }
+
         const uint64_t lo = std::max<uint64_t>(w->i_lo, r_lo), hi = std::min<uint64_t>(w->i_hi, r_hi);
         for (int v = 0; v < M && (phases & 2) && lo < hi; ++v) {
             ReduceArgs r{};

@@ -210,18 +210,15 @@ def test_samespin_kernel_variants(kernel, monkeypatch):
             assert rel_diff(detci.matvec(b, x).reshape(len(a), -1)[r], rows["sigma_rows"]) <= 1e-12
 
 
-@pytest.mark.parametrize("mixed,dbytes,rem", [("gather", None, None), ("scatter", None, None),
-                                              ("scatter", None, "binary"), ("scatter", "3000000", None),
-                                              ("scatter", "1", "binary")])
-def test_mixed_kernel_variants(mixed, dbytes, rem, monkeypatch):
+@pytest.mark.parametrize("mixed,dbytes", [("gather", None), ("scatter", None), ("scatter", "3000000"),
+                                          ("scatter", "1")])
+def test_mixed_kernel_variants(mixed, dbytes, monkeypatch):
     """Mixed term through the gather kernel (DETCI_MIXED=gather) and the
     default scatter kernel + deterministic D reduction, with the D buffer
     forced into several output windows (DETCI_MIXED_DBYTES; "1" = one alpha
     row per window), against the reference rows at C1, the fixtures and
     virtual blocks; bitwise run-to-run determinism."""
     monkeypatch.setenv("DETCI_MIXED", mixed)
-    if rem:
-        monkeypatch.setenv("DETCI_SCATTER_REM", rem)
     if dbytes:
         monkeypatch.setenv("DETCI_MIXED_DBYTES", dbytes)
     for name in ("h4_chain", "chain8"):
