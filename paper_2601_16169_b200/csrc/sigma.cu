@@ -217,13 +217,17 @@ k_samespin(const SameSpinArgs a, uint32_t chunk0) {
 // the others from L1 (simulated 45-59% L1 hits at C2) instead of L2, which
 // bounds the one-row-per-CTA kernel (84.6% L2 throughput, 98% L2 hits).
 constexpr int kGStage = 32;   // entries staged per warp
+// Warps per SM the grouped kernel is compiled for (64 registers).  Measured:
+// 40 or 48 warps per SM (48 / 40 registers) are slower (C3 alpha 121 vs 114
+// ms): more rows in flight thrash L1.
+constexpr int kSSMinBlocks = 32;
 
 // GW warps = output rows per CTA (8 or 16; 1024 threads per SM either way)
 // kV2 (M = 1, full chunks, 16-byte aligned rows): each lane owns two pairs
 // of adjacent columns and reads them with one 16-byte load each, halving
 // the load instructions per element.
 template <bool kTail, int M, int GW, bool kV2 = false>
-__global__ void __launch_bounds__(GW * kWarp, 32 / GW)
+__global__ void __launch_bounds__(GW * kWarp, kSSMinBlocks / GW)
 k_samespin_g(const SameSpinArgs a, uint32_t chunk0, uint32_t ngroups) {
     constexpr int kGW = GW;
     constexpr int R = SSR<M>::value;
