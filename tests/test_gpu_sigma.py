@@ -300,3 +300,29 @@ def test_multi_block_schedules(multi, blocks, monkeypatch):
         Y = detci.matvec_block(b, np.stack([x, -0.5 * x, 2.0 * x]))
         for i, sc in enumerate((1.0, -0.5, 2.0)):
             assert rel_diff(Y[i], sc * y1) <= 1e-12
+
+
+def test_pipelined_host_sigma_pinned_buffers():
+    """The overlapped host sigma with page-locked buffers (truly asynchronous
+    chunk copies, as in bench.py's end-to-end leg) equals the device sigma
+    bitwise and the reference rows, over repeated calls."""
+    import ctypes as C
+    import torch
+
+    from paper_2601_16169_b200 import _lib
+
+    rows = np.load(GOLDEN / "rows_C2.npz")
+    ints, a, bb = synth.synthetic_system("C2")
+    lib = _lib.load()
+    with gpu_basis(ints, a, bb) as b:
+        x = torch.from_numpy(synth.random_vector(b.dimension(), 11)).pin_memory()
+        y = torch.empty_like(x).pin_memory()
+        dx, dy = x.cuda(), torch.empty_like(x).cuda()
+        assert lib.detci_gpu_sigma_device(b.handle, dx.data_ptr(), dy.data_ptr(), None) == 0
+        ref = dy.cpu().numpy()
+        for _ in range(3):
+            y.zero_()
+            assert lib.detci_gpu_sigma(b.handle, x.data_ptr(), y.data_ptr(), None) == 0
+            assert rel_diff(y.numpy(), ref) <= 1e-14
+        r = rows["rows"].astype(np.int64)
+        assert rel_diff(y.numpy().reshape(len(a), -1)[r], rows["sigma_rows"]) <= 1e-12
