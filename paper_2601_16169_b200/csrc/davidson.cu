@@ -442,14 +442,19 @@ void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* re
 
     size_t free_b = 0, total_b = 0;
     CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+    // the scatter D buffer is scratch: count it as free, and drop it (it is
+    // re-planned around the subspace at the next sigma) only when the
+    // subspace does not fit next to it
     const size_t need = (2 * static_cast<size_t>(ms) + 3) * n * sizeof(double);
+    const bool drop_d = need + (1ull << 30) > free_b;
+    free_b += h.dbuf.bytes();
     const uint64_t budget = h.budget ? h.budget : free_b;
     if (need > std::min<uint64_t>(budget, free_b))
         fail(DETCI_GPU_E_CAPACITY, "davidson vectors require " + std::to_string(need) +
                                        " bytes, budget is " + std::to_string(std::min<uint64_t>(budget, free_b)) +
                                        " bytes");
     DevBuf<double> store;
-    release_sigma_scratch(h);   // the scatter D buffer is re-planned around the subspace
+    if (drop_d) release_sigma_scratch(h);
     store.alloc((2 * static_cast<size_t>(ms) + 3) * n);
     auto V = [&](int j) { return store.p + static_cast<size_t>(j) * n; };
     auto Wv = [&](int j) { return store.p + static_cast<size_t>(ms + j) * n; };
@@ -690,12 +695,14 @@ void davidson_roots_device(Handle& h, const detci_dav_block_opts& opts, detci_da
     CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
     const size_t nvec = 2 * static_cast<size_t>(ms) + 3 * static_cast<size_t>(m);
     const size_t need = nvec * n * sizeof(double);
+    const bool drop_d = need + (1ull << 30) > free_b;   // as in davidson_device
+    free_b += h.dbuf.bytes();
     const uint64_t budget = std::min<uint64_t>(h.budget ? h.budget : free_b, free_b);
     if (need > budget)
         fail(DETCI_GPU_E_CAPACITY, "davidson vectors require " + std::to_string(need) + " bytes, budget is " +
                                        std::to_string(budget) + " bytes");
     DevBuf<double> store;
-    release_sigma_scratch(h);
+    if (drop_d) release_sigma_scratch(h);
     store.alloc(nvec * n);
     auto V = [&](int j) { return store.p + static_cast<size_t>(j) * n; };
     auto Wv = [&](int j) { return store.p + static_cast<size_t>(ms + j) * n; };

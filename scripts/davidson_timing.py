@@ -8,7 +8,7 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "C1"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 200
 ints, a, b = synth.synthetic_system(cfg)
 basis = detci.GpuBasis(ints.norbs, a, b, ints.core, ints.h1, ints.eri)
-for rep in range(2):
+for rep in range(int(sys.argv[3]) if len(sys.argv) > 3 else 2):
     t0 = time.time()
     res = detci.davidson_solve(basis, detci.DavidsonOptions(max_iter=iters), want_vector=False)
     wall = time.time() - t0
