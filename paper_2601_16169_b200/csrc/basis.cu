@@ -683,6 +683,7 @@ void release_basis(Handle& h) {
     h.ct.reset();
     h.yt.reset();
     h.xs.reset();
+    h.dav_store.reset();
     h.cs_full.reset();
     h.mix_t.reset();
     h.mix_r.reset();

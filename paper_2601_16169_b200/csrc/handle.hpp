@@ -150,6 +150,7 @@ struct Handle {
     DevBuf<double> ring[2];            // max_blk * nb
     DevBuf<double> xbuf, ybuf;         // host-pointer staging, local length
     DevBuf<double> red;                // reduction partials
+    DevBuf<double> dav_store;          // Davidson subspace, cached across solves
     DevBuf<unsigned int> red_count;
 
     // stored-matrix method (stored.cu): CSR of H, used by every sigma call
