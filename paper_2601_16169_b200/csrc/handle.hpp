@@ -96,6 +96,15 @@ struct SellTable {
 // CTA cuts it into passes of kmax rows and one padded remainder pass).
 struct ScatterWindow {
     uint64_t i_lo = 0, i_hi = 0, d_base = 0, d_rows = 0;
+    // Single-block plans cut the work by ja instead (items stay whole): the
+    // window holds ja in [j0, j1) for all output rows, and its D is
+    // compacted per row: D row of (ia, pos) = base[ia] + pos - lo[ia], where
+    // [lo[ia], lo[ia] + base[ia+1] - base[ia]) are the positions of the
+    // window's ja in ia's list.  (No arrays when one window covers all ja.)
+    bool by_ja = false;
+    uint64_t j0 = 0, j1 = 0;
+    DevBuf<uint32_t> lo;
+    DevBuf<uint64_t> base;
     DevBuf<uint2> items[kScatterClasses];            // by log2(kmax) (built on demand)
     std::vector<uint64_t> item_off[kScatterClasses]; // per alpha block, size P + 1
 };

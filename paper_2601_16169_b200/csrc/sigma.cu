@@ -103,7 +103,9 @@ __device__ __forceinline__ void samespin_store(const SameSpinArgs& a, uint64_t a
 #pragma unroll
     for (int vv = 0; vv < M; ++vv) {
         const double v = flip_sign(acc[vv], flip);
-        if (a.accumulate) {
+        if (a.accumulate && a.diag) {   // accumulate the diagonal term too
+            a.Y[vv][yi] += fma(a.diag[yi], a.Cself[vv][yi], v);
+        } else if (a.accumulate) {
             a.Y[vv][yi] += v;
         } else if (a.diag) {
             a.Y[vv][yi] = fma(a.diag[yi], a.Cself[vv][yi], v);
@@ -615,6 +617,8 @@ struct ScatterArgs {
     uint64_t d_base;
     uint32_t ldd;
     uint32_t slot0, slot_end;   // beta slots [slot0, slot_end) (multi-GPU column share)
+    const uint32_t* w_lo;       // ja-window D compaction (ScatterWindow::by_ja), or null
+    const uint64_t* w_base;
 };
 
 // One pass of the scatter CTA: K output rows ia_k = list(ja)[kbeg + k], k <
@@ -652,7 +656,8 @@ __device__ __forceinline__ void scatter_pass(const ScatterArgs& a, double* vsub,
             const int qa = __ffsll(static_cast<long long>(Aj & ~Ak)) - 1;
             vr = static_cast<uint64_t>(pa * n + qa) * nn |
                  static_cast<uint64_t>(mixed_alpha_parity(Ak, pa, qa)) << 63;
-            dr = a.sa_off[ia] + a.tpos[oja + kbeg + tid] - a.d_base;
+            dr = a.w_lo ? a.w_base[ia] + a.tpos[oja + kbeg + tid] - a.w_lo[ia]
+                        : a.sa_off[ia] + a.tpos[oja + kbeg + tid] - a.d_base;
         }
         s_vrow[tid] = vr;
         s_drow[tid] = dr;
@@ -789,6 +794,9 @@ struct ReduceArgs {
     uint32_t slot0, slot_end;   // slots [slot0, slot_end); D column = slot - slot0
     double* T;                  // if set: T[(ia - y_row0) * ldt + slot - slot0] = result (slot order)
     size_t ldt;
+    int t_accumulate;           // T += instead of = (later ja windows)
+    const uint32_t* w_lo;       // ja-window D compaction, or null
+    const uint64_t* w_base;
 };
 
 constexpr int kRedBlock = 256;
@@ -799,15 +807,21 @@ k_mixed_reduce(const ReduceArgs a) {
     const uint32_t ia = a.i_lo + blockIdx.x / a.nparts;
     const uint32_t slot = a.slot0 + (blockIdx.x % a.nparts) * kRedBlock + threadIdx.x;
     const uint64_t o = a.sa_off[ia];
-    if (threadIdx.x < 2) {
+    if (a.w_lo) {   // ja window: the positions and D rows come compacted
+        if (threadIdx.x == 0) {
+            s_rng[0] = a.w_lo[ia];
+            s_rng[1] = a.w_lo[ia] + static_cast<uint32_t>(a.w_base[ia + 1] - a.w_base[ia]);
+        }
+    } else if (threadIdx.x < 2) {
         const uint32_t* f = a.sa_flat + o;
         s_rng[threadIdx.x] = lower_bound_u32(f, a.sa_len[ia], threadIdx.x == 0 ? a.j0 : a.j1);
     }
     __syncthreads();
     if (slot >= a.nb || slot >= a.slot_end) return;
     const uint32_t lo = s_rng[0], hi = s_rng[1];
-    if (lo == hi && !a.T) return;
-    const double* d = a.D + (o + lo - a.d_base) * a.ldd + (slot - a.slot0);
+    if (lo == hi && (!a.T || a.t_accumulate)) return;
+    const uint64_t drow = a.w_lo ? a.w_base[ia] : o + lo - a.d_base;
+    const double* d = a.D + drow * a.ldd + (slot - a.slot0);
     double s = 0.0;
     uint32_t p = lo;
 #pragma unroll 1
@@ -821,8 +835,12 @@ k_mixed_reduce(const ReduceArgs a) {
     for (; p < hi; ++p) s += __ldcs(d + static_cast<size_t>(p - lo) * a.ldd);
     const uint32_t ib = a.perm[slot];
     const uint32_t flip = static_cast<uint32_t>(__popcll(a.alpha[ia] & a.beta_prefix[ib]));
-    if (a.T) a.T[static_cast<size_t>(ia - a.y_row0) * a.ldt + (slot - a.slot0)] = flip_sign(s, flip);
-    else a.Y[static_cast<size_t>(ia - a.y_row0) * a.ldy + ib] += flip_sign(s, flip);
+    if (a.T) {
+        double& t = a.T[static_cast<size_t>(ia - a.y_row0) * a.ldt + (slot - a.slot0)];
+        t = a.t_accumulate ? t + flip_sign(s, flip) : flip_sign(s, flip);
+    } else {
+        a.Y[static_cast<size_t>(ia - a.y_row0) * a.ldy + ib] += flip_sign(s, flip);
+    }
 }
 
 // y[r * ldy + perm[s]] += R[r * ldr + s], s < ns (perm already offset to the
@@ -1026,7 +1044,7 @@ void fill_lists(SameSpinArgs& s, const ChannelTables& t) {
 
 template <int M>
 void launch_alpha(const Handle& h, const Ptrs& Cb, uint32_t b0, uint32_t b1, const Ptrs& x_loc,
-                  const MPtrs& y_loc, uint64_t a0, uint64_t a1, bool first) {
+                  const MPtrs& y_loc, uint64_t a0, uint64_t a1, bool first, bool add_to_y = false) {
     SameSpinArgs s{};
     for (int v = 0; v < M; ++v) {
         s.C[v] = Cb[v];
@@ -1047,7 +1065,7 @@ void launch_alpha(const Handle& h, const Ptrs& Cb, uint32_t b0, uint32_t b1, con
     s.eps_row = h.ch[0].strings.p;
     s.eps_col = h.ch[1].prefix.p;
     s.diag = first ? h.diag.p + (a0 - h.a0) * h.nb() : nullptr;
-    s.accumulate = first ? 0 : 1;
+    s.accumulate = (first && !add_to_y) ? 0 : 1;   // first && add_to_y: y += diag*C + alpha
     launch_samespin<M>(s, h.stream);
 }
 
@@ -1155,10 +1173,49 @@ const std::vector<std::unique_ptr<ScatterWindow>>& scatter_windows(Handle& h, in
         h.dplan_m = M;
     }
     auto& wins = h.scatter_plan[g];
+    if (wins.empty() && P == 1) {
+        // P == 1 (also the gather schedule's column share on a multi-block
+        // handle): all output rows; windows cut the ja range, so every item
+        // keeps its whole list
+        const uint64_t na = h.na();
+        uint64_t j = 0;
+        while (j < na) {
+            auto w = std::make_unique<ScatterWindow>();
+            w->j0 = j;
+            uint64_t rows = 0;
+            while (j < na && (j == w->j0 || rows + (off[j + 1] - off[j]) <= h.dcap_rows)) {
+                rows += off[j + 1] - off[j];
+                ++j;
+            }
+            w->j1 = j;
+            w->i_lo = 0;
+            w->i_hi = na;
+            w->d_base = 0;
+            w->d_rows = rows;
+            w->by_ja = !(w->j0 == 0 && w->j1 == na);
+            if (w->by_ja) {
+                std::vector<uint32_t> lo(na);
+                std::vector<uint64_t> base(na + 1, 0);
+                for (uint64_t ia = 0; ia < na; ++ia) {
+                    const uint32_t* f = flat + off[ia];
+                    const uint32_t* e = flat + off[ia + 1];
+                    const uint32_t l = static_cast<uint32_t>(std::lower_bound(f, e, static_cast<uint32_t>(w->j0)) - f);
+                    const uint32_t hgh = static_cast<uint32_t>(std::lower_bound(f, e, static_cast<uint32_t>(w->j1)) - f);
+                    lo[ia] = l;
+                    base[ia + 1] = base[ia] + (hgh - l);
+                }
+                if (base[na] != rows) fail(DETCI_GPU_E_CUDA, "mixed term: singles lists are not mutual");
+                w->lo.alloc(na);
+                w->base.alloc(na + 1);
+                CUDA_CHECK(cudaMemcpy(w->lo.p, lo.data(), na * 4, cudaMemcpyHostToDevice));
+                CUDA_CHECK(cudaMemcpy(w->base.p, base.data(), (na + 1) * 8, cudaMemcpyHostToDevice));
+            }
+            wins.push_back(std::move(w));
+        }
+    }
     if (wins.empty()) {
-        // P == 1: all rows and all ja (also the gather schedule's column
-        // share on a multi-block handle)
-        const uint64_t r0 = P == 1 ? 0 : h.blk[g], r1 = P == 1 ? h.na() : h.blk[g + 1];
+        // block-rank of the ring schedule: windows over the rank's output rows
+        const uint64_t r0 = h.blk[g], r1 = h.blk[g + 1];
         uint64_t i = r0;
         while (i < r1) {
             auto w = std::make_unique<ScatterWindow>();
@@ -1179,12 +1236,13 @@ const std::vector<std::unique_ptr<ScatterWindow>>& scatter_windows(Handle& h, in
         w->item_off[ki].assign(static_cast<size_t>(P) + 1, 0);
         for (int b = 0; b < P; ++b) {
             w->item_off[ki][b] = items.size();
-            const uint64_t j0 = P == 1 ? 0 : h.blk[b], j1 = P == 1 ? h.na() : h.blk[b + 1];
+            const uint64_t j0 = P == 1 ? w->j0 : h.blk[b], j1 = P == 1 ? w->j1 : h.blk[b + 1];
             for (uint64_t ja = j0; ja < j1; ++ja) {
                 const uint32_t* f = flat + off[ja];
                 const uint32_t* e = flat + off[ja + 1];
-                const uint32_t p_lo = static_cast<uint32_t>(std::lower_bound(f, e, static_cast<uint32_t>(w->i_lo)) - f);
-                const uint32_t p_hi = static_cast<uint32_t>(std::lower_bound(f, e, static_cast<uint32_t>(w->i_hi)) - f);
+                const uint32_t p_lo = P == 1 ? 0u : static_cast<uint32_t>(std::lower_bound(f, e, static_cast<uint32_t>(w->i_lo)) - f);
+                const uint32_t p_hi = P == 1 ? static_cast<uint32_t>(e - f)
+                                             : static_cast<uint32_t>(std::lower_bound(f, e, static_cast<uint32_t>(w->i_hi)) - f);
                 if (p_hi > p_lo) {
                     if (p_hi - p_lo >= (1u << 12) || p_lo >= (1u << 20))
                         fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: singles list too long for the item encoding");
@@ -1268,6 +1326,8 @@ void launch_mixed_scatter(Handle& h, int g, int P, int b, const Ptrs& Cb, uint32
         a.norbs = h.norbs;
         a.d_base = w->d_base;
         a.ldd = ldd;
+        a.w_lo = w->by_ja ? w->lo.p : nullptr;
+        a.w_base = w->by_ja ? w->base.p : nullptr;
         a.slot0 = tgt.slot0;
         a.slot_end = std::min<uint32_t>(tgt.slot_end, h.nslices * kWarp);
         if (a.slot_end <= a.slot0) return;   // empty column share (more ranks than slices)
@@ -1298,6 +1358,9 @@ void launch_mixed_scatter(Handle& h, int g, int P, int b, const Ptrs& Cb, uint32
             r.nparts = (r.slot_end - r.slot0 + kRedBlock - 1) / kRedBlock;
             r.T = tgt.T[v];
             r.ldt = tgt.ldt;
+            r.t_accumulate = wi > 0 ? 1 : 0;
+            r.w_lo = a.w_lo;
+            r.w_base = a.w_base;
             r.i_lo = static_cast<uint32_t>(lo);
             r.j0 = b0;
             r.j1 = b1;
@@ -1814,38 +1877,47 @@ bool sigma_host_pipelined(Handle& h, const double* x, double* y, detci_gpu_timin
     yl[0] = dy;
     const int nw = static_cast<int>(wins.size());
     int last_chunk = -1;
-    for (int wi = 0; wi < nw; ++wi) {
-        launch_mixed_scatter<1>(h, 0, 1, 0, held, 0, static_cast<uint32_t>(h.na()), yl, a0, 1, 0, ~0ull, wi);
-        if (dbg && wi == 0) CUDA_CHECK(cudaEventRecord(e_scatter, h.stream));
-        const uint64_t w0 = wins[wi]->i_lo - a0, w1 = wins[wi]->i_hi - a0;
-        std::vector<uint64_t> edges = {w0, w1};
-        if (wi + 1 == nw) {
-            edges = pipe_edges(w1 - w0, kTailWeight);
-            for (auto& e : edges) e += w0;
-        }
-        for (size_t c = 0; c + 1 < edges.size(); ++c) {
-            const uint64_t r0 = edges[c], r1 = edges[c + 1];
-            if (r1 == r0) continue;
+    auto tail_chunk = [&](uint64_t r0, uint64_t r1, bool alpha_combine, int wi) {
+        if (r1 == r0) return;
+        if (alpha_combine) {
             Ptrs xl{};
             xl[0] = dx + r0 * nb;
             MPtrs yc{};
             yc[0] = dy + r0 * nb;
-            launch_alpha<1>(h, held, 0, static_cast<uint32_t>(h.na()), xl, yc, a0 + r0, a0 + r1, true);
+            launch_alpha<1>(h, held, 0, static_cast<uint32_t>(h.na()), xl, yc, a0 + r0, a0 + r1, true, nw > 1);
             const uint32_t rc = static_cast<uint32_t>(r1 - r0);
             dim3 tb(kTile, 8), tg(static_cast<unsigned>((nb + kTile - 1) / kTile), (rc + kTile - 1) / kTile);
             k_transpose_add_eps<<<tg, tb, 0, h.stream>>>(h.yt.p + r0, nloc, dy + r0 * nb, nb, rc,
                                                          static_cast<uint32_t>(nb), h.ch[0].strings.p + a0 + r0,
                                                          h.ch[1].prefix.p);
             CUDA_LAUNCH_CHECK();
-            launch_mixed_scatter<1>(h, 0, 1, 0, held, 0, static_cast<uint32_t>(h.na()), yl, a0, 2, a0 + r0,
-                                    a0 + r1, wi);
-            last_chunk = (last_chunk + 1) % kTailChunks;
-            cudaEvent_t done = final_rows[last_chunk];
-            CUDA_CHECK(cudaEventRecord(done, h.stream));
-            CUDA_CHECK(cudaStreamWaitEvent(h.comm_stream, done, 0));
-            CUDA_CHECK(cudaMemcpyAsync(y + r0 * nb, dy + r0 * nb, (r1 - r0) * nb * 8, cudaMemcpyDeviceToHost,
-                                       h.comm_stream));
         }
+        launch_mixed_scatter<1>(h, 0, 1, 0, held, 0, static_cast<uint32_t>(h.na()), yl, a0, 2, a0 + r0, a0 + r1, wi);
+        last_chunk = (last_chunk + 1) % kTailChunks;
+        cudaEvent_t done = final_rows[last_chunk];
+        CUDA_CHECK(cudaEventRecord(done, h.stream));
+        CUDA_CHECK(cudaStreamWaitEvent(h.comm_stream, done, 0));
+        CUDA_CHECK(cudaMemcpyAsync(y + r0 * nb, dy + r0 * nb, (r1 - r0) * nb * 8, cudaMemcpyDeviceToHost,
+                                   h.comm_stream));
+    };
+    const std::vector<uint64_t> edges = pipe_edges(nloc, kTailWeight);
+    if (nw == 1) {
+        // one window: the scatter, then per row chunk alpha term, combine,
+        // reduction and D2H (the chunk's copy runs under the next chunk)
+        launch_mixed_scatter<1>(h, 0, 1, 0, held, 0, static_cast<uint32_t>(h.na()), yl, a0, 1, 0, ~0ull, 0);
+        if (dbg) CUDA_CHECK(cudaEventRecord(e_scatter, h.stream));
+        for (size_t c = 0; c + 1 < edges.size(); ++c) tail_chunk(edges[c], edges[c + 1], true, 0);
+    } else {
+        // ja windows add into every row: y starts at zero, every window but
+        // the last adds its mixed part whole, then per row chunk the alpha
+        // term (y += diag*C + alpha), the combine, the last window's
+        // reduction and the D2H
+        CUDA_CHECK(cudaMemsetAsync(dy, 0, n * sizeof(double), h.stream));
+        for (int wi = 0; wi + 1 < nw; ++wi)
+            launch_mixed_scatter<1>(h, 0, 1, 0, held, 0, static_cast<uint32_t>(h.na()), yl, a0, 3, 0, ~0ull, wi);
+        launch_mixed_scatter<1>(h, 0, 1, 0, held, 0, static_cast<uint32_t>(h.na()), yl, a0, 1, 0, ~0ull, nw - 1);
+        if (dbg) CUDA_CHECK(cudaEventRecord(e_scatter, h.stream));
+        for (size_t c = 0; c + 1 < edges.size(); ++c) tail_chunk(edges[c], edges[c + 1], true, nw - 1);
     }
     CUDA_CHECK(cudaEventRecord(t1, h.comm_stream));
     CUDA_CHECK(cudaEventSynchronize(t1));

@@ -148,3 +148,20 @@ def test_plan_partition_weighted_balances_work():
 
         assert imbalance(wtd) <= imbalance(even) + 1e-12
         assert imbalance(wtd) < 1.01
+
+
+def test_library_then_torch_share_one_nccl():
+    """Loading libdetci_gpu.so before torch must not break torch's CUDA
+    libraries: both resolve the same libnccl.so.2 (the library's rpath points
+    at the copy torch ships)."""
+    import subprocess
+    import sys
+
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_2601_16169_b200 import _lib\n"
+            "_lib.load()\n"
+            "import torch\n"
+            "import torch.distributed\n"
+            "print('ok', torch.cuda.nccl.version())\n") % str(Path(__file__).resolve().parents[1])
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and out.stdout.startswith("ok"), out.stderr[-2000:]
