@@ -447,6 +447,9 @@ void build_mixed_sell(Handle& h, SellTable& st, int M, int format) {
                         return wv * (uw >= 0 && uw != wi) + (uc >= 0 && uc != jbl);
                     };
                     auto wkey = [](uint32_t key) { return key & 0x7fffffffu; };
+                    int vrem[16] = {0};
+                    for (int i = 0; i < 16; ++i)
+                        for (const auto& en : lanes[half * 16 + i]) ++vrem[wkey(en.second) % 16];
                     // greedy first-fit over the 16 lanes, best of a few lane orders
                     int order[16], best_order[16], best_total = 1 << 30;
                     size_t pick[16], best_pick[16];
@@ -462,14 +465,18 @@ void build_mixed_sell(Handle& h, SellTable& st, int M, int format) {
                         for (int oi = 0; oi < 16; ++oi) {
                             const auto& r = lanes[order[oi]];
                             if (r.empty()) continue;
+                            // least cost; ties go to the V bank with the most
+                            // entries left in the half-warp (keeps later steps
+                            // from running out of distinct banks)
                             size_t best = 0;
-                            int best_cost = 1 << 20;
+                            int best_cost = 1 << 20, best_rem = -1;
                             for (size_t i = 0; i < r.size(); ++i) {
                                 const int c = cost(r[i].first, r[i].second);
-                                if (c < best_cost) {
+                                const int rm = vrem[wkey(r[i].second) % 16];
+                                if (c < best_cost || (c == best_cost && rm > best_rem)) {
                                     best_cost = c;
+                                    best_rem = rm;
                                     best = i;
-                                    if (c == 0) break;
                                 }
                             }
                             pick[oi] = best;
