@@ -362,7 +362,8 @@ void build_mixed_sell(Handle& h, SellTable& st, int M, int format) {
         if (room(K) < 64 * M) fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: V rows do not fit shared memory");
         st.kmax = K;
     }
-    const uint32_t budget = format == 2 ? static_cast<uint32_t>(kScatterSmem / 8 - st.kmax * scatter_vpitch(n))
+    // (format 2 keeps a zero slot after each staged row segment: 2 doubles)
+    const uint32_t budget = format == 2 ? static_cast<uint32_t>(kScatterSmem / 8 - st.kmax * scatter_vpitch(n) - 2 * M)
                                         : 220u * 1024 / 8 - 2 * wdbl;   // doubles for C stages
     const uint32_t single_seg = std::min<uint32_t>(cap, (budget / M) & ~1u);
     const uint32_t double_seg = std::min<uint32_t>(std::min<uint32_t>(16000, cap), (budget / 2 / M) & ~1u);
@@ -511,6 +512,21 @@ void build_mixed_sell(Handle& h, SellTable& st, int M, int format) {
                                         : encode_mixed_entry(e.first, e.second);
                     }
                     for (int p = 0; p < npad; ++p) {
+                        if (format == 2) {
+                            // scatter kernel: the C side reads the zero slot
+                            // after the staged segment (index seg_cols); any V
+                            // address already read in this step (broadcast)
+                            uint32_t wz = 0;
+                            for (int i = 0; i < 16; ++i)
+                                if (used_w[i] >= 0) {
+                                    wz = static_cast<uint32_t>(used_w[i]);
+                                    break;
+                                }
+                            if (used_w[wz % 16] < 0) used_w[wz % 16] = wz;
+                            if (used_c[seg_cols % 16] < 0) used_c[seg_cols % 16] = seg_cols;
+                            out[static_cast<size_t>(k) * kWarp + pads[p]] = encode_scatter_entry(seg_cols, wz, 0);
+                            continue;
+                        }
                         // a zero of W (diagonal c == d) on a free or same-address bank
                         uint32_t wz = 0;
                         for (int c = 0; c < n; ++c) {

@@ -406,6 +406,10 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
@@ -633,7 +637,7 @@ __device__ __forceinline__ void scatter_pass(const ScatterArgs& a, double* vsub,
                                              uint32_t cnt, bool staged, uint32_t part) {
     const int n = a.norbs, nn = n * n;
     const uint32_t tid = threadIdx.x, lane = tid % kWarp;
-    const uint32_t segpad = (a.seg_cols + 1) & ~1u;
+    const uint32_t segpad = (a.seg_cols + 2) & ~1u;   // + the zero slot at seg_cols
     const size_t crow = static_cast<size_t>(ja - a.c_row0) * a.ldc;
     auto stage = [&](uint32_t g) {
         const uint32_t segw = min(a.seg_cols, a.nb - g * a.seg_cols);
@@ -662,16 +666,26 @@ __device__ __forceinline__ void scatter_pass(const ScatterArgs& a, double* vsub,
         s_vrow[tid] = vr;
         s_drow[tid] = dr;
     }
-    if (!staged) stage(0);   // streams in under the V build
+    if (!staged) stage(0);   // streams in under the V copies
     __syncthreads();
-    for (uint32_t t = tid; t < static_cast<uint32_t>(K * nn); t += kMxBlock) {
-        const uint32_t k = t / nn, cd = t - k * nn;
-        const uint64_t vr = s_vrow[k];
-        double v = 0.0;
-        if (vr != ~0ull && cd % (n + 1) != 0)   // c == d <=> cd divisible by n + 1
-            v = flip_sign(a.eri[(vr & 0x7fffffffffffffffull) + cd], static_cast<uint32_t>(vr >> 63));
-        vsub[k * a.vpitch + cd] = v;
+    // V rows: the raw ERI rows (pa qa|..) by cp.async; the alpha sign goes on
+    // the partial at the store, padding entries read the C zero slot, and
+    // rows k >= cnt copy row 0 (finite, never stored)
+    if ((nn & 1) == 0) {
+        const uint32_t h2 = static_cast<uint32_t>(nn) / 2;
+        for (uint32_t t = tid; t < static_cast<uint32_t>(K) * h2; t += kMxBlock) {
+            const uint32_t k = t / h2, u = t - k * h2;
+            const uint64_t vr = s_vrow[k < cnt ? k : 0];
+            cp_async16(vsub + k * a.vpitch + 2 * u, a.eri + (vr & 0x7fffffffffffffffull) + 2 * u);
+        }
+    } else {
+        for (uint32_t t = tid; t < static_cast<uint32_t>(K * nn); t += kMxBlock) {
+            const uint32_t k = t / nn, cd = t - k * nn;
+            const uint64_t vr = s_vrow[k < cnt ? k : 0];
+            cp_async8(vsub + k * a.vpitch + cd, a.eri + (vr & 0x7fffffffffffffffull) + cd);
+        }
     }
+    cp_async_commit();   // waited for with the first segment below
 
     const uint32_t slot = a.slot0 + part * kMxBlock + tid;
     const uint32_t sl = slot / kWarp;
@@ -726,9 +740,11 @@ __device__ __forceinline__ void scatter_pass(const ScatterArgs& a, double* vsub,
     if (!active) return;
 #pragma unroll
     for (int k = 0; k < K; ++k)
-        if (k < static_cast<int>(cnt))
+        if (k < static_cast<int>(cnt)) {
+            const uint32_t sgn = static_cast<uint32_t>(s_vrow[k] >> 63);
 #pragma unroll
-            for (int v = 0; v < M; ++v) a.D[v][s_drow[k] * a.ldd + (slot - a.slot0)] = acc[v][k];
+            for (int v = 0; v < M; ++v) a.D[v][s_drow[k] * a.ldd + (slot - a.slot0)] = flip_sign(acc[v][k], sgn);
+        }
 }
 
 // CTA = (item = (ja, a run of len entries of its singles list), 1024 beta
@@ -749,8 +765,9 @@ k_mixed_scatter(const ScatterArgs a) {
     const uint32_t ja = it.x, kbeg = it.y & 0xfffffu, len = it.y >> 20;
     const uint64_t oja = a.sa_off[ja];
     const bool whole = a.nseg == 1;
+    const uint32_t segpad = (a.seg_cols + 2) & ~1u;
+    if (threadIdx.x < M) cseg[threadIdx.x * segpad + a.seg_cols] = 0.0;   // zero slot (padding entries)
     if (whole) {
-        const uint32_t segpad = (a.seg_cols + 1) & ~1u;
         const size_t crow = static_cast<size_t>(ja - a.c_row0) * a.ldc;
 #pragma unroll
         for (int v = 0; v < M; ++v) {
@@ -1296,7 +1313,7 @@ void launch_mixed_scatter(Handle& h, int g, int P, int b, const Ptrs& Cb, uint32
     const int ki = __builtin_ctz(static_cast<unsigned>(t.kmax));
     const uint32_t ldd = mixed_ldd(h);
     const uint32_t vpitch = scatter_vpitch(h.norbs);
-    const size_t cbytes = ((t.seg_cols + 1) & ~1u) * sizeof(double);
+    const size_t cbytes = ((t.seg_cols + 2) & ~1u) * sizeof(double);   // + zero slot
     for (size_t wi = 0; wi < wins.size(); ++wi) {
         if (only_window >= 0 && static_cast<size_t>(only_window) != wi) continue;
         const auto& w = wins[wi];
