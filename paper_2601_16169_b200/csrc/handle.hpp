@@ -28,7 +28,7 @@ namespace detci_gpu {
 // shared-memory budget, V-table row pitch (doubles).
 constexpr int kScatterKMax = 16;
 constexpr int kScatterClasses = 5;   // possible kmax values (item lists cached per kmax)
-constexpr uint32_t kScatterSmem = 226u * 1024;
+constexpr uint32_t kScatterSmem = 222u * 1024;   // dynamic; + 4.3 KB static row tables <= 227 KB
 inline uint32_t scatter_vpitch(int n) { return static_cast<uint32_t>((n * n + 1) & ~1); }
 // DETCI_MIXED=gather selects the gather kernel (k_mixed) for M = 1.
 inline bool mixed_scatter_enabled() {

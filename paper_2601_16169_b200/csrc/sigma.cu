@@ -626,15 +626,32 @@ struct ScatterArgs {
 };
 
 // One pass of the scatter CTA: K output rows ia_k = list(ja)[kbeg + k], k <
-// cnt (rows cnt..K-1 padded with zero V rows).  Builds V for the pass, runs
+// cnt (rows cnt..K-1 padded: computed, never stored).  Builds V for the pass, runs
 // the row segments (reusing the staged row when it fits whole: `staged`),
 // and stores the partials.  M = 1 or 2 vectors share the V gathers (the
 // multi-root block's pairs): an element costs (M + K) / (M K) gathers per
 // FMA.
+// (V row offset | alpha sign << 63, D row) of output ia = list(ja)[pos].
+__device__ __forceinline__ void scatter_row(const ScatterArgs& a, uint32_t ja, uint64_t oja, uint32_t pos,
+                                            uint64_t& vr, uint64_t& dr) {
+    const int n = a.norbs, nn = n * n;
+    const uint64_t Aj = a.alpha[ja];
+    const uint32_t ia = a.sa_flat[oja + pos];
+    const uint64_t Ak = a.alpha[ia];
+    const int pa = __ffsll(static_cast<long long>(Ak & ~Aj)) - 1;
+    const int qa = __ffsll(static_cast<long long>(Aj & ~Ak)) - 1;
+    vr = static_cast<uint64_t>(pa * n + qa) * nn | static_cast<uint64_t>(mixed_alpha_parity(Ak, pa, qa)) << 63;
+    dr = a.w_lo ? a.w_base[ia] + a.tpos[oja + pos] - a.w_lo[ia] : a.sa_off[ia] + a.tpos[oja + pos] - a.d_base;
+}
+
+// Entries of a CTA's run whose (V row, D row) are computed once up front
+// (one latency for all passes instead of one per pass).
+constexpr uint32_t kRunPre = 256;
+
 template <int K, int M>
 __device__ __forceinline__ void scatter_pass(const ScatterArgs& a, double* vsub, double* cseg, uint64_t* s_vrow,
                                              uint64_t* s_drow, uint32_t ja, uint64_t oja, uint32_t kbeg,
-                                             uint32_t cnt, bool staged, uint32_t part) {
+                                             uint32_t cnt, bool staged, uint32_t part, bool precomputed) {
     const int n = a.norbs, nn = n * n;
     const uint32_t tid = threadIdx.x, lane = tid % kWarp;
     const uint32_t segpad = (a.seg_cols + 2) & ~1u;   // + the zero slot at seg_cols
@@ -650,19 +667,9 @@ __device__ __forceinline__ void scatter_pass(const ScatterArgs& a, double* vsub,
         cp_async_commit();
     };
     __syncthreads();   // the previous pass is done with V, the row tables and the segment
-    if (tid < K) {
+    if (!precomputed && tid < K) {
         uint64_t vr = ~0ull, dr = 0;
-        if (tid < cnt) {
-            const uint64_t Aj = a.alpha[ja];
-            const uint32_t ia = a.sa_flat[oja + kbeg + tid];
-            const uint64_t Ak = a.alpha[ia];
-            const int pa = __ffsll(static_cast<long long>(Ak & ~Aj)) - 1;
-            const int qa = __ffsll(static_cast<long long>(Aj & ~Ak)) - 1;
-            vr = static_cast<uint64_t>(pa * n + qa) * nn |
-                 static_cast<uint64_t>(mixed_alpha_parity(Ak, pa, qa)) << 63;
-            dr = a.w_lo ? a.w_base[ia] + a.tpos[oja + kbeg + tid] - a.w_lo[ia]
-                        : a.sa_off[ia] + a.tpos[oja + kbeg + tid] - a.d_base;
-        }
+        if (tid < cnt) scatter_row(a, ja, oja, kbeg + tid, vr, dr);
         s_vrow[tid] = vr;
         s_drow[tid] = dr;
     }
@@ -757,13 +764,20 @@ k_mixed_scatter(const ScatterArgs a) {
     extern __shared__ double smem[];
     double* const vsub = smem;                      // KMAX rows of vpitch
     double* const cseg = smem + KMAX * a.vpitch;    // Cs_v[ja, segment], v < M
-    __shared__ uint64_t s_vrow[KMAX];               // eri row offset | sign << 63
+    __shared__ uint64_t s_vrow[KMAX];               // eri row offset | sign << 63 (runs past kRunPre)
     __shared__ uint64_t s_drow[KMAX];               // D row of output k
+    __shared__ uint64_t s_vall[kRunPre], s_dall[kRunPre];   // the run's first kRunPre rows
 
     const uint32_t item = blockIdx.x / a.nparts, part = blockIdx.x % a.nparts;
     const uint2 it = a.items[item];
     const uint32_t ja = it.x, kbeg = it.y & 0xfffffu, len = it.y >> 20;
     const uint64_t oja = a.sa_off[ja];
+    for (uint32_t t = threadIdx.x; t < min(len, kRunPre); t += kMxBlock) {
+        uint64_t vr, dr;
+        scatter_row(a, ja, oja, kbeg + t, vr, dr);
+        s_vall[t] = vr;
+        s_dall[t] = dr;
+    }   // visible after the first pass's barrier
     const bool whole = a.nseg == 1;
     const uint32_t segpad = (a.seg_cols + 2) & ~1u;
     if (threadIdx.x < M) cseg[threadIdx.x * segpad + a.seg_cols] = 0.0;   // zero slot (padding entries)
@@ -779,16 +793,27 @@ k_mixed_scatter(const ScatterArgs a) {
     }
     uint32_t p = kbeg;
     const uint32_t end = kbeg + len;
+    // row tables of a pass: the precomputed slice, or s_vrow/s_drow
+    auto tabs = [&](uint32_t pp, uint32_t k, uint64_t*& v, uint64_t*& d) {
+        const bool pre = pp - kbeg + k <= kRunPre;
+        v = pre ? s_vall + (pp - kbeg) : s_vrow;
+        d = pre ? s_dall + (pp - kbeg) : s_drow;
+        return pre;
+    };
+    uint64_t *tv, *td;
 #pragma unroll 1
-    for (; p + KMAX <= end; p += KMAX)
-        scatter_pass<KMAX, M>(a, vsub, cseg, s_vrow, s_drow, ja, oja, p, KMAX, whole, part);
+    for (; p + KMAX <= end; p += KMAX) {
+        const bool pre = tabs(p, KMAX, tv, td);
+        scatter_pass<KMAX, M>(a, vsub, cseg, tv, td, ja, oja, p, KMAX, whole, part, pre);
+    }
     const uint32_t r = end - p;
     if (r == 0) return;
-    if constexpr (KMAX > 8) { if (r > 8) { scatter_pass<16, M>(a, vsub, cseg, s_vrow, s_drow, ja, oja, p, r, whole, part); return; } }
-    if constexpr (KMAX > 4) { if (r > 4) { scatter_pass<8, M>(a, vsub, cseg, s_vrow, s_drow, ja, oja, p, r, whole, part); return; } }
-    if constexpr (KMAX > 2) { if (r > 2) { scatter_pass<4, M>(a, vsub, cseg, s_vrow, s_drow, ja, oja, p, r, whole, part); return; } }
-    if constexpr (KMAX > 1) { if (r > 1) { scatter_pass<2, M>(a, vsub, cseg, s_vrow, s_drow, ja, oja, p, r, whole, part); return; } }
-    scatter_pass<1, M>(a, vsub, cseg, s_vrow, s_drow, ja, oja, p, r, whole, part);
+    const bool pre = tabs(p, r, tv, td);
+    if constexpr (KMAX > 8) { if (r > 8) { scatter_pass<16, M>(a, vsub, cseg, tv, td, ja, oja, p, r, whole, part, pre); return; } }
+    if constexpr (KMAX > 4) { if (r > 4) { scatter_pass<8, M>(a, vsub, cseg, tv, td, ja, oja, p, r, whole, part, pre); return; } }
+    if constexpr (KMAX > 2) { if (r > 2) { scatter_pass<4, M>(a, vsub, cseg, tv, td, ja, oja, p, r, whole, part, pre); return; } }
+    if constexpr (KMAX > 1) { if (r > 1) { scatter_pass<2, M>(a, vsub, cseg, tv, td, ja, oja, p, r, whole, part, pre); return; } }
+    scatter_pass<1, M>(a, vsub, cseg, tv, td, ja, oja, p, r, whole, part, pre);
 }
 
 // y[ia, ib] += eps(A_ia, B_ib) sum_{pos in [lo, hi)} D[sa_off[ia] + pos - d_base, slot]
