@@ -454,7 +454,10 @@ def run_gpu_arm(args):
                        "norbs": ints.norbs, "n_electrons": ints.nelec, "n_alpha": na, "n_beta": nb, "dim": dim,
                        "nnz_offdiag": nnz["total"], "nnz_alpha": nnz["alpha"], "nnz_beta": nnz["beta"],
                        "nnz_mixed": nnz["mixed"], "l2": "inputs larger than L2 (x, y = 8*dim bytes each)",
-                       "parallelism": f"alpha-block ring x{world} (NCCL send/recv)" if world > 1 else "single GPU",
+                       "parallelism": (f"alpha-block ring x{world} (NCCL send/recv)"
+                                       if os.environ.get("DETCI_MULTI") == "ring" else
+                                       f"alpha blocks x{world}: NCCL allgather of C, beta-column share of the "
+                                       f"mixed term, point-to-point exchange") if world > 1 else "single GPU",
                        "build_seconds": build_s, "sigma_s_per_iter": per_step,
                        "phase_seconds": split, "parity_rows_max_rel_err": parity},
             "roofline": roofline,
