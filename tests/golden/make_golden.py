@@ -140,6 +140,32 @@ def synthetic(ref: RefLib, c1_davidson: bool):
     return meta
 
 
+def c4_rows(ref: RefLib):
+    """C4 (1e9 determinants): two reference sigma rows and the table digests
+    (the full reference sigma is ~23 h on 8 cores; two rows take minutes)."""
+    t0 = time.time()
+    ints, a, b = synth.synthetic_system("C4")
+    entry = {"eri_sha256": eri_digest(ints), "n_strings": int(len(a)),
+             "strings_sha256": hashlib.sha256(a.tobytes()).hexdigest()}
+    tables = {}
+    for ch, strs in ((0, a), (1, b)):
+        for kind in (0, 1):
+            f, o, l = ref.generate_table(strs, ints.norbs, kind)
+            tables[f"{ch}{kind}"] = table_digest(f, o, l)
+            entry[f"len_stats_{ch}{kind}"] = [float(l.mean()), int(l.max()), int(l.sum())]
+    entry["tables_sha256"] = tables
+    rb = ref.table_from_integrals(ints).basis(a, b, cache=False, budget=48 << 30)
+    rows = np.array([0, len(a) - 1], dtype=np.uint64)
+    x = synth.random_vector(rb.dim(), 11)
+    yr = rb.matvec_rows(rows, x)
+    del x
+    np.savez_compressed(OUT / "rows_C4.npz", rows=rows, sigma_rows=yr,
+                        diag_rows=rb.diag().reshape(len(a), -1)[rows.astype(np.int64)])
+    entry["rows"] = rows.tolist()
+    print(f"C4: {time.time() - t0:.1f}s", flush=True)
+    return entry
+
+
 def elements(ref: RefLib):
     """Random connected pairs at 36 orbitals, reference hij at bit_length 20
     (multi-word determinants), for the factorized-formula check."""
@@ -183,7 +209,7 @@ def elements(ref: RefLib):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c1-davidson", action="store_true")
-    ap.add_argument("--only", choices=["fixtures", "synthetic", "elements"])
+    ap.add_argument("--only", choices=["fixtures", "synthetic", "elements", "c4"])
     args = ap.parse_args()
     ref = RefLib()
     meta_path = OUT / "golden.json"
@@ -192,6 +218,8 @@ def main():
         fixtures(ref)
     if args.only in (None, "elements"):
         meta["elements"] = elements(ref)
+    if args.only == "c4":   # not part of the default run (minutes, 16 GB of host memory)
+        meta["C4"] = c4_rows(ref)
     if args.only in (None, "synthetic"):
         syn = synthetic(ref, args.c1_davidson)
         for k, v in syn.items():

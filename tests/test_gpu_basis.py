@@ -52,7 +52,7 @@ def test_c1_tables_full_and_diag_rows():
         assert rel_diff(diag[rows["rows"].astype(np.int64)], rows["diag_rows"]) <= 1e-12
 
 
-@pytest.mark.parametrize("cfg", ["C2", "C3"])
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4"])
 def test_config_helper_lists_digest(cfg):
     meta = golden_meta()[cfg]
     ints, a, bb = synth.synthetic_system(cfg)

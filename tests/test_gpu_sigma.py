@@ -134,6 +134,26 @@ def test_config_sigma_rows_vs_reference(cfg):
         assert abs(x @ hz - y @ z) <= 1e-10 * max(1.0, abs(x @ hz))
 
 
+def test_c4_sigma_rows_vs_reference():
+    """C4 (1e9 determinants, the 8-GPU target problem, on one GPU): the first
+    and last reference sigma rows (tests/golden/make_golden.py --only c4) and
+    symmetry of the full sigma (x.Hz = z.Hx)."""
+    path = GOLDEN / "rows_C4.npz"
+    if not path.exists():
+        pytest.skip("rows_C4.npz not generated")
+    rows = np.load(path)
+    ints, a, bb = synth.synthetic_system("C4")
+    with gpu_basis(ints, a, bb) as b:
+        x = synth.random_vector(b.dimension(), 11)
+        y = detci.matvec(b, x)
+        r = rows["rows"].astype(np.int64)
+        assert rel_diff(y.reshape(len(a), -1)[r], rows["sigma_rows"]) <= 1e-12
+        assert rel_diff(b.diag().reshape(len(a), -1)[r], rows["diag_rows"]) <= 1e-12
+        z = synth.random_vector(b.dimension(), 12)
+        xhz = x @ detci.matvec(b, z)
+        assert abs(xhz - y @ z) <= 1e-10 * max(1.0, abs(xhz))
+
+
 @pytest.mark.parametrize("m,blocks", [(4, 1), (3, 1), (2, 1), (4, 3), (5, 2)])
 def test_blocked_sigma_equals_per_vector(m, blocks):
     """detci_gpu_sigma_block (M = 4/2/1 kernels, virtual blocks too) against
