@@ -582,16 +582,17 @@ void launch_mixed(Handle& h, const Ptrs& Cb, uint32_t b0, uint32_t b1, const MPt
     m.norbs = h.norbs;
     if (m.nrows == 0) return;
     const size_t smem = mixed_smem(h, t, M);
-    static size_t configured[2][kMaxM + 1] = {};
+    static size_t configured[kMaxDevices][2][kMaxM + 1] = {};
     const int db = t.double_buffer ? 1 : 0;
-    if (smem > configured[db][M]) {
+    const int dev = current_device();
+    if (smem > configured[dev][db][M]) {
         if (db)
             CUDA_CHECK(cudaFuncSetAttribute(k_mixed<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(smem)));
         else
             CUDA_CHECK(cudaFuncSetAttribute(k_mixed<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(smem)));
-        configured[db][M] = smem;
+        configured[dev][db][M] = smem;
     }
     const uint64_t grid = static_cast<uint64_t>(m.nrows) * m.nparts;
     if (db)
@@ -734,11 +735,12 @@ const std::vector<std::unique_ptr<ScatterWindow>>& scatter_windows(Handle& h, in
 template <int KMAX, int M>
 void launch_scatter_k(const ScatterArgs& a, uint64_t grid, uint32_t vpitch, size_t cbytes, cudaStream_t st) {
     const size_t smem = static_cast<size_t>(KMAX) * vpitch * sizeof(double) + M * cbytes;
-    static size_t configured = 0;
-    if (smem > configured) {
+    static size_t configured[kMaxDevices] = {};
+    const int dev = current_device();
+    if (smem > configured[dev]) {
         CUDA_CHECK(cudaFuncSetAttribute(k_mixed_scatter<KMAX, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
-        configured = smem;
+        configured[dev] = smem;
     }
     k_mixed_scatter<KMAX, M><<<static_cast<unsigned>(grid), kMxBlock, smem, st>>>(a);
     CUDA_LAUNCH_CHECK();
