@@ -513,12 +513,12 @@ k_mixed_reduce(const ReduceArgs a) {
     double s = 0.0;
     uint32_t p = lo;
 #pragma unroll 1
-    for (; p + 4 <= hi; p += 4) {
-        double v[4];
+    for (; p + 8 <= hi; p += 8) {
+        double v[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = __ldcs(d + static_cast<size_t>(p - lo + u) * a.ldd);
+        for (int u = 0; u < 8; ++u) v[u] = __ldcs(d + static_cast<size_t>(p - lo + u) * a.ldd);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) s += v[u];
+        for (int u = 0; u < 8; ++u) s += v[u];
     }
     for (; p < hi; ++p) s += __ldcs(d + static_cast<size_t>(p - lo) * a.ldd);
     const uint32_t ib = a.perm[slot];
