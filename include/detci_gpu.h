@@ -10,6 +10,9 @@
  *
  * Reference interfaces each entry point replaces:
  *   detci_gpu_create / _destroy     Basis lifetime (basis.hpp:42-79)
+ *   detci_gpu_create_loopback       the same, with the in-process rank
+ *                                   transport standing in for the paper's
+ *                                   MPI ranks (PAPER.md "Mpi2dSlide") 
  *   detci_gpu_set_strings           Basis::alpha_strings/beta_strings, the
  *                                   prepare_channel checks (basis.cpp:26-47)
  *   detci_gpu_set_integrals         IntegralTable + build_direct_exchange
@@ -143,6 +146,15 @@ int detci_gpu_abi_version(void);
 int detci_gpu_create(const detci_gpu_desc* desc, detci_gpu_handle** out);
 void detci_gpu_destroy(detci_gpu_handle* h);
 const char* detci_gpu_last_error(const detci_gpu_handle* h); /* h may be NULL */
+
+/* world_size > 1 without NCCL: the ranks of one loopback group (same
+ * `group` id, same world_size) live in ONE process, each handle driven by
+ * its own host thread, usually all on one GPU.  They exchange through device
+ * copies ordered by CUDA events and a host barrier, and run exactly the
+ * multi-rank code paths the NCCL transport runs (sigma schedules, Davidson
+ * reductions and argmin).  desc->nccl_id is ignored.  A failing collective
+ * call on one rank makes its peers' calls fail (E_ERROR) instead of hang. */
+int detci_gpu_create_loopback(const detci_gpu_desc* desc, uint64_t group, detci_gpu_handle** out);
 
 /* 128-byte NCCL unique id for rank 0 to broadcast (torch.distributed). */
 int detci_gpu_nccl_unique_id(uint8_t out[128]);

@@ -105,6 +105,7 @@ TRACE_CB = C.CFUNCTYPE(None, C.POINTER(DavIter), C.c_int, vp)
 SIGNATURES = {
     "detci_gpu_abi_version": (C.c_int, []),
     "detci_gpu_create": (C.c_int, [C.POINTER(Desc), C.POINTER(vp)]),
+    "detci_gpu_create_loopback": (C.c_int, [C.POINTER(Desc), C.c_uint64, C.POINTER(vp)]),
     "detci_gpu_destroy": (None, [vp]),
     "detci_gpu_last_error": (C.c_char_p, [vp]),
     "detci_gpu_nccl_unique_id": (C.c_int, [u8p]),

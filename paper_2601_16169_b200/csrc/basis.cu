@@ -391,8 +391,8 @@ void build_mixed_sell(Handle& h, SellTable& st, int M, int format) {
 
     std::vector<uint32_t> flat(std::max<uint64_t>(b.nflat[0], 1));
     std::vector<uint64_t> off(nb);
-    CUDA_CHECK(cudaMemcpy(flat.data(), b.flat[0].p, b.nflat[0] * 4, cudaMemcpyDeviceToHost));
-    CUDA_CHECK(cudaMemcpy(off.data(), b.offset[0].p, nb * 8, cudaMemcpyDeviceToHost));
+    copy_sync(flat.data(), b.flat[0].p, b.nflat[0] * 4, cudaMemcpyDeviceToHost, h.stream);
+    copy_sync(off.data(), b.offset[0].p, nb * 8, cudaMemcpyDeviceToHost, h.stream);
     const std::vector<uint32_t>& deg = b.h_len[0];
     std::vector<uint32_t> perm(nb);
     std::iota(perm.begin(), perm.end(), 0u);
@@ -568,12 +568,18 @@ void build_partition(Handle& h) {
     // rows are the beta term's columns, and a partial 128-column chunk runs
     // the clamped tail kernel (C3 at 8 blocks: 29 ms of tails vs 7 ms at one
     // block).  Costs <= 64 rows (3% at C3 / 8) of balance.
+    // Kept only when no block becomes empty.
     if (P > 1 && na >= 1024ull * P) {
+        std::vector<uint64_t> r = h.blk;
+        bool nonempty = true;
         for (int g = 1; g < P; ++g) {
-            uint64_t e = (h.blk[g] + 64) / 128 * 128;
-            e = std::max(e, h.blk[g - 1]);
-            h.blk[g] = std::min(e, na);
+            uint64_t e = (r[g] + 64) / 128 * 128;
+            e = std::max(e, r[g - 1]);
+            r[g] = std::min(e, na);
+            nonempty = nonempty && r[g] > r[g - 1];
         }
+        nonempty = nonempty && r[P] > r[P - 1];
+        if (nonempty) h.blk = r;
     }
     uint64_t sum_sb = 0, sum_db = 0, sum_sa = 0, sum_da = 0;
     for (uint64_t i = 0; i < nb; ++i) {
@@ -732,9 +738,12 @@ void build_device_basis(Handle& h) {
     CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
     const uint64_t budget = h.budget ? h.budget : free_b;
     const size_t need = estimate_bytes(h);
-    if (need > budget)  // basis.cpp:113-118 convention
-        fail(DETCI_GPU_E_CAPACITY, "device basis requires " + std::to_string(need) +
-                                       " bytes, budget is " + std::to_string(budget) + " bytes");
+    // basis.cpp:113-118 convention; free memory differs per rank, so the
+    // decision is collective (no rank builds while a peer has given up)
+    collective_require(h, need <= budget, DETCI_GPU_E_CAPACITY,
+                       "device basis requires " + std::to_string(need) + " bytes, budget is " +
+                           std::to_string(budget) + " bytes",
+                       "build_basis");
 
     for (int c = 0; c < 2; ++c) build_pair_tables(h, c);
     if (mixed_scatter_enabled()) scatter_table(h, 1);
@@ -744,12 +753,9 @@ void build_device_basis(Handle& h) {
     h.ct.alloc(std::max<size_t>(scratch, 1));
     h.yt.alloc(std::max<size_t>(scratch, 1));
     h.xs.alloc(std::max<size_t>(h.vblocks > 1 ? h.na() * h.nb() : scratch, 1));
-    if (std::max(h.world, h.vblocks) > 1) {
-        h.ring[0].alloc(scratch);
-        h.ring[1].alloc(scratch);
-    }
+    // (the ring buffers of DETCI_MULTI=ring are allocated by its first sigma)
     CUDA_CHECK(cudaStreamSynchronize(h.stream));
-    h.built = true;
+    h.built = all_ranks_ok(h, true);
 }
 
 } // namespace detci_gpu

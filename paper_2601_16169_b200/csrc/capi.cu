@@ -9,6 +9,9 @@
 #include <string>
 #include <vector>
 
+#include <nccl.h>
+
+#include "comm.hpp"
 #include "formulas.cuh"
 #include "handle.hpp"
 
@@ -27,25 +30,32 @@ namespace {
 
 thread_local std::string g_last_error;
 
+// collective: the call may enter rank collectives (build, sigma, Davidson).
+// A failure there aborts the rank transport, so peers blocked in (or later
+// entering) a collective fail instead of waiting forever; the handle's
+// multi-rank calls fail from then on (recreate the group).
 template <class F>
-int guarded(detci_gpu_handle* hh, F&& body) {
+int guarded(detci_gpu_handle* hh, F&& body, bool collective = false) {
+    int code = DETCI_GPU_OK;
     try {
         body();
         return DETCI_GPU_OK;
     } catch (const Failure& f) {
         if (hh) hh->h.err = f.what();
         g_last_error = f.what();
-        return f.code;
+        code = f.code;
     } catch (const std::bad_alloc&) {
         const char* msg = "host allocation failed";
         if (hh) hh->h.err = msg;
         g_last_error = msg;
-        return DETCI_GPU_E_CAPACITY;
+        code = DETCI_GPU_E_CAPACITY;
     } catch (const std::exception& e) {
         if (hh) hh->h.err = e.what();
         g_last_error = e.what();
-        return DETCI_GPU_E_ERROR;
+        code = DETCI_GPU_E_ERROR;
     }
+    if (collective && hh && hh->h.comm) hh->h.comm->abort();
+    return code;
 }
 
 void require(bool ok, int code, const std::string& msg) {
@@ -105,7 +115,9 @@ int detci_gpu_nccl_unique_id(uint8_t out[128]) {
     });
 }
 
-int detci_gpu_create(const detci_gpu_desc* desc, detci_gpu_handle** out) {
+namespace {
+// transport: 0 NCCL (desc->nccl_id), 1 loopback group `group`
+int create_handle(const detci_gpu_desc* desc, detci_gpu_handle** out, int transport, uint64_t group) {
     return guarded(nullptr, [&] {
         require(desc && out, DETCI_GPU_E_INPUT, "create: null argument");
         *out = nullptr;
@@ -132,12 +144,11 @@ int detci_gpu_create(const detci_gpu_desc* desc, detci_gpu_handle** out) {
             CUDA_CHECK(cudaStreamCreateWithFlags(&h.stream, cudaStreamNonBlocking));
             CUDA_CHECK(cudaStreamCreateWithFlags(&h.comm_stream, cudaStreamNonBlocking));
             for (auto& e : h.ev) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-            if (h.world > 1) {
+            if (h.world > 1 && transport == 0) {
                 require(desc->nccl_id != nullptr, DETCI_GPU_E_CONFIG, "create: nccl_id required");
-                ncclUniqueId id;
-                std::memcpy(&id, desc->nccl_id, sizeof(id));
-                if (ncclCommInitRank(&h.nccl, h.world, id, h.rank) != ncclSuccess)
-                    fail(DETCI_GPU_E_CUDA, "ncclCommInitRank failed");
+                h.comm = make_nccl_comm(h.rank, h.world, desc->nccl_id);
+            } else if (h.world > 1) {
+                h.comm = make_loopback_comm(group, h.rank, h.world);
             }
         } catch (...) {
             detci_gpu_destroy(hh);
@@ -145,6 +156,15 @@ int detci_gpu_create(const detci_gpu_desc* desc, detci_gpu_handle** out) {
         }
         *out = hh;
     });
+}
+} // namespace
+
+int detci_gpu_create(const detci_gpu_desc* desc, detci_gpu_handle** out) {
+    return create_handle(desc, out, 0, 0);
+}
+
+int detci_gpu_create_loopback(const detci_gpu_desc* desc, uint64_t group, detci_gpu_handle** out) {
+    return create_handle(desc, out, 1, group);
 }
 
 void detci_gpu_destroy(detci_gpu_handle* hh) {
@@ -162,7 +182,7 @@ void detci_gpu_destroy(detci_gpu_handle* hh) {
     h.d_eri.reset();
     h.red.reset();
     h.red_count.reset();
-    if (h.nccl) ncclCommDestroy(h.nccl);
+    h.comm.reset();
     for (auto& e : h.ev)
         if (e) cudaEventDestroy(e);
     if (h.stream) cudaStreamDestroy(h.stream);
@@ -212,13 +232,13 @@ int detci_gpu_set_strings(detci_gpu_handle* hh, int norbs, const uint64_t* alpha
             t.n = cnt[c];
             t.h_strings.assign(src[c], src[c] + cnt[c]);
             t.strings.alloc(t.n);
-            CUDA_CHECK(cudaMemcpy(t.strings.p, t.h_strings.data(), t.n * sizeof(uint64_t),
-                                  cudaMemcpyHostToDevice));
+            copy_sync(t.strings.p, t.h_strings.data(), t.n * sizeof(uint64_t),
+                                  cudaMemcpyHostToDevice, h.stream);
             // exclusive prefix parities P(s) for eps(A,B) = popc(A & P(B)) & 1
             std::vector<uint64_t> pre(t.n);
             for (size_t i = 0; i < t.n; ++i) pre[i] = prefix_parity(t.h_strings[i]);
             t.prefix.alloc(t.n);
-            CUDA_CHECK(cudaMemcpy(t.prefix.p, pre.data(), t.n * sizeof(uint64_t), cudaMemcpyHostToDevice));
+            copy_sync(t.prefix.p, pre.data(), t.n * sizeof(uint64_t), cudaMemcpyHostToDevice, h.stream);
         }
         h.have_strings = true;
     });
@@ -238,8 +258,8 @@ int detci_gpu_set_integrals(detci_gpu_handle* hh, double core, const double* h1,
         h.eri.assign(eri, eri + n * n * n * n);
         h.d_h1.alloc(n * n);
         h.d_eri.alloc(n * n * n * n);
-        CUDA_CHECK(cudaMemcpy(h.d_h1.p, h.h1.data(), n * n * 8, cudaMemcpyHostToDevice));
-        CUDA_CHECK(cudaMemcpy(h.d_eri.p, h.eri.data(), n * n * n * n * 8, cudaMemcpyHostToDevice));
+        copy_sync(h.d_h1.p, h.h1.data(), n * n * 8, cudaMemcpyHostToDevice, h.stream);
+        copy_sync(h.d_eri.p, h.eri.data(), n * n * n * n * 8, cudaMemcpyHostToDevice, h.stream);
         h.have_ints = true;
     });
 }
@@ -249,7 +269,7 @@ int detci_gpu_build_basis(detci_gpu_handle* hh) {
         require(hh != nullptr, DETCI_GPU_E_INPUT, "build_basis: null handle");
         activate(hh->h);
         build_device_basis(hh->h);
-    });
+    }, true);
 }
 
 int detci_gpu_helper_size(const detci_gpu_handle* hh, int channel, int kind, uint64_t* nflat) {
@@ -271,9 +291,9 @@ int detci_gpu_get_helpers(const detci_gpu_handle* hh, int channel, int kind, uin
         activate(h);
         const ChannelTables& t = h.ch[channel];
         if (flat && t.nflat[kind])
-            CUDA_CHECK(cudaMemcpy(flat, t.flat[kind].p, t.nflat[kind] * 4, cudaMemcpyDeviceToHost));
-        if (offset) CUDA_CHECK(cudaMemcpy(offset, t.offset[kind].p, t.n * 8, cudaMemcpyDeviceToHost));
-        if (len) CUDA_CHECK(cudaMemcpy(len, t.len[kind].p, t.n * 4, cudaMemcpyDeviceToHost));
+            copy_sync(flat, t.flat[kind].p, t.nflat[kind] * 4, cudaMemcpyDeviceToHost, h.stream);
+        if (offset) copy_sync(offset, t.offset[kind].p, t.n * 8, cudaMemcpyDeviceToHost, h.stream);
+        if (len) copy_sync(len, t.len[kind].p, t.n * 4, cudaMemcpyDeviceToHost, h.stream);
     });
 }
 
@@ -302,7 +322,7 @@ int detci_gpu_diag(const detci_gpu_handle* hh, double* out) {
     return guarded(const_cast<detci_gpu_handle*>(hh), [&] {
         require(hh && hh->h.built, DETCI_GPU_E_INPUT, "diag: basis not built");
         activate(hh->h);
-        CUDA_CHECK(cudaMemcpy(out, hh->h.diag.p, hh->h.local_len() * 8, cudaMemcpyDeviceToHost));
+        copy_sync(out, hh->h.diag.p, hh->h.local_len() * 8, cudaMemcpyDeviceToHost, hh->h.stream);
     });
 }
 
@@ -322,7 +342,7 @@ int detci_gpu_sigma_device(detci_gpu_handle* hh, const double* dx, double* dy, d
         activate(hh->h);
         if (tm) *tm = detci_gpu_timings{};
         sigma_device(hh->h, dx, dy, tm);
-    });
+    }, true);
 }
 
 int detci_gpu_sigma_async(detci_gpu_handle* hh, const double* dx, double* dy) {
@@ -331,7 +351,7 @@ int detci_gpu_sigma_async(detci_gpu_handle* hh, const double* dx, double* dy) {
         require(dx != dy, DETCI_GPU_E_INPUT, "sigma: x and y must not alias");
         activate(hh->h);
         sigma_enqueue(hh->h, dx, dy);
-    });
+    }, true);
 }
 
 int detci_gpu_stream(const detci_gpu_handle* hh, void** stream) {
@@ -379,7 +399,7 @@ int detci_gpu_sigma(detci_gpu_handle* hh, const double* x, double* y, detci_gpu_
             tm->total_seconds = c * 1e-3;
         }
         for (auto& ev : e) cudaEventDestroy(ev);
-    });
+    }, true);
 }
 
 int detci_gpu_alloc_vector(detci_gpu_handle* hh, double** dptr) {
@@ -416,7 +436,7 @@ int detci_gpu_davidson(detci_gpu_handle* hh, const detci_dav_opts* opts, detci_d
         require(hh && opts && res, DETCI_GPU_E_INPUT, "davidson: null argument");
         activate(hh->h);
         davidson_device(hh->h, *opts, res, cb, user);
-    });
+    }, true);
 }
 
 int detci_gpu_davidson_roots(detci_gpu_handle* hh, const detci_dav_block_opts* opts,
@@ -425,7 +445,7 @@ int detci_gpu_davidson_roots(detci_gpu_handle* hh, const detci_dav_block_opts* o
         require(hh && opts && res, DETCI_GPU_E_INPUT, "davidson_roots: null argument");
         activate(hh->h);
         davidson_roots_device(hh->h, *opts, res);
-    });
+    }, true);
 }
 
 int detci_gpu_sigma_block(detci_gpu_handle* hh, const double* const* dx, double* const* dy, int m) {
@@ -433,7 +453,7 @@ int detci_gpu_sigma_block(detci_gpu_handle* hh, const double* const* dx, double*
         require(hh && dx && dy && m >= 1, DETCI_GPU_E_INPUT, "sigma_block: bad argument");
         activate(hh->h);
         sigma_block(hh->h, dx, dy, m);
-    });
+    }, true);
 }
 
 int detci_gpu_build_stored(detci_gpu_handle* hh, uint64_t memory_budget_bytes, uint64_t* nnz) {
@@ -451,9 +471,9 @@ int detci_gpu_stored_arrays(const detci_gpu_handle* hh, uint64_t* row_offset, ui
         require(h.st_off.p != nullptr, DETCI_GPU_E_INPUT, "stored_arrays: matrix not built");
         activate(const_cast<Handle&>(h));
         const uint64_t dim = h.na() * h.nb();
-        if (row_offset) CUDA_CHECK(cudaMemcpy(row_offset, h.st_off.p, (dim + 1) * 8, cudaMemcpyDeviceToHost));
-        if (col) CUDA_CHECK(cudaMemcpy(col, h.st_col.p, h.st_nnz * 4, cudaMemcpyDeviceToHost));
-        if (value) CUDA_CHECK(cudaMemcpy(value, h.st_val.p, h.st_nnz * 8, cudaMemcpyDeviceToHost));
+        if (row_offset) copy_sync(row_offset, h.st_off.p, (dim + 1) * 8, cudaMemcpyDeviceToHost, h.stream);
+        if (col) copy_sync(col, h.st_col.p, h.st_nnz * 4, cudaMemcpyDeviceToHost, h.stream);
+        if (value) copy_sync(value, h.st_val.p, h.st_nnz * 8, cudaMemcpyDeviceToHost, h.stream);
     });
 }
 
@@ -484,8 +504,8 @@ int detci_gpu_inner_product(detci_gpu_handle* hh, const double* x, const double*
         DevBuf<double> dx, dy;
         dx.alloc(std::max<uint64_t>(n, 1));
         dy.alloc(std::max<uint64_t>(n, 1));
-        CUDA_CHECK(cudaMemcpy(dx.p, x, n * 8, cudaMemcpyHostToDevice));
-        CUDA_CHECK(cudaMemcpy(dy.p, y, n * 8, cudaMemcpyHostToDevice));
+        copy_sync(dx.p, x, n * 8, cudaMemcpyHostToDevice, hh->h.stream);
+        copy_sync(dy.p, y, n * 8, cudaMemcpyHostToDevice, hh->h.stream);
         *out = device_dot(hh->h, dx.p, dy.p, n);
     });
 }
@@ -501,8 +521,8 @@ int detci_gpu_orthonormalize(detci_gpu_handle* hh, const double* vs, int k, uint
         DevBuf<double> dv, dc;
         dv.alloc(std::max<uint64_t>(static_cast<uint64_t>(k) * n, 1));
         dc.alloc(std::max<uint64_t>(n, 1));
-        if (k) CUDA_CHECK(cudaMemcpy(dv.p, vs, static_cast<size_t>(k) * n * 8, cudaMemcpyHostToDevice));
-        CUDA_CHECK(cudaMemcpy(dc.p, candidate, n * 8, cudaMemcpyHostToDevice));
+        if (k) copy_sync(dv.p, vs, static_cast<size_t>(k) * n * 8, cudaMemcpyHostToDevice, h.stream);
+        copy_sync(dc.p, candidate, n * 8, cudaMemcpyHostToDevice, h.stream);
         for (int pass = 0; pass < 2; ++pass)
             for (int j = 0; j < k; ++j) {
                 const double* bv = dv.p + static_cast<size_t>(j) * n;
@@ -517,7 +537,7 @@ int detci_gpu_orthonormalize(detci_gpu_handle* hh, const double* vs, int k, uint
             CUDA_LAUNCH_CHECK();
         }
         CUDA_CHECK(cudaStreamSynchronize(h.stream));
-        CUDA_CHECK(cudaMemcpy(out, dc.p, n * 8, cudaMemcpyDeviceToHost));
+        copy_sync(out, dc.p, n * 8, cudaMemcpyDeviceToHost, h.stream);
     });
 }
 
@@ -530,12 +550,12 @@ int detci_gpu_precondition(detci_gpu_handle* hh, const double* residual, const d
         DevBuf<double> dr, dd;
         dr.alloc(std::max<uint64_t>(n, 1));
         dd.alloc(std::max<uint64_t>(n, 1));
-        CUDA_CHECK(cudaMemcpy(dr.p, residual, n * 8, cudaMemcpyHostToDevice));
-        CUDA_CHECK(cudaMemcpy(dd.p, diag, n * 8, cudaMemcpyHostToDevice));
+        copy_sync(dr.p, residual, n * 8, cudaMemcpyHostToDevice, h.stream);
+        copy_sync(dd.p, diag, n * 8, cudaMemcpyHostToDevice, h.stream);
         k_precondition<<<592, 256, 0, h.stream>>>(dr.p, dd.p, n, theta, dr.p);
         CUDA_LAUNCH_CHECK();
         CUDA_CHECK(cudaStreamSynchronize(h.stream));
-        CUDA_CHECK(cudaMemcpy(out, dr.p, n * 8, cudaMemcpyDeviceToHost));
+        copy_sync(out, dr.p, n * 8, cudaMemcpyDeviceToHost, h.stream);
     });
 }
 

@@ -34,6 +34,17 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 }
 
 #define CUDA_CHECK(expr) ::detci_gpu::cuda_check((expr), #expr, __FILE__, __LINE__)
+// Host<->device copy ordered on `s` and complete at return.  (A plain
+// cudaMemcpy runs on the legacy stream, which does not order with the
+// non-blocking streams the kernels run on, and a pageable H2D cudaMemcpy may
+// return before its DMA lands: a kernel launched right after on another
+// stream could read stale data.)
+inline void copy_sync(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t s) {
+    if (bytes == 0) return;
+    cuda_check(cudaMemcpyAsync(dst, src, bytes, kind, s), "cudaMemcpyAsync", __FILE__, __LINE__);
+    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize", __FILE__, __LINE__);
+}
+
 // Every kernel launch site ends with CUDA_LAUNCH_CHECK(), which also counts
 // the launch (detci_gpu_launch_count; bench.py reports it as gpu_launches).
 void count_launch();

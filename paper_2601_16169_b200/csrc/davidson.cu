@@ -6,7 +6,7 @@
 // (Jacobi on the lower triangle, as Eigen's SelfAdjointEigenSolver reads
 // it).  Reductions are two-stage with a fixed order, so a run is bitwise
 // reproducible; with several GPUs the per-rank partials are summed with
-// ncclAllReduce before use.  Algorithmic rules kept from the reference:
+// an all-reduce over the rank transport (comm.hpp) before use.  Algorithmic rules kept from the reference:
 // argmin-diagonal guess with lowest-index ties, lower-triangle projected
 // fill, 2-pass modified Gram-Schmidt with the 1e-10 dependence threshold,
 // the 1e-8 preconditioner clamp, collapse to the Ritz pair at
@@ -289,8 +289,7 @@ double* scalar_slot(Handle& h, int i) { return h.red.p + 2 * kMaxVec * kRedBlock
 
 void allreduce_device(Handle& h, double* dptr, int count) {
     if (h.world <= 1) return;
-    if (ncclAllReduce(dptr, dptr, count, ncclDouble, ncclSum, h.nccl, h.stream) != ncclSuccess)
-        fail(DETCI_GPU_E_CUDA, "ncclAllReduce failed");
+    h.comm->allreduce_sum(dptr, static_cast<size_t>(count), h.stream);
 }
 
 // Finalize `k` partial rows into device slots [slot, slot + k), allreduced.
@@ -332,13 +331,26 @@ void cgs_pass(Handle& h, double* dst, const double* src, double scale, VF&& V, i
 } // namespace
 
 void allreduce_sum(Handle& h, double* host_vals, int count) {
-    if (h.world <= 1) return;
-    ensure_red(h);
-    double* d = scalar_slot(h, 3 * kMaxVec);
+    if (h.world <= 1 || count <= 0) return;
+    if (h.red_host.n < static_cast<size_t>(count)) h.red_host.alloc(static_cast<size_t>(count));
+    double* d = h.red_host.p;
     CUDA_CHECK(cudaMemcpyAsync(d, host_vals, count * sizeof(double), cudaMemcpyHostToDevice, h.stream));
     allreduce_device(h, d, count);
     CUDA_CHECK(cudaMemcpyAsync(host_vals, d, count * sizeof(double), cudaMemcpyDeviceToHost, h.stream));
     CUDA_CHECK(cudaStreamSynchronize(h.stream));
+}
+
+bool all_ranks_ok(Handle& h, bool ok) {
+    if (h.world <= 1) return ok;
+    double bad = ok ? 0.0 : 1.0;
+    allreduce_sum(h, &bad, 1);
+    return bad == 0.0;
+}
+
+void collective_require(Handle& h, bool ok, int code, const std::string& msg, const char* what) {
+    if (all_ranks_ok(h, ok)) return;
+    if (!ok) fail(code, msg);
+    fail(DETCI_GPU_E_ERROR, std::string(what) + ": another rank failed");
 }
 
 void device_dot_many(Handle& h, const double* x, const double* const* ys, int k, uint64_t n,
@@ -430,7 +442,6 @@ void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* re
                      detci_trace_cb cb, void* user) {
     if (!h.built) fail(DETCI_GPU_E_INPUT, "davidson_solve: basis not built");
     const uint64_t n = h.local_len();
-    if (n == 0) fail(DETCI_GPU_E_INPUT, "davidson_solve: empty diagonal");
     if (!(opts.tol > 0.0)) fail(DETCI_GPU_E_CONFIG, "davidson_solve: tol must be positive");
     if (opts.max_subspace < 2) fail(DETCI_GPU_E_CONFIG, "davidson_solve: max_subspace must be >= 2");
     if (opts.max_iter < 1) fail(DETCI_GPU_E_CONFIG, "davidson_solve: max_iter must be positive");
@@ -452,10 +463,13 @@ void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* re
     const bool drop_d = grow && need + (1ull << 30) > free_b + h.dav_store.bytes();
     free_b += h.dbuf.bytes() + h.dav_store.bytes();
     const uint64_t budget = h.budget ? h.budget : free_b;
-    if (need > std::min<uint64_t>(budget, free_b))
-        fail(DETCI_GPU_E_CAPACITY, "davidson vectors require " + std::to_string(need) +
-                                       " bytes, budget is " + std::to_string(std::min<uint64_t>(budget, free_b)) +
-                                       " bytes");
+    // per-rank conditions, decided collectively
+    if (n == 0) collective_require(h, false, DETCI_GPU_E_INPUT, "davidson_solve: empty diagonal", "davidson_solve");
+    else
+        collective_require(h, need <= std::min<uint64_t>(budget, free_b), DETCI_GPU_E_CAPACITY,
+                           "davidson vectors require " + std::to_string(need) + " bytes, budget is " +
+                               std::to_string(std::min<uint64_t>(budget, free_b)) + " bytes",
+                           "davidson_solve");
     DevBuf<double>& store = h.dav_store;
     if (drop_d) release_sigma_scratch(h);
     if (grow) {
@@ -685,7 +699,6 @@ void davidson_roots_device(Handle& h, const detci_dav_block_opts& opts, detci_da
     if (!h.built) fail(DETCI_GPU_E_INPUT, "davidson_solve: basis not built");
     const uint64_t n = h.local_len();
     const int m = opts.nroots;
-    if (n == 0) fail(DETCI_GPU_E_INPUT, "davidson_solve: empty diagonal");
     if (m < 1) fail(DETCI_GPU_E_CONFIG, "davidson_roots: nroots must be positive");
     if (!(opts.tol > 0.0)) fail(DETCI_GPU_E_CONFIG, "davidson_solve: tol must be positive");
     if (opts.max_iter < 1) fail(DETCI_GPU_E_CONFIG, "davidson_solve: max_iter must be positive");
@@ -705,9 +718,12 @@ void davidson_roots_device(Handle& h, const detci_dav_block_opts& opts, detci_da
     const bool drop_d = grow && need + (1ull << 30) > free_b + h.dav_store.bytes();
     free_b += h.dbuf.bytes() + h.dav_store.bytes();
     const uint64_t budget = std::min<uint64_t>(h.budget ? h.budget : free_b, free_b);
-    if (need > budget)
-        fail(DETCI_GPU_E_CAPACITY, "davidson vectors require " + std::to_string(need) + " bytes, budget is " +
-                                       std::to_string(budget) + " bytes");
+    if (n == 0) collective_require(h, false, DETCI_GPU_E_INPUT, "davidson_solve: empty diagonal", "davidson_roots");
+    else
+        collective_require(h, need <= budget, DETCI_GPU_E_CAPACITY,
+                       "davidson vectors require " + std::to_string(need) + " bytes, budget is " +
+                           std::to_string(budget) + " bytes",
+                       "davidson_roots");
     DevBuf<double>& store = h.dav_store;
     if (drop_d) release_sigma_scratch(h);
     if (grow) {
@@ -723,7 +739,7 @@ void davidson_roots_device(Handle& h, const detci_dav_block_opts& opts, detci_da
     // guesses: the m lowest diagonal entries (lowest index first on ties)
     {
         std::vector<double> d(n);
-        CUDA_CHECK(cudaMemcpy(d.data(), h.diag.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+        copy_sync(d.data(), h.diag.p, n * sizeof(double), cudaMemcpyDeviceToHost, h.stream);
         std::vector<uint64_t> idx(n);
         for (uint64_t i = 0; i < n; ++i) idx[i] = i;
         const uint64_t keep = std::min<uint64_t>(n, static_cast<uint64_t>(m));

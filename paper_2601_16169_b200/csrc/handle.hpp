@@ -10,7 +10,6 @@
 #pragma once
 
 #include <cuda_runtime.h>
-#include <nccl.h>
 
 #include <cstdint>
 #include <cstdlib>
@@ -19,6 +18,7 @@
 #include <vector>
 
 #include "../../include/detci_gpu.h"
+#include "comm.hpp"
 #include "common.cuh"
 
 namespace detci_gpu {
@@ -172,7 +172,8 @@ struct Handle {
 
     cudaStream_t stream = nullptr, comm_stream = nullptr;
     cudaEvent_t ev[16] = {};
-    ncclComm_t nccl = nullptr;
+    std::unique_ptr<Comm> comm;        // world > 1: NCCL or loopback (comm.hpp)
+    DevBuf<double> red_host;           // allreduce_sum staging (grown to the count)
 
     uint64_t nnz_alpha = 0, nnz_beta = 0, nnz_mixed = 0;
 
@@ -221,6 +222,13 @@ double device_dot(Handle& h, const double* x, const double* y, uint64_t n);
 void device_dot_many(Handle& h, const double* x, const double* const* ys, int k, uint64_t n,
                      double* out_host);
 void allreduce_sum(Handle& h, double* host_vals, int count);
+// Collective agreement: true when every rank passes ok (world 1: ok).  Used
+// before committing to work that one rank alone could refuse (capacity), so
+// no rank is left waiting in a collective its peer never enters.
+bool all_ranks_ok(Handle& h, bool ok);
+// Every rank fails when any rank fails `ok`: the failing rank with its own
+// (code, msg), the others with E_ERROR "<what>: another rank failed".
+void collective_require(Handle& h, bool ok, int code, const std::string& msg, const char* what);
 double smallest_eigenpair(const std::vector<double>& lower, int ld, int k, std::vector<double>& vec);
 void jacobi_eigen(const std::vector<double>& lower, int ld, int k, std::vector<double>& evals,
                   std::vector<double>& vecs);

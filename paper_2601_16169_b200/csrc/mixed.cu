@@ -582,18 +582,9 @@ void launch_mixed(Handle& h, const Ptrs& Cb, uint32_t b0, uint32_t b1, const MPt
     m.norbs = h.norbs;
     if (m.nrows == 0) return;
     const size_t smem = mixed_smem(h, t, M);
-    static size_t configured[kMaxDevices][2][kMaxM + 1] = {};
     const int db = t.double_buffer ? 1 : 0;
-    const int dev = current_device();
-    if (smem > configured[dev][db][M]) {
-        if (db)
-            CUDA_CHECK(cudaFuncSetAttribute(k_mixed<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(smem)));
-        else
-            CUDA_CHECK(cudaFuncSetAttribute(k_mixed<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(smem)));
-        configured[dev][db][M] = smem;
-    }
+    if (db) ensure_dynamic_smem(reinterpret_cast<const void*>(k_mixed<M, true>), smem);
+    else ensure_dynamic_smem(reinterpret_cast<const void*>(k_mixed<M, false>), smem);
     const uint64_t grid = static_cast<uint64_t>(m.nrows) * m.nparts;
     if (db)
         k_mixed<M, true><<<static_cast<unsigned>(grid), kMxBlock, smem, h.stream>>>(m);
@@ -678,8 +669,8 @@ const std::vector<std::unique_ptr<ScatterWindow>>& scatter_windows(Handle& h, in
                 if (base[na] != rows) fail(DETCI_GPU_E_CUDA, "mixed term: singles lists are not mutual");
                 w->lo.alloc(na);
                 w->base.alloc(na + 1);
-                CUDA_CHECK(cudaMemcpy(w->lo.p, lo.data(), na * 4, cudaMemcpyHostToDevice));
-                CUDA_CHECK(cudaMemcpy(w->base.p, base.data(), (na + 1) * 8, cudaMemcpyHostToDevice));
+                copy_sync(w->lo.p, lo.data(), na * 4, cudaMemcpyHostToDevice, h.stream);
+                copy_sync(w->base.p, base.data(), (na + 1) * 8, cudaMemcpyHostToDevice, h.stream);
             }
             wins.push_back(std::move(w));
         }
@@ -724,7 +715,7 @@ const std::vector<std::unique_ptr<ScatterWindow>>& scatter_windows(Handle& h, in
         w->item_off[ki][P] = items.size();
         w->items[ki].alloc(std::max<size_t>(items.size(), 1));
         if (!items.empty())
-            CUDA_CHECK(cudaMemcpy(w->items[ki].p, items.data(), items.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+            copy_sync(w->items[ki].p, items.data(), items.size() * sizeof(uint2), cudaMemcpyHostToDevice, h.stream);
     }
     uint64_t need = 0;
     for (auto& w : wins) need = std::max(need, w->d_rows);
@@ -735,13 +726,7 @@ const std::vector<std::unique_ptr<ScatterWindow>>& scatter_windows(Handle& h, in
 template <int KMAX, int M>
 void launch_scatter_k(const ScatterArgs& a, uint64_t grid, uint32_t vpitch, size_t cbytes, cudaStream_t st) {
     const size_t smem = static_cast<size_t>(KMAX) * vpitch * sizeof(double) + M * cbytes;
-    static size_t configured[kMaxDevices] = {};
-    const int dev = current_device();
-    if (smem > configured[dev]) {
-        CUDA_CHECK(cudaFuncSetAttribute(k_mixed_scatter<KMAX, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem)));
-        configured[dev] = smem;
-    }
+    ensure_dynamic_smem(reinterpret_cast<const void*>(k_mixed_scatter<KMAX, M>), smem);
     k_mixed_scatter<KMAX, M><<<static_cast<unsigned>(grid), kMxBlock, smem, st>>>(a);
     CUDA_LAUNCH_CHECK();
 }

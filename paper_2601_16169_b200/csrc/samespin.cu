@@ -330,16 +330,10 @@ void launch_samespin_g(const SameSpinArgs& s, cudaStream_t st) {
     const uint64_t full = s.ncols / kChunk;
     const bool tail = s.ncols % kChunk != 0;
     const uint32_t ngroups = (s.nrows + GW - 1) / GW;
-    static bool configured[kMaxDevices] = {};
-    const int dev = current_device();
-    if (!configured[dev]) {  // favour L1 over shared memory (the kernel uses <= 32 KB)
-        CUDA_CHECK(cudaFuncSetAttribute(k_samespin_g<false, M, GW>, cudaFuncAttributePreferredSharedMemoryCarveout, 10));
-        CUDA_CHECK(cudaFuncSetAttribute(k_samespin_g<true, M, GW>, cudaFuncAttributePreferredSharedMemoryCarveout, 10));
-        if constexpr (M == 1)
-            CUDA_CHECK(cudaFuncSetAttribute(k_samespin_g<false, 1, GW, true>,
-                                            cudaFuncAttributePreferredSharedMemoryCarveout, 10));
-        configured[dev] = true;
-    }
+    // favour L1 over shared memory (the kernel uses <= 32 KB)
+    ensure_carveout(reinterpret_cast<const void*>(k_samespin_g<false, M, GW>), 10);
+    ensure_carveout(reinterpret_cast<const void*>(k_samespin_g<true, M, GW>), 10);
+    if constexpr (M == 1) ensure_carveout(reinterpret_cast<const void*>(k_samespin_g<false, 1, GW, true>), 10);
     // 16-byte loads need even strides and 16-byte aligned bases
     const bool v2 = M == 1 && samespin_vec2() && s.ldc % 2 == 0 && s.ldj % 2 == 0 &&
                     reinterpret_cast<uintptr_t>(s.C[0]) % 16 == 0 && reinterpret_cast<uintptr_t>(s.J) % 16 == 0;

@@ -296,7 +296,8 @@ void ensure_gather_scratch(Handle& h, int M, int P) {
     }
 }
 
-// One rank (world > 1) of the gather schedule over NCCL.
+// One rank (world > 1) of the gather schedule over the rank transport
+// (comm.hpp: NCCL, or the in-process loopback).
 template <int M>
 void sigma_gather_rank(Handle& h, const Ptrs& x_loc, const MPtrs& y_loc, PhaseTimer& tm) {
     const int g = h.rank, P = h.world;
@@ -313,15 +314,13 @@ void sigma_gather_rank(Handle& h, const Ptrs& x_loc, const MPtrs& y_loc, PhaseTi
     CUDA_CHECK(cudaEventRecord(h.ev[4], h.stream));
     CUDA_CHECK(cudaStreamWaitEvent(h.comm_stream, h.ev[4], 0));
     // allgather of the P row blocks (in-place broadcasts from each owner)
-    if (ncclGroupStart() != ncclSuccess) fail(DETCI_GPU_E_CUDA, "ncclGroupStart");
+    h.comm->group_start();
     for (int v = 0; v < M; ++v)
         for (int b = 0; b < P; ++b) {
             double* blk = h.cs_full.p + v * full + h.blk[b] * nb;
-            const size_t n = (h.blk[b + 1] - h.blk[b]) * nb;
-            if (n && ncclBroadcast(blk, blk, n, ncclDouble, b, h.nccl, h.comm_stream) != ncclSuccess)
-                fail(DETCI_GPU_E_CUDA, "ncclBroadcast (Cs allgather)");
+            h.comm->broadcast(blk, (h.blk[b + 1] - h.blk[b]) * nb, b, h.comm_stream);
         }
-    if (ncclGroupEnd() != ncclSuccess) fail(DETCI_GPU_E_CUDA, "ncclGroupEnd (Cs allgather)");
+    h.comm->group_end();
     CUDA_CHECK(cudaEventRecord(h.ev[5], h.comm_stream));
     beta_term<M>(h, a0, a1);                        // local, under the allgather
     tm.end(id);
@@ -345,7 +344,7 @@ void sigma_gather_rank(Handle& h, const Ptrs& x_loc, const MPtrs& y_loc, PhaseTi
         const auto [t0, t1] = mixed_slots(h, b, P);
         roff[b + 1] = roff[b] + nloc * (t1 - t0);
     }
-    if (ncclGroupStart() != ncclSuccess) fail(DETCI_GPU_E_CUDA, "ncclGroupStart");
+    h.comm->group_start();
     for (int v = 0; v < M; ++v)
         for (int b = 0; b < P; ++b) {
             const auto [t0, t1] = mixed_slots(h, b, P);
@@ -357,12 +356,10 @@ void sigma_gather_rank(Handle& h, const Ptrs& x_loc, const MPtrs& y_loc, PhaseTi
                     CUDA_CHECK(cudaMemcpyAsync(dst, src, send_n * 8, cudaMemcpyDeviceToDevice, h.comm_stream));
                 continue;
             }
-            if (send_n && ncclSend(src, send_n, ncclDouble, b, h.nccl, h.comm_stream) != ncclSuccess)
-                fail(DETCI_GPU_E_CUDA, "ncclSend (mixed slab)");
-            if (recv_n && ncclRecv(dst, recv_n, ncclDouble, b, h.nccl, h.comm_stream) != ncclSuccess)
-                fail(DETCI_GPU_E_CUDA, "ncclRecv (mixed slab)");
+            h.comm->send(src, send_n, b, h.comm_stream);
+            h.comm->recv(dst, recv_n, b, h.comm_stream);
         }
-    if (ncclGroupEnd() != ncclSuccess) fail(DETCI_GPU_E_CUDA, "ncclGroupEnd (mixed slab)");
+    h.comm->group_end();
     CUDA_CHECK(cudaEventRecord(h.ev[7], h.comm_stream));
     CUDA_CHECK(cudaStreamWaitEvent(h.stream, h.ev[7], 0));
     for (int v = 0; v < M; ++v)
@@ -445,12 +442,12 @@ void sigma_schedule_m(Handle& h, const Ptrs& dx, const MPtrs& dy, PhaseTimer& tm
             const int cur = (g + s) % P;
             const size_t send_n = (h.blk[cur + 1] - h.blk[cur]) * nb;
             const size_t recv_n = (h.blk[next + 1] - h.blk[next]) * nb;
-            if (ncclGroupStart() != ncclSuccess) fail(DETCI_GPU_E_CUDA, "ncclGroupStart");
+            h.comm->group_start();
             for (int v = 0; v < M; ++v) {
-                ncclSend(held[v], send_n, ncclDouble, (g - 1 + P) % P, h.nccl, h.comm_stream);
-                ncclRecv(dst + v * block, recv_n, ncclDouble, (g + 1) % P, h.nccl, h.comm_stream);
+                h.comm->send(held[v], send_n, (g - 1 + P) % P, h.comm_stream);
+                h.comm->recv(dst + v * block, recv_n, (g + 1) % P, h.comm_stream);
             }
-            if (ncclGroupEnd() != ncclSuccess) fail(DETCI_GPU_E_CUDA, "ncclGroupEnd (ring)");
+            h.comm->group_end();
         });
     } else if (P > 1) {
         // Virtual blocks: every block-rank's schedule runs in turn on this GPU;

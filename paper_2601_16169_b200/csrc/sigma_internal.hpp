@@ -7,22 +7,13 @@
 #include <cstdint>
 #include <utility>
 
+#include "comm.hpp"
 #include "handle.hpp"
 
 namespace detci_gpu {
 
 constexpr int kMaxM = 4;   // vectors per blocked pass
 constexpr int kMxBlock = 1024;   // mixed-term CTA: one per SM, 32 warps
-
-// Kernel attributes (shared-memory limits, carveouts) are per device and
-// one process may drive several GPUs: launchers keep their "already set"
-// records per device.
-constexpr int kMaxDevices = 64;
-inline int current_device() {
-    int d = 0;
-    CUDA_CHECK(cudaGetDevice(&d));
-    return d < kMaxDevices ? d : kMaxDevices - 1;
-}
 
 using Ptrs = std::array<const double*, kMaxM>;
 using MPtrs = std::array<double*, kMaxM>;

@@ -51,6 +51,9 @@ class BasisOptions:
     nccl_id: Optional[bytes] = None
     virtual_blocks: int = 1
     weighted_partition: bool = False
+    # world_size ranks in this process (one host thread each) over the
+    # loopback transport instead of NCCL; ranks of one group share the id
+    loopback_group: Optional[int] = None
 
 
 @dataclass
@@ -100,7 +103,11 @@ class GpuBasis:
         desc.virtual_blocks = opts.virtual_blocks
         desc.weighted_partition = int(opts.weighted_partition)
         desc.memory_budget_bytes = opts.memory_budget_bytes
-        self._check(self._lib.detci_gpu_create(C.byref(desc), C.byref(self._h)), use_handle=False)
+        if opts.loopback_group is not None:
+            self._check(self._lib.detci_gpu_create_loopback(C.byref(desc), int(opts.loopback_group),
+                                                            C.byref(self._h)), use_handle=False)
+        else:
+            self._check(self._lib.detci_gpu_create(C.byref(desc), C.byref(self._h)), use_handle=False)
         self.norbs = int(norbs)
         self.alpha = _u64(alpha)
         self.beta = _u64(beta)
