@@ -227,6 +227,19 @@ int detci_gpu_alloc_vector(detci_gpu_handle* h, double** dptr);
 int detci_gpu_free_vector(detci_gpu_handle* h, double* dptr);
 int detci_gpu_copy_vector(detci_gpu_handle* h, double* dst, const double* src, int kind);
 
+/* Shape of the single-GPU sigma plan (diagnostics, bench roofline): the
+ * mixed term's scatter pass width K, Cs row segments, ja windows of the D
+ * partials (0 before the first sigma), SELL entries incl. padding, and the
+ * D buffer size. */
+typedef struct {
+    int mixed_kmax;
+    int mixed_segments;
+    int mixed_windows;
+    uint64_t mixed_sell_entries;
+    uint64_t d_bytes;
+} detci_gpu_plan;
+int detci_gpu_sigma_plan(const detci_gpu_handle* h, detci_gpu_plan* out);
+
 /* ---- Davidson -------------------------------------------------------------- */
 int detci_gpu_davidson(detci_gpu_handle* h, const detci_dav_opts* opts, detci_dav_result* res,
                        detci_trace_cb cb, void* user);

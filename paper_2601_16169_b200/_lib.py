@@ -99,6 +99,11 @@ class DavBlockResult(C.Structure):
     ]
 
 
+class Plan(C.Structure):
+    _fields_ = [("mixed_kmax", C.c_int), ("mixed_segments", C.c_int), ("mixed_windows", C.c_int),
+                ("mixed_sell_entries", C.c_uint64), ("d_bytes", C.c_uint64)]
+
+
 TRACE_CB = C.CFUNCTYPE(None, C.POINTER(DavIter), C.c_int, vp)
 
 # name -> (restype, argtypes); mirrors include/detci_gpu.h exactly
@@ -122,6 +127,7 @@ SIGNATURES = {
     "detci_gpu_sigma_async": (C.c_int, [vp, vp, vp]),
     "detci_gpu_stream": (C.c_int, [vp, C.POINTER(vp)]),
     "detci_gpu_launch_count": (C.c_int, [u64p]),
+    "detci_gpu_sigma_plan": (C.c_int, [vp, C.POINTER(Plan)]),
     "detci_gpu_alloc_vector": (C.c_int, [vp, C.POINTER(vp)]),
     "detci_gpu_free_vector": (C.c_int, [vp, vp]),
     "detci_gpu_copy_vector": (C.c_int, [vp, vp, vp, C.c_int]),

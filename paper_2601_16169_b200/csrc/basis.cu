@@ -363,7 +363,7 @@ void build_mixed_sell(Handle& h, SellTable& st, int M, int format) {
         st.kmax = K;
     }
     // (format 2 keeps a zero slot after each staged row segment: 2 doubles)
-    const uint32_t budget = format == 2 ? static_cast<uint32_t>(kScatterSmem / 8 - st.kmax * scatter_vpitch(n) - 2 * M)
+    const uint32_t budget = format == 2 ? static_cast<uint32_t>(kScatterSmem / 8 - st.kmax * scatter_vpitch(n) - 3 * M)
                                         : 220u * 1024 / 8 - 2 * wdbl;   // doubles for C stages
     const uint32_t single_seg = std::min<uint32_t>(cap, (budget / M) & ~1u);
     const uint32_t double_seg = std::min<uint32_t>(std::min<uint32_t>(16000, cap), (budget / 2 / M) & ~1u);
@@ -433,8 +433,11 @@ void build_mixed_sell(Handle& h, SellTable& st, int M, int format) {
                     const uint32_t jb = flat[off[ib] + k];
                     if (jb / seg_cols != g) continue;
                     const MixedMove mv = mixed_move(bs[ib], bs[jb], n);
+                    // format 2: the pair-ERI column tri(pb, qb) (V rows are
+                    // pair-ERI rows); format 1: the +-W index
+                    const uint32_t pcol = tri_index(static_cast<int>(mv.cd) / n, static_cast<int>(mv.cd) % n);
                     lanes[l].emplace_back(jb - g * seg_cols,
-                                          format == 2 ? (mv.cd | mv.sbit << 31) : mv.cd + mv.sbit * nn);
+                                          format == 2 ? (pcol | mv.sbit << 31) : mv.cd + mv.sbit * nn);
                 }
             }
             const uint32_t L = slen[sl * nseg + g];
@@ -726,6 +729,23 @@ void release_basis(Handle& h) {
     h.built = false;
 }
 
+// Pair-ERI matrix PE[tri(p,q)][tri(r,s)] = (pq|rs) over unordered pairs
+// p != q, r != s (rows padded to scatter_vpitch): the scatter kernel's V rows.
+// 8-fold symmetry of the real integrals ((pq|rs) = (qp|rs) = (pq|sr); the
+// reference reads them that way, integrals.hpp) makes one value per pair.
+void build_pair_eri(Handle& h) {
+    const int n = h.norbs;
+    const uint32_t T = pair_count(n), vp = scatter_vpitch(n);
+    std::vector<double> pe(static_cast<size_t>(std::max<uint32_t>(T, 1)) * vp, 0.0);
+    for (int p = 1; p < n; ++p)
+        for (int q = 0; q < p; ++q)
+            for (int r = 1; r < n; ++r)
+                for (int s = 0; s < r; ++s)
+                    pe[static_cast<size_t>(tri_index(p, q)) * vp + tri_index(r, s)] = eri_at(h.eri.data(), n, p, q, r, s);
+    h.d_pair.alloc(pe.size());
+    copy_sync(h.d_pair.p, pe.data(), pe.size() * sizeof(double), cudaMemcpyHostToDevice, h.stream);
+}
+
 void build_device_basis(Handle& h) {
     if (!h.have_strings) fail(DETCI_GPU_E_INPUT, "build_basis: strings not set");
     if (!h.have_ints) fail(DETCI_GPU_E_INPUT, "build_basis: integrals not set");
@@ -746,6 +766,7 @@ void build_device_basis(Handle& h) {
                        "build_basis");
 
     for (int c = 0; c < 2; ++c) build_pair_tables(h, c);
+    build_pair_eri(h);
     if (mixed_scatter_enabled()) scatter_table(h, 1);
     else build_mixed_sell(h, h.sell_m[0], 1, 1);
     build_diag(h);

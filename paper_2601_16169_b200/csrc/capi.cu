@@ -402,6 +402,20 @@ int detci_gpu_sigma(detci_gpu_handle* hh, const double* x, double* y, detci_gpu_
     }, true);
 }
 
+int detci_gpu_sigma_plan(const detci_gpu_handle* hh, detci_gpu_plan* out) {
+    return guarded(const_cast<detci_gpu_handle*>(hh), [&] {
+        require(hh && out && hh->h.built, DETCI_GPU_E_INPUT, "sigma_plan: basis not built");
+        const Handle& h = hh->h;
+        *out = detci_gpu_plan{};
+        const SellTable& t = h.sell_scatter[0];
+        out->mixed_kmax = t.kmax;
+        out->mixed_segments = static_cast<int>(t.nseg);
+        out->mixed_windows = h.scatter_plan.empty() ? 0 : static_cast<int>(h.scatter_plan[0].size());
+        out->mixed_sell_entries = t.sell.n;
+        out->d_bytes = h.dbuf.bytes();
+    });
+}
+
 int detci_gpu_alloc_vector(detci_gpu_handle* hh, double** dptr) {
     return guarded(hh, [&] {
         require(hh && hh->h.built && dptr, DETCI_GPU_E_INPUT, "alloc_vector: basis not built");

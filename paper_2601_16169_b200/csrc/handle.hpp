@@ -11,6 +11,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <memory>
@@ -29,7 +30,15 @@ namespace detci_gpu {
 constexpr int kScatterKMax = 16;
 constexpr int kScatterClasses = 5;   // possible kmax values (item lists cached per kmax)
 constexpr uint32_t kScatterSmem = 222u * 1024;   // dynamic; + 4.3 KB static row tables <= 227 KB
-inline uint32_t scatter_vpitch(int n) { return static_cast<uint32_t>((n * n + 1) & ~1); }
+// V rows of the scatter kernel are rows of the pair-ERI matrix
+// PE[tri(pa,qa)][tri(pb,qb)] = (pa qa|pb qb) (8-fold symmetry: one value per
+// unordered beta move), pitch even so every row is 16-byte aligned.
+inline uint32_t pair_count(int n) { return static_cast<uint32_t>(n * (n - 1) / 2); }
+inline uint32_t scatter_vpitch(int n) { return std::max<uint32_t>(2, (pair_count(n) + 1) & ~1u); }
+// Staged Cs row segment of seg_cols doubles: one double of alignment shift
+// (the bulk copy needs source and destination congruent mod 16 bytes) and
+// the zero slot the padding entries read, rounded to an even pitch.
+__host__ __device__ inline uint32_t scatter_segpad(uint32_t seg_cols) { return (seg_cols + 3) & ~1u; }
 // DETCI_MIXED=gather selects the gather kernel (k_mixed) for M = 1.
 inline bool mixed_scatter_enabled() {
     const char* e = std::getenv("DETCI_MIXED");
@@ -123,6 +132,7 @@ struct Handle {
     double core = 0.0;
     std::vector<double> h1, eri;
     DevBuf<double> d_h1, d_eri;
+    DevBuf<double> d_pair;             // pair-ERI matrix (scatter_vpitch rows), scatter V rows
 
     ChannelTables ch[2];
 

@@ -261,8 +261,7 @@ struct ScatterArgs {
     const uint32_t* sell;
     const uint64_t* sell_off;
     const uint32_t* sell_len;
-    const double* eri;
-    int norbs;
+    const double* pair;         // pair-ERI matrix, rows of vpitch doubles
     double* D[2];               // D_v row (sa_off[ia] + pos - d_base), ldd slots
     uint64_t d_base;
     uint32_t ldd;
@@ -271,22 +270,18 @@ struct ScatterArgs {
     const uint64_t* w_base;
 };
 
-// One pass of the scatter CTA: K output rows ia_k = list(ja)[kbeg + k], k <
-// cnt (rows cnt..K-1 padded: computed, never stored).  Builds V for the pass, runs
-// the row segments (reusing the staged row when it fits whole: `staged`),
-// and stores the partials.  M = 1 or 2 vectors share the V gathers (the
-// multi-root block's pairs): an element costs (M + K) / (M K) gathers per
-// FMA.
 // (V row offset | alpha sign << 63, D row) of output ia = list(ja)[pos].
+// The V row of the alpha move pa -> qa is row tri(pa, qa) of the pair-ERI
+// matrix: V[tri(pb, qb)] = (pa qa|pb qb).
 __device__ __forceinline__ void scatter_row(const ScatterArgs& a, uint32_t ja, uint64_t oja, uint32_t pos,
                                             uint64_t& vr, uint64_t& dr) {
-    const int n = a.norbs, nn = n * n;
     const uint64_t Aj = a.alpha[ja];
     const uint32_t ia = a.sa_flat[oja + pos];
     const uint64_t Ak = a.alpha[ia];
     const int pa = __ffsll(static_cast<long long>(Ak & ~Aj)) - 1;
     const int qa = __ffsll(static_cast<long long>(Aj & ~Ak)) - 1;
-    vr = static_cast<uint64_t>(pa * n + qa) * nn | static_cast<uint64_t>(mixed_alpha_parity(Ak, pa, qa)) << 63;
+    vr = static_cast<uint64_t>(tri_index(pa, qa)) * a.vpitch |
+         static_cast<uint64_t>(mixed_alpha_parity(Ak, pa, qa)) << 63;
     dr = a.w_lo ? a.w_base[ia] + a.tpos[oja + pos] - a.w_lo[ia] : a.sa_off[ia] + a.tpos[oja + pos] - a.d_base;
 }
 
@@ -294,51 +289,91 @@ __device__ __forceinline__ void scatter_row(const ScatterArgs& a, uint32_t ja, u
 // (one latency for all passes instead of one per pass).
 constexpr uint32_t kRunPre = 256;
 
+// Staging of one Cs row segment (doubles [g * seg_cols, + segw) of row ja,
+// vector v) into its smem slot by 1-D TMA: the 16-byte aligned interior by
+// one bulk copy (issued by the elected thread, completing on `bar`), the
+// unaligned first / last double by plain stores.  The smem row is shifted
+// by one double when the source starts at 8 mod 16 so that source and
+// destination stay congruent; returns that shift.
+__device__ __forceinline__ uint32_t seg_shift(const double* src) {
+    return static_cast<uint32_t>((reinterpret_cast<uintptr_t>(src) >> 3) & 1u);
+}
+// bytes the elected thread's bulk copy of the segment moves
+__device__ __forceinline__ uint32_t seg_bulk_bytes(const double* src, uint32_t segw) {
+    const uintptr_t s = reinterpret_cast<uintptr_t>(src), e = s + static_cast<uintptr_t>(segw) * 8;
+    const uintptr_t s0 = (s + 15) & ~uintptr_t{15}, e0 = e & ~uintptr_t{15};
+    return e0 > s0 ? static_cast<uint32_t>(e0 - s0) : 0u;
+}
+__device__ __forceinline__ void seg_issue(double* dst, const double* src, uint32_t segw, uint64_t* bar) {
+    const uint32_t sh = seg_shift(src);
+    const uint32_t bytes = seg_bulk_bytes(src, segw);
+    if (bytes) bulk_g2s(dst + sh + sh, src + sh, bytes, bar);   // element i at dst + sh + i
+}
+// The doubles outside the bulk copy (at most one at each end) by plain
+// stores, and the zero slot the padding entries read (element seg_cols of
+// the shifted row; never overlaps the copy, segpad >= seg_cols + 2).
+__device__ __forceinline__ void seg_edges(double* dst, const double* src, uint32_t segw, uint32_t seg_cols,
+                                          uint32_t t) {
+    const uint32_t sh = seg_shift(src);
+    const uint32_t bytes = seg_bulk_bytes(src, segw);
+    const uint32_t first = sh, last = first + bytes / 8;   // bulk covers [first, last)
+    if (t == 0) {
+        if (first > 0 && segw > 0) dst[sh] = src[0];
+        dst[sh + seg_cols] = 0.0;
+    }
+    if (t == 1)
+        for (uint32_t i = (bytes ? last : first); i < segw; ++i) dst[sh + i] = src[i];
+}
+
+// One pass of the scatter CTA: K output rows ia_k = list(ja)[kbeg + k], k <
+// cnt (rows cnt..K-1 padded: computed, never stored).  The elected thread
+// stages the pass's K V rows (pair-ERI rows, one 1-D TMA bulk copy each) and,
+// unless the whole row is already resident (`staged`), the Cs row segments,
+// all completing on the CTA's mbarrier; every thread then walks its SELL
+// entries (one 4-byte entry per element, prefetched a batch ahead) and
+// stores its K partials.  M = 1 or 2 vectors share the V gathers (the
+// multi-root block's pairs): an element costs (M + K) / (M K) gathers per
+// FMA.
 template <int K, int M>
 __device__ __forceinline__ void scatter_pass(const ScatterArgs& a, double* vsub, double* cseg, uint64_t* s_vrow,
-                                             uint64_t* s_drow, uint32_t ja, uint64_t oja, uint32_t kbeg,
-                                             uint32_t cnt, bool staged, uint32_t part, bool precomputed) {
-    const int n = a.norbs, nn = n * n;
+                                             uint64_t* s_drow, uint64_t* bar, uint32_t& phase, uint32_t ja,
+                                             uint64_t oja, uint32_t kbeg, uint32_t cnt, bool staged, bool stage_row,
+                                             uint32_t part, bool precomputed) {
     const uint32_t tid = threadIdx.x, lane = tid % kWarp;
-    const uint32_t segpad = (a.seg_cols + 2) & ~1u;   // + the zero slot at seg_cols
+    const uint32_t segpad = scatter_segpad(a.seg_cols);
     const size_t crow = static_cast<size_t>(ja - a.c_row0) * a.ldc;
-    auto stage = [&](uint32_t g) {
-        const uint32_t segw = min(a.seg_cols, a.nb - g * a.seg_cols);
-#pragma unroll
-        for (int v = 0; v < M; ++v) {
-            const double* src = a.C[v] + crow + static_cast<size_t>(g) * a.seg_cols;
-            double* dst = cseg + v * segpad;
-            for (uint32_t c = tid; c < segw; c += kMxBlock) cp_async8(dst + c, src + c);
-        }
-        cp_async_commit();
-    };
+    const uint32_t vbytes = a.vpitch * 8;
     __syncthreads();   // the previous pass is done with V, the row tables and the segment
-    if (!precomputed && tid < K) {
-        uint64_t vr = ~0ull, dr = 0;
-        if (tid < cnt) scatter_row(a, ja, oja, kbeg + tid, vr, dr);
-        s_vrow[tid] = vr;
-        s_drow[tid] = dr;
-    }
-    if (!staged) stage(0);   // streams in under the V copies
-    __syncthreads();
-    // V rows: the raw ERI rows (pa qa|..) by cp.async; the alpha sign goes on
-    // the partial at the store, padding entries read the C zero slot, and
-    // rows k >= cnt copy row 0 (finite, never stored)
-    if ((nn & 1) == 0) {
-        const uint32_t h2 = static_cast<uint32_t>(nn) / 2;
-        for (uint32_t t = tid; t < static_cast<uint32_t>(K) * h2; t += kMxBlock) {
-            const uint32_t k = t / h2, u = t - k * h2;
-            const uint64_t vr = s_vrow[k < cnt ? k : 0];
-            cp_async16(vsub + k * a.vpitch + 2 * u, a.eri + (vr & 0x7fffffffffffffffull) + 2 * u);
+    if (!precomputed) {
+        if (tid < K) {
+            uint64_t vr = ~0ull, dr = 0;
+            if (tid < cnt) scatter_row(a, ja, oja, kbeg + tid, vr, dr);
+            s_vrow[tid] = vr;
+            s_drow[tid] = dr;
         }
-    } else {
-        for (uint32_t t = tid; t < static_cast<uint32_t>(K * nn); t += kMxBlock) {
-            const uint32_t k = t / nn, cd = t - k * nn;
-            const uint64_t vr = s_vrow[k < cnt ? k : 0];
-            cp_async8(vsub + k * a.vpitch + cd, a.eri + (vr & 0x7fffffffffffffffull) + cd);
-        }
+        __syncthreads();
     }
-    cp_async_commit();   // waited for with the first segment below
+    // segment g of vector v: source and smem slot
+    auto seg_src = [&](int v, uint32_t g) { return a.C[v] + crow + static_cast<size_t>(g) * a.seg_cols; };
+    auto seg_w = [&](uint32_t g) { return min(a.seg_cols, a.nb - g * a.seg_cols); };
+    // elected thread: V rows of this pass (+ segment 0, or the whole row on
+    // the CTA's first pass), one arrive with the byte count
+    if (tid == 0) {
+        fence_proxy_async_smem();   // the CTA's reads of the old V / segment precede the new writes
+        uint32_t bytes = static_cast<uint32_t>(K) * vbytes;
+        const bool seg0 = stage_row || !staged;
+        if (seg0)
+            for (int v = 0; v < M; ++v) bytes += seg_bulk_bytes(seg_src(v, 0), seg_w(0));
+        mbar_arrive_expect_tx(bar, bytes);
+        for (int k = 0; k < K; ++k) {
+            const uint64_t vr = s_vrow[k < static_cast<int>(cnt) ? k : 0];
+            bulk_g2s(vsub + k * a.vpitch, a.pair + (vr & 0x7fffffffffffffffull), vbytes, bar);
+        }
+        if (seg0)
+            for (int v = 0; v < M; ++v) seg_issue(cseg + v * segpad, seg_src(v, 0), seg_w(0), bar);
+    }
+    if ((stage_row || !staged) && tid < 2)
+        for (int v = 0; v < M; ++v) seg_edges(cseg + v * segpad, seg_src(v, 0), seg_w(0), a.seg_cols, tid);
 
     const uint32_t slot = a.slot0 + part * kMxBlock + tid;
     const uint32_t sl = slot / kWarp;
@@ -349,43 +384,69 @@ __device__ __forceinline__ void scatter_pass(const ScatterArgs& a, double* vsub,
 #pragma unroll
         for (int k = 0; k < K; ++k) acc[v][k] = 0.0;
     const char* vb = reinterpret_cast<const char*>(vsub);
-    const char* cb = reinterpret_cast<const char*>(cseg);
-    const uint32_t vstride = a.vpitch * 8, cstride = segpad * 8;
-
-    auto element = [&](uint32_t e) {
-        const char* cp = cb + (e & 0x3ffffu);
-        double c[M];
-#pragma unroll
-        for (int v = 0; v < M; ++v)
-            c[v] = xor_sign(*reinterpret_cast<const double*>(cp + v * cstride), e & 0x80000000u);
-        const char* vp = vb + ((e >> 15) & 0x7ff8u);
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const double w = *reinterpret_cast<const double*>(vp + k * vstride);
-#pragma unroll
-            for (int v = 0; v < M; ++v) acc[v][k] = fma(w, c[v], acc[v][k]);
-        }
-    };
+    const uint32_t vstride = a.vpitch * 8;
 
 #pragma unroll 1
     for (uint32_t g = 0; g < a.nseg; ++g) {
         if (g > 0) {
             __syncthreads();   // previous segment consumed
-            stage(g);
+            if (tid == 0) {
+                fence_proxy_async_smem();
+                uint32_t bytes = 0;
+                for (int v = 0; v < M; ++v) bytes += seg_bulk_bytes(seg_src(v, g), seg_w(g));
+                mbar_arrive_expect_tx(bar, bytes);
+                for (int v = 0; v < M; ++v) seg_issue(cseg + v * segpad, seg_src(v, g), seg_w(g), bar);
+            }
+            if (tid < 2)
+                for (int v = 0; v < M; ++v) seg_edges(cseg + v * segpad, seg_src(v, g), seg_w(g), a.seg_cols, tid);
         }
-        cp_async_wait_all();
-        __syncthreads();
+        const bool fresh = g > 0 || stage_row || !staged;   // this segment was (re)staged just now
+        mbar_wait(bar, phase);   // V rows (g == 0) and the segment's bulk bytes landed
+        phase ^= 1u;
+        if (fresh) __syncthreads();   // plain-store edges and zero slot visible
         if (!active) continue;
+        // per vector: the staged row starts one double in when its source
+        // was misaligned (seg_shift)
+        const char* cbv[M];
+#pragma unroll
+        for (int v = 0; v < M; ++v)
+            cbv[v] = reinterpret_cast<const char*>(cseg + v * segpad + seg_shift(seg_src(v, g)));
+        auto element = [&](uint32_t e) {
+            const uint32_t co = e & 0x3ffffu;
+            double c[M];
+#pragma unroll
+            for (int v = 0; v < M; ++v)
+                c[v] = xor_sign(*reinterpret_cast<const double*>(cbv[v] + co), e & 0x80000000u);
+            const char* vp = vb + ((e >> 15) & 0x7ff8u);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const double w = *reinterpret_cast<const double*>(vp + k * vstride);
+#pragma unroll
+                for (int v = 0; v < M; ++v) acc[v][k] = fma(w, c[v], acc[v][k]);
+            }
+        };
         const uint32_t L = a.sell_len[sl * a.nseg + g];
         const uint32_t* ent = a.sell + a.sell_off[sl * a.nseg + g] + lane;
         uint32_t t = 0;
-#pragma unroll 1
-        for (; t + 4 <= L; t += 4) {
+        if (L >= 4) {
+            // batches of 4 entries, the next batch's loads in flight while
+            // the current one is consumed
             uint32_t e[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) e[u] = __ldg(ent + static_cast<size_t>(t + u) * kWarp);
+            for (int u = 0; u < 4; ++u) e[u] = __ldg(ent + static_cast<size_t>(u) * kWarp);
+#pragma unroll 1
+            for (; t + 8 <= L; t += 4) {
+                uint32_t nx[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) nx[u] = __ldg(ent + static_cast<size_t>(t + 4 + u) * kWarp);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) element(e[u]);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) e[u] = nx[u];
+            }
 #pragma unroll
             for (int u = 0; u < 4; ++u) element(e[u]);
+            t += 4;
         }
 #pragma unroll 1
         for (; t < L; ++t) element(__ldg(ent + static_cast<size_t>(t) * kWarp));
@@ -403,21 +464,28 @@ __device__ __forceinline__ void scatter_pass(const ScatterArgs& a, double* vsub,
 // CTA = (item = (ja, a run of len entries of its singles list), 1024 beta
 // slots).  The row Cs[ja, .] is staged once when it fits whole (nseg == 1)
 // and serves every pass: full passes of KMAX output rows, then one padded
-// remainder pass of the next power of two >= the rest.
+// remainder pass of the next power of two >= the rest.  All staging is 1-D
+// TMA (cp.async.bulk) issued by one thread and completing on one mbarrier
+// (one phase per pass and segment).
 template <int KMAX, int M>
 __global__ void __launch_bounds__(kMxBlock, 1)
 k_mixed_scatter(const ScatterArgs a) {
-    extern __shared__ double smem[];
+    extern __shared__ __align__(16) double smem[];
     double* const vsub = smem;                      // KMAX rows of vpitch
-    double* const cseg = smem + KMAX * a.vpitch;    // Cs_v[ja, segment], v < M
-    __shared__ uint64_t s_vrow[KMAX];               // eri row offset | sign << 63 (runs past kRunPre)
+    double* const cseg = smem + KMAX * a.vpitch;    // Cs_v[ja, segment], v < M (scatter_segpad each)
+    __shared__ uint64_t s_vrow[KMAX];               // pair row offset | sign << 63 (runs past kRunPre)
     __shared__ uint64_t s_drow[KMAX];               // D row of output k
     __shared__ uint64_t s_vall[kRunPre], s_dall[kRunPre];   // the run's first kRunPre rows
+    __shared__ uint64_t bar;
 
     const uint32_t item = blockIdx.x / a.nparts, part = blockIdx.x % a.nparts;
     const uint2 it = a.items[item];
     const uint32_t ja = it.x, kbeg = it.y & 0xfffffu, len = it.y >> 20;
     const uint64_t oja = a.sa_off[ja];
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
     for (uint32_t t = threadIdx.x; t < min(len, kRunPre); t += kMxBlock) {
         uint64_t vr, dr;
         scatter_row(a, ja, oja, kbeg + t, vr, dr);
@@ -425,18 +493,7 @@ k_mixed_scatter(const ScatterArgs a) {
         s_dall[t] = dr;
     }   // visible after the first pass's barrier
     const bool whole = a.nseg == 1;
-    const uint32_t segpad = (a.seg_cols + 2) & ~1u;
-    if (threadIdx.x < M) cseg[threadIdx.x * segpad + a.seg_cols] = 0.0;   // zero slot (padding entries)
-    if (whole) {
-        const size_t crow = static_cast<size_t>(ja - a.c_row0) * a.ldc;
-#pragma unroll
-        for (int v = 0; v < M; ++v) {
-            const double* src = a.C[v] + crow;
-            double* dst = cseg + v * segpad;
-            for (uint32_t c = threadIdx.x; c < a.nb; c += kMxBlock) cp_async8(dst + c, src + c);
-        }
-        cp_async_commit();
-    }
+    uint32_t phase = 0;
     uint32_t p = kbeg;
     const uint32_t end = kbeg + len;
     // row tables of a pass: the precomputed slice, or s_vrow/s_drow
@@ -447,19 +504,23 @@ k_mixed_scatter(const ScatterArgs a) {
         return pre;
     };
     uint64_t *tv, *td;
+    bool first = true;
 #pragma unroll 1
     for (; p + KMAX <= end; p += KMAX) {
         const bool pre = tabs(p, KMAX, tv, td);
-        scatter_pass<KMAX, M>(a, vsub, cseg, tv, td, ja, oja, p, KMAX, whole, part, pre);
+        scatter_pass<KMAX, M>(a, vsub, cseg, tv, td, &bar, phase, ja, oja, p, KMAX, whole && !first,
+                              whole && first, part, pre);
+        first = false;
     }
     const uint32_t r = end - p;
     if (r == 0) return;
     const bool pre = tabs(p, r, tv, td);
-    if constexpr (KMAX > 8) { if (r > 8) { scatter_pass<16, M>(a, vsub, cseg, tv, td, ja, oja, p, r, whole, part, pre); return; } }
-    if constexpr (KMAX > 4) { if (r > 4) { scatter_pass<8, M>(a, vsub, cseg, tv, td, ja, oja, p, r, whole, part, pre); return; } }
-    if constexpr (KMAX > 2) { if (r > 2) { scatter_pass<4, M>(a, vsub, cseg, tv, td, ja, oja, p, r, whole, part, pre); return; } }
-    if constexpr (KMAX > 1) { if (r > 1) { scatter_pass<2, M>(a, vsub, cseg, tv, td, ja, oja, p, r, whole, part, pre); return; } }
-    scatter_pass<1, M>(a, vsub, cseg, tv, td, ja, oja, p, r, whole, part, pre);
+    const bool st = whole && !first, sr = whole && first;
+    if constexpr (KMAX > 8) { if (r > 8) { scatter_pass<16, M>(a, vsub, cseg, tv, td, &bar, phase, ja, oja, p, r, st, sr, part, pre); return; } }
+    if constexpr (KMAX > 4) { if (r > 4) { scatter_pass<8, M>(a, vsub, cseg, tv, td, &bar, phase, ja, oja, p, r, st, sr, part, pre); return; } }
+    if constexpr (KMAX > 2) { if (r > 2) { scatter_pass<4, M>(a, vsub, cseg, tv, td, &bar, phase, ja, oja, p, r, st, sr, part, pre); return; } }
+    if constexpr (KMAX > 1) { if (r > 1) { scatter_pass<2, M>(a, vsub, cseg, tv, td, &bar, phase, ja, oja, p, r, st, sr, part, pre); return; } }
+    scatter_pass<1, M>(a, vsub, cseg, tv, td, &bar, phase, ja, oja, p, r, st, sr, part, pre);
 }
 
 // y[ia, ib] += eps(A_ia, B_ib) sum_{pos in [lo, hi)} D[sa_off[ia] + pos - d_base, slot]
@@ -726,6 +787,7 @@ const std::vector<std::unique_ptr<ScatterWindow>>& scatter_windows(Handle& h, in
 template <int KMAX, int M>
 void launch_scatter_k(const ScatterArgs& a, uint64_t grid, uint32_t vpitch, size_t cbytes, cudaStream_t st) {
     const size_t smem = static_cast<size_t>(KMAX) * vpitch * sizeof(double) + M * cbytes;
+    if (smem > kScatterSmem) fail(DETCI_GPU_E_CUDA, "mixed term: scatter plan exceeds shared memory");
     ensure_dynamic_smem(reinterpret_cast<const void*>(k_mixed_scatter<KMAX, M>), smem);
     k_mixed_scatter<KMAX, M><<<static_cast<unsigned>(grid), kMxBlock, smem, st>>>(a);
     CUDA_LAUNCH_CHECK();
@@ -745,7 +807,7 @@ void launch_mixed_scatter(Handle& h, int g, int P, int b, const Ptrs& Cb, uint32
     const int ki = __builtin_ctz(static_cast<unsigned>(t.kmax));
     const uint32_t ldd = mixed_ldd(h);
     const uint32_t vpitch = scatter_vpitch(h.norbs);
-    const size_t cbytes = ((t.seg_cols + 2) & ~1u) * sizeof(double);   // + zero slot
+    const size_t cbytes = scatter_segpad(t.seg_cols) * sizeof(double);   // + shift and zero slot
     for (size_t wi = 0; wi < wins.size(); ++wi) {
         if (only_window >= 0 && static_cast<size_t>(only_window) != wi) continue;
         const auto& w = wins[wi];
@@ -771,8 +833,7 @@ void launch_mixed_scatter(Handle& h, int g, int P, int b, const Ptrs& Cb, uint32
         a.sell = t.sell.p;
         a.sell_off = t.off.p;
         a.sell_len = t.len.p;
-        a.eri = h.d_eri.p;
-        a.norbs = h.norbs;
+        a.pair = h.d_pair.p;
         a.d_base = w->d_base;
         a.ldd = ldd;
         a.w_lo = w->by_ja ? w->lo.p : nullptr;

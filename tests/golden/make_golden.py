@@ -166,6 +166,32 @@ def c4_rows(ref: RefLib):
     return entry
 
 
+def interior_rows(ref: RefLib, cfg: str, nrand: int):
+    """Reference sigma rows away from the edges (the edge rows
+    alone cannot see a wrong interior row): `nrand` seeded random alpha rows
+    plus the rows of largest and smallest alpha singles / doubles degree and
+    the middle rows.  At C3 these rows straddle the two ja windows of the
+    one-GPU scatter plan; at C4 every row goes through the segmented
+    (nseg = 2) Cs staging."""
+    t0 = time.time()
+    ints, a, b = synth.synthetic_system(cfg)
+    rb = ref.table_from_integrals(ints).basis(a, b, cache=False, budget=48 << 30)
+    la = [ref.generate_table(a, ints.norbs, kind)[2] for kind in (0, 1)]
+    rng = np.random.default_rng(2026)
+    picks = set(int(r) for r in rng.choice(np.arange(1, len(a) - 1), size=nrand, replace=False))
+    picks |= {int(np.argmax(la[0])), int(np.argmin(la[0])), int(np.argmax(la[1])), int(np.argmin(la[1])),
+              len(a) // 2 - 1, len(a) // 2}
+    rows = np.array(sorted(picks), dtype=np.uint64)
+    x = synth.random_vector(rb.dim(), 11)
+    yr = rb.matvec_rows(rows, x)
+    del x
+    np.savez_compressed(OUT / f"rows_{cfg}_interior.npz", rows=rows, sigma_rows=yr,
+                        diag_rows=rb.diag().reshape(len(a), -1)[rows.astype(np.int64)],
+                        singles_degree=la[0][rows.astype(np.int64)], doubles_degree=la[1][rows.astype(np.int64)])
+    print(f"{cfg} interior: {len(rows)} rows, {time.time() - t0:.1f}s", flush=True)
+    return {"rows": rows.tolist(), "seconds": time.time() - t0}
+
+
 def elements(ref: RefLib):
     """Random connected pairs at 36 orbitals, reference hij at bit_length 20
     (multi-word determinants), for the factorized-formula check."""
@@ -209,7 +235,8 @@ def elements(ref: RefLib):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c1-davidson", action="store_true")
-    ap.add_argument("--only", choices=["fixtures", "synthetic", "elements", "c4"])
+    ap.add_argument("--only", choices=["fixtures", "synthetic", "elements", "c4", "interior"])
+    ap.add_argument("--interior", default="C3:20,C4:10", help="cfg:n_random_rows list for --only interior")
     args = ap.parse_args()
     ref = RefLib()
     meta_path = OUT / "golden.json"
@@ -220,6 +247,11 @@ def main():
         meta["elements"] = elements(ref)
     if args.only == "c4":   # not part of the default run (minutes, 16 GB of host memory)
         meta["C4"] = c4_rows(ref)
+    if args.only == "interior":   # not part of the default run (C4: hours on 8 cores)
+        for item in args.interior.split(","):
+            cfg, n = item.split(":")
+            meta.setdefault(cfg, {})["interior"] = interior_rows(ref, cfg, int(n))
+            meta_path.write_text(json.dumps(meta, indent=1))
     if args.only in (None, "synthetic"):
         syn = synthetic(ref, args.c1_davidson)
         for k, v in syn.items():
