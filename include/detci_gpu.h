@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define DETCI_GPU_ABI_VERSION 1
+#define DETCI_GPU_ABI_VERSION 2
 
 enum detci_gpu_status {
     DETCI_GPU_OK = 0,
@@ -85,6 +85,8 @@ typedef struct {
     double h2d_seconds;       /* host -> device copy of x (host-pointer calls) */
     double d2h_seconds;       /* device -> host copy of y */
     double total_seconds;
+    double mixed_reduce_seconds; /* of mixed_seconds: the deterministic D
+                                    reductions (k_mixed_reduce) */
 } detci_gpu_timings;
 
 typedef struct {
@@ -237,6 +239,11 @@ typedef struct {
     int mixed_windows;
     uint64_t mixed_sell_entries;
     uint64_t d_bytes;
+    /* per sigma (one vector), from the plan: shared-memory load bytes the
+     * scatter kernels issue (V and Cs gathers incl. padding), and the D bytes
+     * the reductions read (0 before the first sigma) */
+    uint64_t mixed_lds_bytes;
+    uint64_t d_read_bytes;
 } detci_gpu_plan;
 int detci_gpu_sigma_plan(const detci_gpu_handle* h, detci_gpu_plan* out);
 

@@ -41,6 +41,7 @@ class Timings(C.Structure):
         ("h2d_seconds", C.c_double),
         ("d2h_seconds", C.c_double),
         ("total_seconds", C.c_double),
+        ("mixed_reduce_seconds", C.c_double),
     ]
 
     def as_dict(self):
@@ -101,7 +102,8 @@ class DavBlockResult(C.Structure):
 
 class Plan(C.Structure):
     _fields_ = [("mixed_kmax", C.c_int), ("mixed_segments", C.c_int), ("mixed_windows", C.c_int),
-                ("mixed_sell_entries", C.c_uint64), ("d_bytes", C.c_uint64)]
+                ("mixed_sell_entries", C.c_uint64), ("d_bytes", C.c_uint64),
+                ("mixed_lds_bytes", C.c_uint64), ("d_read_bytes", C.c_uint64)]
 
 
 TRACE_CB = C.CFUNCTYPE(None, C.POINTER(DavIter), C.c_int, vp)

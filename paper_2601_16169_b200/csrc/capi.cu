@@ -413,6 +413,26 @@ int detci_gpu_sigma_plan(const detci_gpu_handle* hh, detci_gpu_plan* out) {
         out->mixed_windows = h.scatter_plan.empty() ? 0 : static_cast<int>(h.scatter_plan[0].size());
         out->mixed_sell_entries = t.sell.n;
         out->d_bytes = h.dbuf.bytes();
+        // single-GPU plan (P = 1): one item per ja with its whole singles
+        // list, cut into passes of kmax rows plus one remainder pass padded
+        // to the next power of two; every pass walks all SELL entries and
+        // issues (K + 1) 8-byte loads per entry (K V rows, one Cs gather)
+        if (t.kmax > 0 && h.h_sa_off.size() == h.na() + 1) {
+            uint64_t loads_per_entry = 0, pairs = 0;
+            for (size_t ja = 0; ja < h.na(); ++ja) {
+                const uint64_t len = h.h_sa_off[ja + 1] - h.h_sa_off[ja];
+                pairs += len;
+                const uint64_t full = len / t.kmax, rem = len % t.kmax;
+                loads_per_entry += full * (t.kmax + 1);
+                if (rem) {
+                    uint64_t k = 1;
+                    while (k < rem) k <<= 1;
+                    loads_per_entry += k + 1;
+                }
+            }
+            out->mixed_lds_bytes = 8 * t.sell.n * loads_per_entry;
+            out->d_read_bytes = h.scatter_plan.empty() ? 0 : 8 * pairs * h.nb();
+        }
     });
 }
 

@@ -68,6 +68,8 @@ struct DevBuf {
     size_t bytes() const { return n * sizeof(T); }
 };
 
+struct PhaseTimer;   // sigma_internal.hpp
+
 struct ChannelTables {
     size_t n = 0;                      // strings in this channel (global)
     int n_elec = 0;
@@ -180,6 +182,7 @@ struct Handle {
     uint64_t st_nnz = 0;
     bool use_stored = false;
 
+    PhaseTimer* timer = nullptr;       // set while a timed sigma runs
     cudaStream_t stream = nullptr, comm_stream = nullptr;
     cudaEvent_t ev[16] = {};
     std::unique_ptr<Comm> comm;        // world > 1: NCCL or loopback (comm.hpp)

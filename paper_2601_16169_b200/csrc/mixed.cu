@@ -884,8 +884,10 @@ void launch_mixed_scatter(Handle& h, int g, int P, int b, const Ptrs& Cb, uint32
             r.ldy = h.nb();
             r.y_row0 = static_cast<uint32_t>(a0);
             const uint64_t rgrid = (hi - lo) * r.nparts;
+            const int tid = h.timer ? h.timer->begin(4) : -1;
             k_mixed_reduce<<<static_cast<unsigned>(rgrid), kRedBlock, 0, h.stream>>>(r);
             CUDA_LAUNCH_CHECK();
+            if (h.timer) h.timer->end(tid);
         }
     }
 }

@@ -108,41 +108,6 @@ __global__ void k_transpose_add_eps(const double* __restrict__ src, size_t lds, 
 // Host orchestration.
 // ---------------------------------------------------------------------------
 
-struct PhaseTimer {
-    Handle& h;
-    bool on;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
-    std::vector<int> cat;
-    PhaseTimer(Handle& hh, bool enabled) : h(hh), on(enabled) {}
-    ~PhaseTimer() {
-        for (auto& p : ev) {
-            cudaEventDestroy(p.first);
-            cudaEventDestroy(p.second);
-        }
-    }
-    int begin(int category) {
-        if (!on) return -1;
-        cudaEvent_t a, b;
-        CUDA_CHECK(cudaEventCreate(&a));
-        CUDA_CHECK(cudaEventCreate(&b));
-        CUDA_CHECK(cudaEventRecord(a, h.stream));
-        ev.emplace_back(a, b);
-        cat.push_back(category);
-        return static_cast<int>(ev.size()) - 1;
-    }
-    void end(int id) {
-        if (id >= 0) CUDA_CHECK(cudaEventRecord(ev[id].second, h.stream));
-    }
-    // categories: 0 alpha, 1 beta, 2 mixed, 3 combine
-    void collect(double out[4]) {
-        for (int i = 0; i < 4; ++i) out[i] = 0.0;
-        for (size_t i = 0; i < ev.size(); ++i) {
-            float ms = 0.f;
-            CUDA_CHECK(cudaEventElapsedTime(&ms, ev[i].first, ev[i].second));
-            out[cat[i]] += ms * 1e-3;
-        }
-    }
-};
 
 // Scratch for M vectors: Cs^T / sigma^T blocks, the eps-signed Cs (the
 // whole vector for virtual blocks, whose ring reads other blocks before
@@ -716,6 +681,11 @@ void sigma_block(Handle& h, const double* const* dx, double* const* dy, int m) {
 void sigma_device(Handle& h, const double* dx, double* dy, detci_gpu_timings* out) {
     if (!h.built) fail(DETCI_GPU_E_INPUT, "sigma: basis not built");
     PhaseTimer tm(h, out != nullptr);
+    h.timer = out ? &tm : nullptr;
+    struct Reset {
+        Handle& h;
+        ~Reset() { h.timer = nullptr; }
+    } reset{h};
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     if (out) {
         CUDA_CHECK(cudaEventCreate(&t0));
@@ -726,8 +696,9 @@ void sigma_device(Handle& h, const double* dx, double* dy, detci_gpu_timings* ou
     if (out) {
         CUDA_CHECK(cudaEventRecord(t1, h.stream));
         CUDA_CHECK(cudaEventSynchronize(t1));
-        double parts[4];
+        double parts[5];
         tm.collect(parts);
+        out->mixed_reduce_seconds = parts[4];
         float ms = 0.f;
         CUDA_CHECK(cudaEventElapsedTime(&ms, t0, t1));
         out->alpha_seconds = parts[0];

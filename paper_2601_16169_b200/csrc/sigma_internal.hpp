@@ -4,6 +4,7 @@
 #pragma once
 
 #include <array>
+#include <vector>
 #include <cstdint>
 #include <utility>
 
@@ -14,6 +15,44 @@ namespace detci_gpu {
 
 constexpr int kMaxM = 4;   // vectors per blocked pass
 constexpr int kMxBlock = 1024;   // mixed-term CTA: one per SM, 32 warps
+
+// CUDA-event phase timer on the compute stream (detci_gpu_timings split).
+struct PhaseTimer {
+    Handle& h;
+    bool on;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    std::vector<int> cat;
+    PhaseTimer(Handle& hh, bool enabled) : h(hh), on(enabled) {}
+    ~PhaseTimer() {
+        for (auto& p : ev) {
+            cudaEventDestroy(p.first);
+            cudaEventDestroy(p.second);
+        }
+    }
+    int begin(int category) {
+        if (!on) return -1;
+        cudaEvent_t a, b;
+        CUDA_CHECK(cudaEventCreate(&a));
+        CUDA_CHECK(cudaEventCreate(&b));
+        CUDA_CHECK(cudaEventRecord(a, h.stream));
+        ev.emplace_back(a, b);
+        cat.push_back(category);
+        return static_cast<int>(ev.size()) - 1;
+    }
+    void end(int id) {
+        if (id >= 0) CUDA_CHECK(cudaEventRecord(ev[id].second, h.stream));
+    }
+    // categories: 0 alpha, 1 beta, 2 mixed, 3 combine, 4 the D reductions
+    // (inside the mixed phase)
+    void collect(double out[5]) {
+        for (int i = 0; i < 5; ++i) out[i] = 0.0;
+        for (size_t i = 0; i < ev.size(); ++i) {
+            float ms = 0.f;
+            CUDA_CHECK(cudaEventElapsedTime(&ms, ev[i].first, ev[i].second));
+            out[cat[i]] += ms * 1e-3;
+        }
+    }
+};
 
 using Ptrs = std::array<const double*, kMaxM>;
 using MPtrs = std::array<double*, kMaxM>;

@@ -196,6 +196,13 @@ class GpuBasis:
         self._check(self._lib.detci_gpu_nnz(self._h, C.byref(t), C.byref(a), C.byref(b), C.byref(m)))
         return {"total": t.value, "alpha": a.value, "beta": b.value, "mixed": m.value}
 
+    def sigma_plan(self) -> dict:
+        """Shape of the mixed-term plan (K, segments, ja windows, SELL
+        entries, D bytes); windows are 0 before the first sigma."""
+        p = _lib.Plan()
+        self._check(self._lib.detci_gpu_sigma_plan(self._h, C.byref(p)))
+        return {k: getattr(p, k) for k, _ in p._fields_}
+
     def linear_operator(self) -> Callable[[np.ndarray, np.ndarray], None]:
         """LinearOperator (davidson.hpp:28): y = H x on host arrays."""
         return lambda x, y: matvec(self, x, y)

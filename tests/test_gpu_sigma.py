@@ -134,6 +134,29 @@ def test_config_sigma_rows_vs_reference(cfg):
         assert abs(x @ hz - y @ z) <= 1e-10 * max(1.0, abs(x @ hz))
 
 
+@pytest.mark.parametrize("cfg", ["C3", "C4"])
+def test_interior_sigma_rows_vs_reference(cfg):
+    """Interior reference rows (tests/golden/make_golden.py --only interior):
+    seeded random alpha rows plus the rows of largest / smallest singles and
+    doubles degree and the middle rows.  At C3 every row's singles list
+    straddles the one-GPU plan's ja windows of D; at C4 every row goes
+    through the segmented Cs staging.  Also the plan shape is recorded so a
+    change of plan is visible in the failure message."""
+    path = GOLDEN / f"rows_{cfg}_interior.npz"
+    if not path.exists():
+        pytest.skip(f"{path.name} not generated")
+    rows = np.load(path)
+    ints, a, bb = synth.synthetic_system(cfg)
+    with gpu_basis(ints, a, bb) as b:
+        x = synth.random_vector(b.dimension(), 11)
+        y = detci.matvec(b, x)
+        plan = b.sigma_plan()
+        r = rows["rows"].astype(np.int64)
+        err = rel_diff(y.reshape(len(a), -1)[r], rows["sigma_rows"])
+        assert err <= 1e-12, (err, plan)
+        assert rel_diff(b.diag().reshape(len(a), -1)[r], rows["diag_rows"]) <= 1e-12
+
+
 def test_c4_sigma_rows_vs_reference():
     """C4 (1e9 determinants, the 8-GPU target problem, on one GPU): the first
     and last reference sigma rows (tests/golden/make_golden.py --only c4) and
