@@ -247,6 +247,12 @@ typedef struct {
 } detci_gpu_plan;
 int detci_gpu_sigma_plan(const detci_gpu_handle* h, detci_gpu_plan* out);
 
+/* Virtual blocks (desc.virtual_blocks > 1): device seconds of each
+ * block-rank's share of the last timed sigma (detci_gpu_sigma_device with
+ * timings), i.e. what one rank of a P-GPU run computes, transfers excluded.
+ * *count = P (0 when none); up to cap values are written. */
+int detci_gpu_rank_seconds(const detci_gpu_handle* h, double* out, int cap, int* count);
+
 /* ---- Davidson -------------------------------------------------------------- */
 int detci_gpu_davidson(detci_gpu_handle* h, const detci_dav_opts* opts, detci_dav_result* res,
                        detci_trace_cb cb, void* user);

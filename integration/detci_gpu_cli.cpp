@@ -7,7 +7,8 @@
 // nlohmann/json) and libdetci_gpu.so.
 //
 //   detci_gpu run --integrals F --dets D [--method gpu|stored|matrix_free]
-//       [--devices N] [--virtual-blocks V] [--bit-length B] [--shuffle]
+//       [--devices N] [--transport nccl|loopback] [--virtual-blocks V]
+//       [--bit-length B] [--shuffle]
 //       [--seed S] [--tol T] [--max-iter N] [--max-subspace K]
 //       [--memory-budget BYTES] [--workers W] [--format text|json]
 //       [--no-timings] [--out PATH]
@@ -17,8 +18,11 @@
 // and the device Davidson.  stored: the device CSR (build_stored_matrix
 // layout) behind the same device Davidson.  --devices N > 1 runs one host
 // thread per GPU, each with its own handle and an NCCL communicator over the
-// N devices (alpha blocks + C ring); rank 0 reports.  Exit codes follow the
-// reference CLI: 0 converged or reported, 1 error (message on stderr).
+// N devices (alpha blocks + C ring); rank 0 reports.  --transport loopback
+// runs the N ranks as threads on ONE GPU over the in-process transport (the
+// same rank code, for single-GPU machines).  Exit codes follow the reference
+// CLI (tools/detci.cpp:32-34, 59-63): 0 converged, 1 error (message on
+// stderr), 2 reported but not converged.
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -50,7 +54,10 @@ struct GpuConfig {
     std::string method = "gpu";   // gpu | stored | matrix_free
     int devices = 1;
     int virtual_blocks = 1;
+    std::string transport = "nccl";   // nccl | loopback
 };
+
+constexpr int kExitOk = 0, kExitError = 1, kExitNotConverged = 2;   // tools/detci.cpp:32-34
 
 struct GpuRun {
     DavidsonResult solved;
@@ -67,7 +74,9 @@ GpuRun run_rank(const RunConfig& cfg, const GpuConfig& g, int norbs, const std::
                 const std::uint8_t* nccl_id) {
     GpuRun out;
     gpu::DeviceOptions o;
-    o.device = rank;
+    const bool loop = g.transport == "loopback";
+    o.device = loop ? 0 : rank;
+    o.loopback_group = loop && g.devices > 1 ? 1 : 0;
     o.rank = rank;
     o.world_size = g.devices;
     o.nccl_id = nccl_id;
@@ -94,7 +103,8 @@ GpuRun run_rank(const RunConfig& cfg, const GpuConfig& g, int norbs, const std::
 
 std::string usage() {
     return "usage: detci_gpu run --integrals F --dets D [--method gpu|stored|matrix_free] [--devices N]\n"
-           "       [--virtual-blocks V] [--bit-length B] [--shuffle] [--seed S] [--tol T] [--max-iter N]\n"
+           "       [--transport nccl|loopback] [--virtual-blocks V] [--bit-length B] [--shuffle] [--seed S]\n"
+           "       [--tol T] [--max-iter N]\n"
            "       [--max-subspace K] [--memory-budget BYTES] [--workers W] [--format text|json]\n"
            "       [--no-timings] [--out PATH]\n";
 }
@@ -121,6 +131,7 @@ int main(int argc, char** argv) {
             else if (k == "--method") g.method = val();
             else if (k == "--devices") g.devices = std::stoi(val());
             else if (k == "--virtual-blocks") g.virtual_blocks = std::stoi(val());
+            else if (k == "--transport") g.transport = val();
             else if (k == "--bit-length") cfg.bit_length = std::stoi(val());
             else if (k == "--shuffle") cfg.shuffle = true;
             else if (k == "--seed") cfg.seed = std::stoull(val());
@@ -137,15 +148,20 @@ int main(int argc, char** argv) {
         if (g.method != "gpu" && g.method != "stored" && g.method != "matrix_free")
             throw ConfigError("--method must be gpu, stored or matrix_free");
         if (format != "text" && format != "json") throw ConfigError("--format must be text or json");
+        if (g.transport != "nccl" && g.transport != "loopback")
+            throw ConfigError("--transport must be nccl or loopback");
         if (g.devices < 1 || g.virtual_blocks < 1) throw ConfigError("--devices and --virtual-blocks must be >= 1");
         if (g.method == "stored" && (g.devices > 1 || g.virtual_blocks > 1))
             throw UnsupportedError("--method stored runs on one GPU");
         const ReportFormat fmt = format == "json" ? ReportFormat::Json : ReportFormat::Text;
 
         std::string text;
+        bool converged = false;
         if (g.method == "matrix_free") {
             cfg.method = Method::MatrixFree;
-            text = emit_report(run_diagonalization(cfg), fmt);
+            const RunReport rep = run_diagonalization(cfg);
+            converged = rep.converged;
+            text = emit_report(rep, fmt);
         } else {
             cfg.method = g.method == "stored" ? Method::Stored : Method::MatrixFree;
             const auto wall0 = std::chrono::steady_clock::now();
@@ -178,8 +194,8 @@ int main(int argc, char** argv) {
             if (g.devices == 1) {
                 runs[0] = run_rank(cfg, g, n, a, b, table, 0, nullptr);
             } else {
-                std::uint8_t id[128];
-                gpu::rethrow(detci_gpu_nccl_unique_id(id), nullptr);
+                std::uint8_t id[128] = {};
+                if (g.transport == "nccl") gpu::rethrow(detci_gpu_nccl_unique_id(id), nullptr);
                 std::vector<std::exception_ptr> errs(g.devices);
                 std::vector<std::thread> th;
                 for (int r = 0; r < g.devices; ++r)
@@ -204,6 +220,7 @@ int main(int argc, char** argv) {
             report.ground_energy = r0.solved.energy;
             report.iterations = static_cast<int>(r0.solved.trace.iterations.size());
             report.converged = r0.solved.converged;
+            converged = report.converged;
             report.status = r0.solved.status;
             report.trace = r0.solved.trace;
             double matvec = 0.0;
@@ -251,12 +268,12 @@ int main(int argc, char** argv) {
             if (!f) throw InputError("cannot write '" + out_path + "'");
             f << text;
         }
-        return 0;
+        return converged ? kExitOk : kExitNotConverged;   // tools/detci.cpp:59-63
     } catch (const Error& e) {
         std::fprintf(stderr, "error: %s\n", e.what());
-        return 1;
+        return kExitError;
     } catch (const std::exception& e) {
         std::fprintf(stderr, "error: %s\n", e.what());
-        return 1;
+        return kExitError;
     }
 }

@@ -66,6 +66,9 @@ struct DeviceOptions {
     bool weighted_partition = true;
     const std::uint8_t* nccl_id = nullptr;
     std::uint64_t memory_budget_bytes = 0;
+    // > 0: the world_size ranks are host threads of this process over the
+    // loopback transport (group id), not NCCL (detci_gpu_create_loopback)
+    std::uint64_t loopback_group = 0;
 };
 
 class DeviceBasis {
@@ -95,7 +98,8 @@ private:
               const IntegralTable& table, const DeviceOptions& o) {
         detci_gpu_desc d{o.device, o.rank, o.world_size, o.nccl_id, o.virtual_blocks,
                          o.weighted_partition ? 1 : 0, o.memory_budget_bytes};
-        rethrow(detci_gpu_create(&d, &h_), nullptr);
+        if (o.loopback_group) rethrow(detci_gpu_create_loopback(&d, o.loopback_group, &h_), nullptr);
+        else rethrow(detci_gpu_create(&d, &h_), nullptr);
         try {
             rethrow(detci_gpu_set_strings(h_, n, a.data(), a.size(), b.data(), b.size()), h_);
             const std::size_t nn = static_cast<std::size_t>(n);

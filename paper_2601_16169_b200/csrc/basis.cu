@@ -10,6 +10,7 @@
 
 #include "formulas.cuh"
 #include "handle.hpp"
+#include "sigma_internal.hpp"
 
 namespace detci_gpu {
 
@@ -33,7 +34,8 @@ void plan_partition(uint64_t na, uint64_t nb, const uint32_t* sa, const uint32_t
     std::vector<double> prefix(na + 1, 0.0);
     for (uint64_t i = 0; i < na; ++i)
         prefix[i + 1] = prefix[i] + static_cast<double>(sa[i] + da[i]) * nb +
-                        static_cast<double>(sum_sb + sum_db) + static_cast<double>(sa[i]) * sum_sb;
+                        static_cast<double>(sum_sb + sum_db) +
+                        (weighted == 2 ? 0.0 : static_cast<double>(sa[i]) * sum_sb);
     blk[0] = 0;
     blk[P] = na;
     for (int g = 1; g < P; ++g) {
@@ -558,6 +560,19 @@ void build_mixed_sell(Handle& h, SellTable& st, int M, int format) {
     upload(st.off, soff, h.stream);
     upload(st.sell, sell, h.stream);
     CUDA_CHECK(cudaStreamSynchronize(h.stream));
+    if (format == 2 && M == 1) {
+        // scatter work per slice (padded entries over the segments) plus the
+        // per-slot D store + reduction, which costs as much as ~9 entries
+        // (16 B of HBM per (row, single) pair against ~1.1 x 8 B of shared
+        // memory per entry and pair, at ~6 vs ~30 TB/s): the multi-rank
+        // column shares are cut on its prefix (mixed_slots)
+        h.slice_prefix.assign(static_cast<size_t>(nslices) + 1, 0);
+        for (uint32_t sl = 0; sl < nslices; ++sl) {
+            uint64_t w = 9;
+            for (uint32_t g = 0; g < nseg; ++g) w += slen[static_cast<size_t>(sl) * nseg + g];
+            h.slice_prefix[sl + 1] = h.slice_prefix[sl] + w;
+        }
+    }
     st.built = true;
 }
 
@@ -565,8 +580,12 @@ void build_partition(Handle& h) {
     const int P = std::max(h.world, h.vblocks);
     const uint64_t na = h.na(), nb = h.nb();
     h.blk.assign(P + 1, 0);
+    // Under the gather schedule the mixed term is split by beta-slot columns
+    // (mixed_slots), not by rows: the row partition then balances the
+    // same-spin work only (weighted = 2).
+    const bool gather = P > 1 && mixed_scatter_enabled() && !multi_ring();
     plan_partition(na, nb, h.ch[0].h_len[0].data(), h.ch[0].h_len[1].data(), h.ch[1].h_len[0].data(),
-                   h.ch[1].h_len[1].data(), P, h.weighted, h.blk.data());
+                   h.ch[1].h_len[1].data(), P, h.weighted && gather ? 2 : h.weighted, h.blk.data());
     // Block edges on multiples of 128 rows when blocks are large: a block's
     // rows are the beta term's columns, and a partial 128-column chunk runs
     // the clamped tail kernel (C3 at 8 blocks: 29 ms of tails vs 7 ms at one

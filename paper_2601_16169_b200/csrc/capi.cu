@@ -183,6 +183,8 @@ void detci_gpu_destroy(detci_gpu_handle* hh) {
     h.red.reset();
     h.red_count.reset();
     h.comm.reset();
+    if (h.pin_x) cudaFreeHost(h.pin_x);
+    if (h.pin_y) cudaFreeHost(h.pin_y);
     for (auto& e : h.ev)
         if (e) cudaEventDestroy(e);
     if (h.stream) cudaStreamDestroy(h.stream);
@@ -433,6 +435,15 @@ int detci_gpu_sigma_plan(const detci_gpu_handle* hh, detci_gpu_plan* out) {
             out->mixed_lds_bytes = 8 * t.sell.n * loads_per_entry;
             out->d_read_bytes = h.scatter_plan.empty() ? 0 : 8 * pairs * h.nb();
         }
+    });
+}
+
+int detci_gpu_rank_seconds(const detci_gpu_handle* hh, double* out, int cap, int* count) {
+    return guarded(const_cast<detci_gpu_handle*>(hh), [&] {
+        require(hh && count, DETCI_GPU_E_INPUT, "rank_seconds: null argument");
+        const auto& r = hh->h.rank_seconds;
+        *count = static_cast<int>(r.size());
+        for (int i = 0; i < cap && i < static_cast<int>(r.size()); ++i) out[i] = r[i];
     });
 }
 

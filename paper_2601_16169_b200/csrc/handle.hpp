@@ -144,6 +144,7 @@ struct Handle {
     SellTable sell_m[3];
     SellTable sell_scatter[2];         // format 2, M = 1, 2
     DevBuf<uint32_t> sell_perm;        // slot -> beta string (degree-sorted)
+    std::vector<uint64_t> slice_prefix;   // prefix of the scatter work per 32-slot slice (mixed_slots)
     // scatter mixed term: tpos[sa_off[ja] + k] = position of ja in the
     // singles list of its k-th single ia; host copies of the alpha singles;
     // windows per block-rank g (built on first use, dropped with dbuf)
@@ -170,6 +171,11 @@ struct Handle {
     DevBuf<double> mix_t, mix_r;       // gather schedule: own / received mixed slabs
     DevBuf<double> ring[2];            // max_blk * nb
     DevBuf<double> xbuf, ybuf;         // host-pointer staging, local length
+    // page-locked mirrors of x and y for callers that hand pageable memory
+    // (detci_gpu_sigma bounces through them so the copies stay overlapped)
+    double* pin_x = nullptr;
+    double* pin_y = nullptr;
+    size_t pin_n = 0;
     DevBuf<double> red;                // reduction partials
     DevBuf<double> dav_store;          // Davidson subspace, cached across solves
     DevBuf<unsigned int> red_count;
@@ -183,6 +189,7 @@ struct Handle {
     bool use_stored = false;
 
     PhaseTimer* timer = nullptr;       // set while a timed sigma runs
+    std::vector<double> rank_seconds;  // virtual blocks: device seconds per block-rank, last timed sigma
     cudaStream_t stream = nullptr, comm_stream = nullptr;
     cudaEvent_t ev[16] = {};
     std::unique_ptr<Comm> comm;        // world > 1: NCCL or loopback (comm.hpp)

@@ -897,10 +897,24 @@ bool multi_ring() {
     return e && std::string(e) == "ring";
 }
 
-// Beta slots of the mixed term owned by block-rank g (32-slot aligned).
+// Beta slots of the mixed term owned by block-rank g (32-slot aligned),
+// cut on the prefix of the scatter work per slice: the slots are sorted by
+// descending singles degree, so equal slot counts would give rank 0 the
+// heaviest strings (1.5x the mean at C3 / P = 8).
 std::pair<uint32_t, uint32_t> mixed_slots(const Handle& h, int g, int P) {
     const uint64_t total = static_cast<uint64_t>(h.nslices) * kWarp;
-    auto at = [&](int k) { return static_cast<uint32_t>(k == P ? total : total * k / P / kWarp * kWarp); };
+    const auto& pre = h.slice_prefix;
+    const bool weighted = pre.size() == static_cast<size_t>(h.nslices) + 1 && pre.back() > 0;
+    auto at = [&](int k) -> uint32_t {
+        if (k <= 0) return 0;
+        if (k >= P) return static_cast<uint32_t>(total);
+        if (!weighted) return static_cast<uint32_t>(total * k / P / kWarp * kWarp);
+        const double target = static_cast<double>(pre.back()) * k / P;
+        const size_t s = std::lower_bound(pre.begin(), pre.end(), target,
+                                          [](uint64_t v, double t) { return static_cast<double>(v) < t; }) -
+                         pre.begin();
+        return static_cast<uint32_t>(std::min<uint64_t>(s * kWarp, total));
+    };
     return {at(g), at(g + 1)};
 }
 

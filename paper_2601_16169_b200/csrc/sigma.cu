@@ -33,6 +33,7 @@
 #include <array>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <memory>
 #include <string>
 #include <vector>
@@ -352,6 +353,7 @@ void sigma_gather_virtual(Handle& h, const Ptrs& dx, const MPtrs& dy, PhaseTimer
     }
     eps_prologue<M>(h, dx, cfw, false, 0, na);
     for (int g = 0; g < P; ++g) {
+        tm.rank_tag = g;
         const uint64_t a0 = h.blk[g], a1 = h.blk[g + 1];
         Ptrs xg{};
         MPtrs yg{}, cg{};
@@ -369,9 +371,10 @@ void sigma_gather_virtual(Handle& h, const Ptrs& dx, const MPtrs& dy, PhaseTimer
         tm.end(id);
         combine<M>(h, yg, a0, a1, tm);
     }
-    const int id = tm.begin(2);
     size_t toff = 0;
     for (int g = 0; g < P; ++g) {
+        tm.rank_tag = g;
+        const int id = tm.begin(2);
         const auto [s0, s1] = mixed_slots(h, g, P);
         const size_t ns = s1 - s0;
         double* T[kMaxM] = {};
@@ -379,8 +382,9 @@ void sigma_gather_virtual(Handle& h, const Ptrs& dx, const MPtrs& dy, PhaseTimer
         mixed_columns<M>(h, g, P, cf, T, ns);
         for (int v = 0; v < M; ++v) unpack_slab<M>(h, T[v], ns, static_cast<uint32_t>(ns), na, s0, dy[v]);
         toff += na * ns;
+        tm.end(id);
     }
-    tm.end(id);
+    tm.rank_tag = -1;
 }
 
 template <int M>
@@ -430,6 +434,7 @@ void sigma_schedule_m(Handle& h, const Ptrs& dx, const MPtrs& dy, PhaseTimer& tm
                 yg[v] = dy[v] + h.blk[g] * nb;
                 xsg[v] = xs_all[v] + h.blk[g] * nb;
             }
+            tm.rank_tag = g;
             sigma_ring<M>(h, g, P, xg, xsg, yg, tm, [&](int, const Ptrs&, double* dst, int next) {
                 const size_t n = (h.blk[next + 1] - h.blk[next]) * nb;
                 for (int v = 0; v < M; ++v)
@@ -456,6 +461,28 @@ void sigma_schedule(Handle& h, const double* dx, double* dy, PhaseTimer& tm) {
     x[0] = dx;
     y[0] = dy;
     sigma_schedule_m<1>(h, x, y, tm);
+}
+
+// Pageable host memory (not registered with CUDA): its async copies are
+// staged synchronously by the driver and serialise the pipeline.
+bool pageable(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return at.type == cudaMemoryTypeUnregistered;
+}
+
+// memcpy on the host's cores (the bounce copies through the pinned mirrors)
+void host_copy(double* dst, const double* src, size_t n) {
+    constexpr size_t kBlock = size_t{1} << 20;   // doubles per task (8 MB)
+    const int64_t nb = static_cast<int64_t>((n + kBlock - 1) / kBlock);
+#pragma omp parallel for schedule(static)
+    for (int64_t b = 0; b < nb; ++b) {
+        const size_t o = static_cast<size_t>(b) * kBlock;
+        std::memcpy(dst + o, src + o, std::min(kBlock, n - o) * sizeof(double));
+    }
 }
 
 // Row chunks of the pipelined host sigma.  Front (H2D under the beta term):
@@ -503,6 +530,20 @@ bool sigma_host_pipelined(Handle& h, const double* x, double* y, detci_gpu_timin
     double* dx = h.xbuf.p;
     double* dy = h.ybuf.p;
     const uint64_t a0 = h.a0;
+    // pageable caller buffers: bounce through page-locked mirrors (chunk by
+    // chunk on the host's cores, so the DMA and the kernels stay overlapped)
+    const bool bounce_x = pageable(x), bounce_y = pageable(y);
+    if ((bounce_x || bounce_y) && h.pin_n < n) {
+        if (h.pin_x) cudaFreeHost(h.pin_x);
+        if (h.pin_y) cudaFreeHost(h.pin_y);
+        h.pin_x = h.pin_y = nullptr;
+        h.pin_n = 0;
+        CUDA_CHECK(cudaMallocHost(&h.pin_x, n * sizeof(double)));
+        CUDA_CHECK(cudaMallocHost(&h.pin_y, n * sizeof(double)));
+        h.pin_n = n;
+    }
+    const double* xs_src = bounce_x ? h.pin_x : x;   // the H2D source
+    double* yd_dst = bounce_y ? h.pin_y : y;         // the D2H destination
     const std::vector<uint64_t> fe = pipe_edges(nloc, kFrontWeight), te = pipe_edges(nloc, kTailWeight);
     cudaEvent_t ev[kFrontChunks + kTailChunks + 2];
     const bool dbg = std::getenv("DETCI_PIPE_DEBUG") != nullptr;
@@ -512,16 +553,23 @@ bool sigma_host_pipelined(Handle& h, const double* x, double* y, detci_gpu_timin
     cudaEvent_t t0 = ev[kFrontChunks + kTailChunks], t1 = ev[kFrontChunks + kTailChunks + 1];
     CUDA_CHECK(cudaEventRecord(t0, h.stream));
     CUDA_CHECK(cudaStreamWaitEvent(h.comm_stream, t0, 0));   // previous work on the buffers is done
-    for (int c = 0; c < kFrontChunks; ++c) {
+    auto front_copy = [&](int c) {
         const uint64_t r0 = fe[c], r1 = fe[c + 1];
-        if (r1 > r0)
-            CUDA_CHECK(cudaMemcpyAsync(dx + r0 * nb, x + r0 * nb, (r1 - r0) * nb * 8, cudaMemcpyHostToDevice,
+        if (r1 > r0) {
+            if (bounce_x) host_copy(h.pin_x + r0 * nb, x + r0 * nb, (r1 - r0) * nb);
+            CUDA_CHECK(cudaMemcpyAsync(dx + r0 * nb, xs_src + r0 * nb, (r1 - r0) * nb * 8, cudaMemcpyHostToDevice,
                                        h.comm_stream));
+        }
         CUDA_CHECK(cudaEventRecord(landed[c], h.comm_stream));
-    }
+    };
+    // with page-locked x every chunk's copy is enqueued up front; with a
+    // bounce, chunk c is copied on the host while the GPU runs chunk c - 1
+    if (!bounce_x)
+        for (int c = 0; c < kFrontChunks; ++c) front_copy(c);
     // prologue + beta term per landed chunk
     for (int c = 0; c < kFrontChunks; ++c) {
         const uint64_t r0 = fe[c], r1 = fe[c + 1];
+        if (bounce_x) front_copy(c);
         CUDA_CHECK(cudaStreamWaitEvent(h.stream, landed[c], 0));
         if (r1 == r0) continue;
         const uint32_t rc = static_cast<uint32_t>(r1 - r0);
@@ -563,6 +611,13 @@ bool sigma_host_pipelined(Handle& h, const double* x, double* y, detci_gpu_timin
     yl[0] = dy;
     const int nw = static_cast<int>(wins.size());
     int last_chunk = -1;
+    // D2H of each tail chunk into the pinned mirror, then (bounce) the host
+    // copies it out once that chunk's event fires
+    struct TailCopy {
+        uint64_t r0, r1;
+        cudaEvent_t done;
+    };
+    std::vector<TailCopy> tails;
     auto tail_chunk = [&](uint64_t r0, uint64_t r1, bool alpha_combine, int wi) {
         if (r1 == r0) return;
         if (alpha_combine) {
@@ -583,8 +638,14 @@ bool sigma_host_pipelined(Handle& h, const double* x, double* y, detci_gpu_timin
         cudaEvent_t done = final_rows[last_chunk];
         CUDA_CHECK(cudaEventRecord(done, h.stream));
         CUDA_CHECK(cudaStreamWaitEvent(h.comm_stream, done, 0));
-        CUDA_CHECK(cudaMemcpyAsync(y + r0 * nb, dy + r0 * nb, (r1 - r0) * nb * 8, cudaMemcpyDeviceToHost,
+        CUDA_CHECK(cudaMemcpyAsync(yd_dst + r0 * nb, dy + r0 * nb, (r1 - r0) * nb * 8, cudaMemcpyDeviceToHost,
                                    h.comm_stream));
+        if (bounce_y) {
+            cudaEvent_t e;
+            CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            CUDA_CHECK(cudaEventRecord(e, h.comm_stream));
+            tails.push_back({r0, r1, e});
+        }
     };
     const std::vector<uint64_t> edges = pipe_edges(nloc, kTailWeight);
     if (nw == 1) {
@@ -604,6 +665,11 @@ bool sigma_host_pipelined(Handle& h, const double* x, double* y, detci_gpu_timin
         launch_mixed_scatter<1>(h, 0, 1, 0, held, 0, static_cast<uint32_t>(h.na()), yl, a0, 1, 0, ~0ull, nw - 1);
         if (dbg) CUDA_CHECK(cudaEventRecord(e_scatter, h.stream));
         for (size_t c = 0; c + 1 < edges.size(); ++c) tail_chunk(edges[c], edges[c + 1], true, nw - 1);
+    }
+    for (auto& tc : tails) {
+        CUDA_CHECK(cudaEventSynchronize(tc.done));
+        host_copy(y + tc.r0 * nb, h.pin_y + tc.r0 * nb, (tc.r1 - tc.r0) * nb);
+        cudaEventDestroy(tc.done);
     }
     CUDA_CHECK(cudaEventRecord(t1, h.comm_stream));
     CUDA_CHECK(cudaEventSynchronize(t1));
@@ -699,6 +765,7 @@ void sigma_device(Handle& h, const double* dx, double* dy, detci_gpu_timings* ou
         double parts[5];
         tm.collect(parts);
         out->mixed_reduce_seconds = parts[4];
+        h.rank_seconds = tm.per_rank(std::max(h.world, h.vblocks) > 1 && h.world == 1 ? h.vblocks : 0);
         float ms = 0.f;
         CUDA_CHECK(cudaEventElapsedTime(&ms, t0, t1));
         out->alpha_seconds = parts[0];

@@ -21,7 +21,8 @@ struct PhaseTimer {
     Handle& h;
     bool on;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
-    std::vector<int> cat;
+    std::vector<int> cat, rk;
+    int rank_tag = -1;   // virtual block-rank the following phases belong to (-1: none)
     PhaseTimer(Handle& hh, bool enabled) : h(hh), on(enabled) {}
     ~PhaseTimer() {
         for (auto& p : ev) {
@@ -37,6 +38,7 @@ struct PhaseTimer {
         CUDA_CHECK(cudaEventRecord(a, h.stream));
         ev.emplace_back(a, b);
         cat.push_back(category);
+        rk.push_back(rank_tag);
         return static_cast<int>(ev.size()) - 1;
     }
     void end(int id) {
@@ -51,6 +53,18 @@ struct PhaseTimer {
             CUDA_CHECK(cudaEventElapsedTime(&ms, ev[i].first, ev[i].second));
             out[cat[i]] += ms * 1e-3;
         }
+    }
+    // device seconds per tagged block-rank (phases 0-3; the reductions are
+    // inside the mixed phase)
+    std::vector<double> per_rank(int P) {
+        std::vector<double> t(std::max(P, 0), 0.0);
+        for (size_t i = 0; i < ev.size(); ++i) {
+            if (rk[i] < 0 || rk[i] >= P || cat[i] == 4) continue;
+            float ms = 0.f;
+            CUDA_CHECK(cudaEventElapsedTime(&ms, ev[i].first, ev[i].second));
+            t[rk[i]] += ms * 1e-3;
+        }
+        return t;
     }
 };
 

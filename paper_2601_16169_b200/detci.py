@@ -203,6 +203,14 @@ class GpuBasis:
         self._check(self._lib.detci_gpu_sigma_plan(self._h, C.byref(p)))
         return {k: getattr(p, k) for k, _ in p._fields_}
 
+    def rank_seconds(self) -> List[float]:
+        """Virtual blocks: device seconds of each block-rank's share of the
+        last timed sigma (matvec(..., timings={})), transfers excluded."""
+        cnt = C.c_int()
+        buf = (C.c_double * 64)()
+        self._check(self._lib.detci_gpu_rank_seconds(self._h, buf, 64, C.byref(cnt)))
+        return [buf[i] for i in range(min(cnt.value, 64))]
+
     def linear_operator(self) -> Callable[[np.ndarray, np.ndarray], None]:
         """LinearOperator (davidson.hpp:28): y = H x on host arrays."""
         return lambda x, y: matvec(self, x, y)

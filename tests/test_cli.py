@@ -79,3 +79,32 @@ def test_json_report(tmp_path, method, extra):
     if method == "stored":
         assert doc["gpu"]["stored_nnz"] > 0
     assert abs(doc["result"]["iterations"] - rdoc["result"]["iterations"]) <= 1
+
+
+def test_not_converged_exit_code(tmp_path):
+    """tools/detci.cpp:32-34, 59-63: a reported but non-converged run exits 2."""
+    f, d = inputs(tmp_path)
+    out = run("run", "--integrals", f, "--dets", d, "--method", "matrix_free", "--max-iter", "2", "--workers", "2")
+    assert out.returncode == 2, out.stderr
+    assert "GROUND_ENERGY" in out.stdout
+    bad = run("run", "--integrals", f, "--dets", d, "--transport", "carrier-pigeon")
+    assert bad.returncode == 1 and "--transport" in bad.stderr
+
+
+@pytest.mark.gpu
+def test_gpu_not_converged_exit_code(tmp_path):
+    f, d = inputs(tmp_path)
+    out = run("run", "--integrals", f, "--dets", d, "--method", "gpu", "--max-iter", "2")
+    assert out.returncode == 2, out.stderr
+    assert "GROUND_ENERGY" in out.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("devices", [2, 3])
+def test_gpu_loopback_devices(tmp_path, devices):
+    """--devices N --transport loopback: N ranks (threads) on one GPU through
+    the multi-rank code; the reference's golden energy."""
+    f, d = inputs(tmp_path)
+    out = run("run", "--integrals", f, "--dets", d, "--method", "gpu", "--devices", devices, "--transport", "loopback")
+    assert out.returncode == 0, out.stderr
+    assert ground(out.stdout) == "-2.420193979007e+00"
