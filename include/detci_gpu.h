@@ -252,6 +252,19 @@ int detci_gpu_sigma_plan(const detci_gpu_handle* h, detci_gpu_plan* out);
  * timings), i.e. what one rank of a P-GPU run computes, transfers excluded.
  * *count = P (0 when none); up to cap values are written. */
 int detci_gpu_rank_seconds(const detci_gpu_handle* h, double* out, int cap, int* count);
+/* The same split by phase: out[4 * rank + phase], phases alpha, beta, mixed,
+ * combine (count = 4 * P). */
+int detci_gpu_rank_phase_seconds(const detci_gpu_handle* h, double* out, int cap, int* count);
+
+/* Measured rebalance (P = world or virtual blocks > 1; collective when
+ * world > 1): `rounds` timed sigmas, each followed by a re-cut of the alpha
+ * row blocks and of the mixed term's beta-slot column shares from the
+ * per-rank phase times (each rank's measured cost per modelled unit).  The
+ * local row range changes: call before allocating rank-local vectors or
+ * running a solver, and re-query detci_gpu_local_rows.  *max_over_mean
+ * (optional) = the slowest rank over the mean rank of the first timed
+ * sigma, i.e. before rebalancing. */
+int detci_gpu_rebalance(detci_gpu_handle* h, int rounds, double* max_over_mean);
 
 /* ---- Davidson -------------------------------------------------------------- */
 int detci_gpu_davidson(detci_gpu_handle* h, const detci_dav_opts* opts, detci_dav_result* res,

@@ -131,6 +131,8 @@ SIGNATURES = {
     "detci_gpu_launch_count": (C.c_int, [u64p]),
     "detci_gpu_sigma_plan": (C.c_int, [vp, C.POINTER(Plan)]),
     "detci_gpu_rank_seconds": (C.c_int, [vp, dp, C.c_int, C.POINTER(C.c_int)]),
+    "detci_gpu_rank_phase_seconds": (C.c_int, [vp, dp, C.c_int, C.POINTER(C.c_int)]),
+    "detci_gpu_rebalance": (C.c_int, [vp, C.c_int, dp]),
     "detci_gpu_alloc_vector": (C.c_int, [vp, C.POINTER(vp)]),
     "detci_gpu_free_vector": (C.c_int, [vp, vp]),
     "detci_gpu_copy_vector": (C.c_int, [vp, vp, vp, C.c_int]),

@@ -576,6 +576,45 @@ void build_mixed_sell(Handle& h, SellTable& st, int M, int format) {
     st.built = true;
 }
 
+namespace {
+// Block edges on multiples of 128 rows when blocks are large: a block's
+// rows are the beta term's columns, and a partial 128-column chunk runs
+// the clamped tail kernel (C3 at 8 blocks: 29 ms of tails vs 7 ms at one
+// block).  Costs <= 64 rows (3% at C3 / 8) of balance.  Kept only when no
+// block becomes empty.
+void round_block_edges(std::vector<uint64_t>& blk, uint64_t na) {
+    const int P = static_cast<int>(blk.size()) - 1;
+    if (P <= 1 || na < 1024ull * P) return;
+    std::vector<uint64_t> r = blk;
+    bool nonempty = true;
+    for (int g = 1; g < P; ++g) {
+        uint64_t e = (r[g] + 64) / 128 * 128;
+        e = std::max(e, r[g - 1]);
+        r[g] = std::min(e, na);
+        nonempty = nonempty && r[g] > r[g - 1];
+    }
+    nonempty = nonempty && r[P] > r[P - 1];
+    if (nonempty) blk = r;
+}
+
+// P cuts of a prefix array (size n + 1) at equal shares, each part >= 1.
+std::vector<uint64_t> cut_prefix(const std::vector<double>& prefix, int P) {
+    const uint64_t n = prefix.size() - 1;
+    std::vector<uint64_t> c(P + 1, 0);
+    c[P] = n;
+    for (int g = 1; g < P; ++g) {
+        const double target = prefix[n] * g / P;
+        uint64_t cut = std::lower_bound(prefix.begin(), prefix.end(), target) - prefix.begin();
+        cut = std::max<uint64_t>(cut, c[g - 1] + 1);
+        cut = std::min<uint64_t>(cut, n - (P - g));
+        c[g] = cut;
+    }
+    return c;
+}
+} // namespace
+
+void set_local_rows(Handle& h);
+
 void build_partition(Handle& h) {
     const int P = std::max(h.world, h.vblocks);
     const uint64_t na = h.na(), nb = h.nb();
@@ -591,18 +630,7 @@ void build_partition(Handle& h) {
     // the clamped tail kernel (C3 at 8 blocks: 29 ms of tails vs 7 ms at one
     // block).  Costs <= 64 rows (3% at C3 / 8) of balance.
     // Kept only when no block becomes empty.
-    if (P > 1 && na >= 1024ull * P) {
-        std::vector<uint64_t> r = h.blk;
-        bool nonempty = true;
-        for (int g = 1; g < P; ++g) {
-            uint64_t e = (r[g] + 64) / 128 * 128;
-            e = std::max(e, r[g - 1]);
-            r[g] = std::min(e, na);
-            nonempty = nonempty && r[g] > r[g - 1];
-        }
-        nonempty = nonempty && r[P] > r[P - 1];
-        if (nonempty) h.blk = r;
-    }
+    round_block_edges(h.blk, na);
     uint64_t sum_sb = 0, sum_db = 0, sum_sa = 0, sum_da = 0;
     for (uint64_t i = 0; i < nb; ++i) {
         sum_sb += h.ch[1].h_len[0][i];
@@ -615,6 +643,13 @@ void build_partition(Handle& h) {
     h.nnz_alpha = (sum_sa + sum_da) * nb;
     h.nnz_beta = (sum_sb + sum_db) * na;
     h.nnz_mixed = sum_sa * sum_sb;
+    h.slot_cut.clear();
+    set_local_rows(h);
+}
+
+void set_local_rows(Handle& h) {
+    const int P = std::max(h.world, h.vblocks);
+    const uint64_t na = h.na();
     h.max_blk = 0;
     for (int g = 0; g < P; ++g) h.max_blk = std::max(h.max_blk, h.blk[g + 1] - h.blk[g]);
     if (h.world > 1) {
@@ -796,6 +831,76 @@ void build_device_basis(Handle& h) {
     // (the ring buffers of DETCI_MULTI=ring are allocated by its first sigma)
     CUDA_CHECK(cudaStreamSynchronize(h.stream));
     h.built = all_ranks_ok(h, true);
+}
+
+// Measured rebalance (detci_gpu_rebalance): re-cut the alpha-row blocks and
+// the mixed term's beta-slot shares from the per-rank phase times of a timed
+// sigma, t[4 g + phase] (phases alpha, beta, mixed, combine).  The static
+// cuts weight rows by alpha elements + beta work and slices by scatter work
+// (plan_partition, slice_prefix) at one cost per unit; here each block-rank's
+// measured seconds per modelled unit replace that cost over its own range,
+// so the new cuts follow what the model misses (the L2 locality of a row
+// range, the per-CTA staging of a light column share).  matvec.cpp:108-111
+// is the reference's n*g/P; PAPER.md:304 names load imbalance as what limits
+// its scaling.
+void rebalance_partition(Handle& h, const std::vector<double>& t) {
+    const int P = std::max(h.world, h.vblocks);
+    if (P <= 1 || t.size() < 4 * static_cast<size_t>(P)) return;
+    const uint64_t na = h.na();
+    const auto& sa = h.ch[0].h_len[0];
+    const auto& da = h.ch[0].h_len[1];
+    auto floor_rates = [&](std::vector<double>& r) {
+        double m = 0.0;
+        for (double v : r) m += v;
+        m /= P;
+        for (double& v : r) v = std::max(v, 0.1 * m);
+    };
+    // rows: alpha seconds per alpha element, beta + combine seconds per row
+    std::vector<double> ra(P, 0.0), rb(P, 0.0);
+    for (int g = 0; g < P; ++g) {
+        double wa = 0.0;
+        for (uint64_t i = h.blk[g]; i < h.blk[g + 1]; ++i) wa += static_cast<double>(sa[i] + da[i]);
+        const double rows = static_cast<double>(h.blk[g + 1] - h.blk[g]);
+        ra[g] = wa > 0 ? t[4 * g] / wa : 0.0;
+        rb[g] = rows > 0 ? (t[4 * g + 1] + t[4 * g + 3]) / rows : 0.0;
+    }
+    floor_rates(ra);
+    floor_rates(rb);
+    std::vector<double> prefix(na + 1, 0.0);
+    for (int g = 0; g < P; ++g)
+        for (uint64_t i = h.blk[g]; i < h.blk[g + 1]; ++i)
+            prefix[i + 1] = prefix[i] + static_cast<double>(sa[i] + da[i]) * ra[g] + rb[g];
+    std::vector<uint64_t> blk = cut_prefix(prefix, P);
+    round_block_edges(blk, na);
+    // beta-slot shares of the mixed term: seconds per unit of slice work
+    std::vector<uint32_t> cut;
+    const auto& pre = h.slice_prefix;
+    const uint32_t nsl = h.nslices;
+    if (pre.size() == static_cast<size_t>(nsl) + 1 && nsl >= static_cast<uint32_t>(P)) {
+        std::vector<uint32_t> old(P + 1, 0);
+        for (int g = 0; g < P; ++g) old[g] = mixed_slots(h, g, P).first / kWarp;
+        old[P] = nsl;
+        std::vector<double> rm(P, 0.0);
+        for (int g = 0; g < P; ++g) {
+            const double w = static_cast<double>(pre[std::min(old[g + 1], nsl)] - pre[std::min(old[g], nsl)]);
+            rm[g] = w > 0 ? t[4 * g + 2] / w : 0.0;
+        }
+        floor_rates(rm);
+        std::vector<double> sp(nsl + 1, 0.0);
+        int g = 0;
+        for (uint32_t sl = 0; sl < nsl; ++sl) {
+            while (g + 1 < P && sl >= old[g + 1]) ++g;
+            sp[sl + 1] = sp[sl] + static_cast<double>(pre[sl + 1] - pre[sl]) * rm[g];
+        }
+        const std::vector<uint64_t> c = cut_prefix(sp, P);
+        cut.resize(P + 1);
+        for (int k = 0; k <= P; ++k) cut[k] = static_cast<uint32_t>(c[k]) * kWarp;
+    }
+    h.blk = blk;
+    h.slot_cut = cut;
+    set_local_rows(h);
+    release_sigma_scratch(h);
+    if (h.world > 1) build_diag(h);
 }
 
 } // namespace detci_gpu

@@ -347,6 +347,44 @@ int detci_gpu_sigma_device(detci_gpu_handle* hh, const double* dx, double* dy, d
     }, true);
 }
 
+int detci_gpu_rebalance(detci_gpu_handle* hh, int rounds, double* max_over_mean) {
+    return guarded(hh, [&] {
+        require(hh != nullptr && hh->h.built, DETCI_GPU_E_INPUT, "rebalance: basis not built");
+        require(rounds >= 0, DETCI_GPU_E_CONFIG, "rebalance: rounds must be >= 0");
+        Handle& h = hh->h;
+        activate(h);
+        const int P = std::max(h.world, h.vblocks);
+        for (int r = 0; r < rounds && P > 1; ++r) {
+            // a timed sigma of a constant vector (the kernels' cost does not
+            // depend on the values)
+            DevBuf<double> x, y;
+            const size_t n = std::max<size_t>(h.local_len(), 1);
+            x.alloc(n);
+            y.alloc(n);
+            CUDA_CHECK(cudaMemsetAsync(x.p, 0x3f, n * sizeof(double), h.stream));
+            detci_gpu_timings tm{};
+            sigma_device(h, x.p, y.p, &tm);
+            std::vector<double> t(4 * static_cast<size_t>(P), 0.0);
+            if (h.world > 1) {
+                for (int q = 0; q < 4; ++q) t[4 * static_cast<size_t>(h.rank) + q] = h.own_phase_seconds[q];
+                allreduce_sum(h, t.data(), static_cast<int>(t.size()));
+            } else {
+                t = h.rank_phase_seconds;
+            }
+            if (max_over_mean && r == 0) {
+                double mx = 0.0, sum = 0.0;
+                for (int g = 0; g < P; ++g) {
+                    const double v = t[4 * g] + t[4 * g + 1] + t[4 * g + 2] + t[4 * g + 3];
+                    mx = std::max(mx, v);
+                    sum += v;
+                }
+                *max_over_mean = sum > 0 ? mx * P / sum : 1.0;
+            }
+            rebalance_partition(h, t);
+        }
+    }, true);
+}
+
 int detci_gpu_sigma_async(detci_gpu_handle* hh, const double* dx, double* dy) {
     return guarded(hh, [&] {
         require(hh != nullptr && dx && dy, DETCI_GPU_E_INPUT, "sigma: null argument");
@@ -442,6 +480,15 @@ int detci_gpu_rank_seconds(const detci_gpu_handle* hh, double* out, int cap, int
     return guarded(const_cast<detci_gpu_handle*>(hh), [&] {
         require(hh && count, DETCI_GPU_E_INPUT, "rank_seconds: null argument");
         const auto& r = hh->h.rank_seconds;
+        *count = static_cast<int>(r.size());
+        for (int i = 0; i < cap && i < static_cast<int>(r.size()); ++i) out[i] = r[i];
+    });
+}
+
+int detci_gpu_rank_phase_seconds(const detci_gpu_handle* hh, double* out, int cap, int* count) {
+    return guarded(const_cast<detci_gpu_handle*>(hh), [&] {
+        require(hh && count, DETCI_GPU_E_INPUT, "rank_phase_seconds: null argument");
+        const auto& r = hh->h.rank_phase_seconds;
         *count = static_cast<int>(r.size());
         for (int i = 0; i < cap && i < static_cast<int>(r.size()); ++i) out[i] = r[i];
     });

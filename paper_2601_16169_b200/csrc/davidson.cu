@@ -14,11 +14,13 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <vector>
 
 #include "handle.hpp"
+#include "sigma_device.cuh"
 
 namespace detci_gpu {
 
@@ -228,10 +230,190 @@ k_combine(double* dst, const double* src, double scale, VecList v, const double*
     }
 }
 
+// ---------------------------------------------------------------------------
+// Fused single-root iteration passes over the subspace (davidson.cpp:126-176
+// restated as 3 + 1 streaming passes instead of ~6.5k vector passes).
+// Every pass streams ns vectors tile by tile into shared memory with 1-D TMA
+// bulk copies (one elected thread, NS-stage mbarrier ring, one persistent
+// CTA per SM), so the bytes in flight do not depend on the thread count;
+// the element-wise part reads the staged tiles, and the dot products of
+// the pass (one stream against a per-element "probe") are accumulated per
+// warp (warp w owns subspace vectors w, w + 8, ...) and written as per-CTA
+// partials for the fixed-order finalize.
+//   kPassProj  streams x, w_0..w_{k-1}:     <x, w_j>                    (projected row)
+//   kPassRitz  streams v_j, w_j, diag:      corr = (W c - theta V c) / clamp(diag - theta),
+//              |res|^2, |corr|^2, <v_j, corr>, <v_{k-1}, v_j>          (Ritz residual + CGS dots + Gram row)
+//   kPassOrth1 streams corr, v_j:           cand = (corr - sum d_j v_j) / |corr|, <v_j, cand>
+//   kPassOrth2 streams cand, v_j:           cand -= sum e_j v_j, |cand|^2
+// ---------------------------------------------------------------------------
+enum StreamPass { kPassProj = 0, kPassRitz = 1, kPassOrth1 = 2, kPassOrth2 = 3 };
+constexpr int kStMaxS = 2 * kMaxVec + 1;
+constexpr int kStMaxStages = 6;
+constexpr size_t kStSmem = 210 * 1024;   // per SM
+
+struct StreamArgs {
+    const double* s[kStMaxS];
+    double c[kMaxVec];       // kPassRitz: Ritz coefficients
+    int ns, k;
+    uint32_t T;              // tile elements (multiple of 32)
+    int nst;                 // pipeline stages (<= kStMaxStages)
+    uint64_t n;
+    double theta;
+    const double* coef;      // kPassOrth1: d_j (unnormalised <v_j, corr>); kPassOrth2: e_j (device slots)
+    const double* norm2;     // kPassOrth1: |corr|^2 (device slot)
+    double* out;             // corr / cand
+    double* partial;         // [reduction][gridDim.x]
+};
+
+template <int MODE, int kStThreads>
+__global__ void __launch_bounds__(kStThreads, 512 / kStThreads)
+k_dav_stream(const StreamArgs a) {
+    constexpr int kStWarps = kStThreads / 32;
+    constexpr int kStJ = kMaxVec / kStWarps;   // subspace vectors per warp
+    const int kStStages = a.nst;
+    extern __shared__ __align__(16) double st_smem[];
+    __shared__ uint64_t bars[kStMaxStages];
+    __shared__ double sh[32];
+    __shared__ double s_coef[kMaxVec];
+    const uint32_t T = a.T;
+    const int ns = a.ns, k = a.k;
+    double* const probe = st_smem + static_cast<size_t>(kStStages) * ns * T;
+    const uint32_t tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
+    const uint64_t ntiles = (a.n + T - 1) / T;
+    const uint32_t my_tiles = blockIdx.x < ntiles
+                                  ? static_cast<uint32_t>((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x)
+                                  : 0u;
+    auto tile_base = [&](uint32_t it) { return (static_cast<uint64_t>(it) * gridDim.x + blockIdx.x) * T; };
+    auto tile_cnt = [&](uint32_t it) { const uint64_t rem = a.n - tile_base(it); return static_cast<uint32_t>(rem < T ? rem : T); };
+    auto stage = [&](uint32_t st) { return st_smem + static_cast<size_t>(st) * ns * T; };
+    auto issue = [&](uint32_t it) {   // elected thread
+        const uint32_t st = it % kStStages, bytes = (tile_cnt(it) * 8u) & ~15u;
+        mbar_arrive_expect_tx(&bars[st], bytes * static_cast<uint32_t>(ns));
+        if (bytes)
+            for (int s = 0; s < ns; ++s) bulk_g2s(stage(st) + static_cast<size_t>(s) * T, a.s[s] + tile_base(it), bytes, &bars[st]);
+    };
+    if (tid == 0) {
+        for (int s = 0; s < kStStages; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+        for (uint32_t it = 0; it < my_tiles && it < kStStages; ++it) issue(it);
+    }
+    if (MODE == kPassOrth1 || MODE == kPassOrth2)
+        for (int j = tid; j < k; j += kStThreads) s_coef[j] = a.coef[j];
+    __syncthreads();
+
+    // per-element scalars
+    double inv_cnorm = 0.0;
+    if (MODE == kPassOrth1) inv_cnorm = 1.0 / sqrt(*a.norm2);
+    double r1 = 0.0, r2 = 0.0;            // |res|^2, |corr|^2 / |cand|^2
+    double acc[kStJ], acc2[kStJ];         // per-warp dots (vector j = warp + kStWarps * jj)
+#pragma unroll
+    for (int jj = 0; jj < kStJ; ++jj) acc[jj] = acc2[jj] = 0.0;
+
+#pragma unroll 1
+    for (uint32_t it = 0; it < my_tiles; ++it) {
+        const uint32_t st = it % kStStages;
+        const uint32_t cnt = tile_cnt(it);
+        const uint64_t base = tile_base(it);
+        double* const S = stage(st);
+        mbar_wait(&bars[st], (it / kStStages) & 1u);
+        if ((cnt & 1u) && static_cast<int>(tid) < ns) S[static_cast<size_t>(tid) * T + cnt - 1] = a.s[tid][base + cnt - 1];
+        __syncthreads();
+        // element-wise part
+        for (uint32_t i = tid; i < cnt; i += kStThreads) {
+            if constexpr (MODE == kPassRitz) {
+                double r = 0.0, m = 0.0;
+#pragma unroll 4
+                for (int j = 0; j < k; ++j) {
+                    r += a.c[j] * S[static_cast<size_t>(j) * T + i];
+                    m += a.c[j] * S[static_cast<size_t>(k + j) * T + i];
+                }
+                const double res = m - a.theta * r;
+                double denom = S[static_cast<size_t>(2 * k) * T + i] - a.theta;
+                if (fabs(denom) < 1e-8) denom = copysign(1e-8, denom);
+                const double cr = res / denom;
+                probe[i] = cr;
+                a.out[base + i] = cr;
+                r1 += res * res;
+                r2 += cr * cr;
+            } else if constexpr (MODE == kPassOrth1 || MODE == kPassOrth2) {
+                double x = S[i];
+#pragma unroll 4
+                for (int j = 0; j < k; ++j) x -= s_coef[j] * S[static_cast<size_t>(1 + j) * T + i];
+                if (MODE == kPassOrth1) x *= inv_cnorm;
+                probe[i] = x;
+                a.out[base + i] = x;
+                r2 += x * x;
+            }
+        }
+        if constexpr (MODE != kPassOrth2) {
+            if (MODE != kPassProj) __syncthreads();   // probe complete
+            const double* pr = MODE == kPassProj ? S : probe;
+            const int off = MODE == kPassRitz ? 0 : 1;   // first subspace stream
+            const double* last = S + static_cast<size_t>(k - 1) * T;   // v_{k-1} (kPassRitz Gram row)
+#pragma unroll
+            for (int jj = 0; jj < kStJ; ++jj) {
+                const int j = static_cast<int>(warp) + kStWarps * jj;
+                if (j < k) {
+                    const double* sj = S + static_cast<size_t>(off + j) * T;
+                    double x = 0.0, g = 0.0;
+                    for (uint32_t i = lane; i < cnt; i += 32) {
+                        const double v = sj[i];
+                        x = fma(v, pr[i], x);
+                        if (MODE == kPassRitz) g = fma(v, last[i], g);
+                    }
+                    acc[jj] += x;
+                    if (MODE == kPassRitz) acc2[jj] += g;
+                }
+            }
+        }
+        __syncthreads();   // stage and probe consumed
+        if (tid == 0 && it + kStStages < my_tiles) {
+            fence_proxy_async_smem();
+            issue(it + kStStages);
+        }
+    }
+    // partials: [0] |res|^2, [1] |corr|^2 (kPassRitz) or [0] |cand|^2 (kPassOrth2);
+    // dots at [dbase + j] (and the Gram row at [dbase + k + j])
+    const int dbase = MODE == kPassRitz ? 2 : 0;
+    if constexpr (MODE == kPassRitz || MODE == kPassOrth2) {
+        const double s2 = block_sum(r2, sh);
+        if (tid == 0) a.partial[static_cast<size_t>(MODE == kPassRitz ? 1 : 0) * gridDim.x + blockIdx.x] = s2;
+    }
+    if constexpr (MODE == kPassRitz) {
+        const double s1 = block_sum(r1, sh);
+        if (tid == 0) a.partial[blockIdx.x] = s1;
+    }
+    if constexpr (MODE != kPassOrth2) {
+#pragma unroll
+        for (int jj = 0; jj < kStJ; ++jj) {
+            const int j = static_cast<int>(warp) + kStWarps * jj;
+            double x = acc[jj], g = acc2[jj];
+            for (int s = 16; s > 0; s >>= 1) {
+                x += __shfl_down_sync(0xffffffffu, x, s);
+                g += __shfl_down_sync(0xffffffffu, g, s);
+            }
+            if (lane == 0 && j < k) {
+                a.partial[static_cast<size_t>(dbase + j) * gridDim.x + blockIdx.x] = x;
+                if (MODE == kPassRitz) a.partial[static_cast<size_t>(dbase + k + j) * gridDim.x + blockIdx.x] = g;
+            }
+        }
+    }
+}
+
 __global__ void k_scale_div(double* __restrict__ x, uint64_t n, double divisor) {
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-        x[i] /= divisor;
+    TILE_LOOP(i0, n) {
+        double v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint64_t i = i0 + static_cast<uint64_t>(u) * blockDim.x;
+            v[u] = i < n ? x[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint64_t i = i0 + static_cast<uint64_t>(u) * blockDim.x;
+            if (i < n) x[i] = v[u] / divisor;
+        }
+    }
 }
 
 __global__ void k_set_unit(double* __restrict__ x, uint64_t n, uint64_t at) {
@@ -280,8 +462,8 @@ double seconds_since(std::chrono::steady_clock::time_point t0) {
 }
 
 void ensure_red(Handle& h) {
-    if (h.red.n < static_cast<size_t>(2 * kMaxVec * kRedBlocks + 4 * kMaxVec))
-        h.red.alloc(static_cast<size_t>(2 * kMaxVec * kRedBlocks + 4 * kMaxVec));
+    if (h.red.n < static_cast<size_t>(2 * kMaxVec * kRedBlocks + 8 * kMaxVec))
+        h.red.alloc(static_cast<size_t>(2 * kMaxVec * kRedBlocks + 8 * kMaxVec));
 }
 
 // Device scalar slot (after the partials region) for MGS overlaps.
@@ -326,6 +508,74 @@ void cgs_pass(Handle& h, double* dst, const double* src, double scale, VF&& V, i
                                                         norm ? h.red.p : nullptr);
     CUDA_LAUNCH_CHECK();
     if (norm) finalize_to(h, 1, 4);
+}
+
+// Device slots of the fused passes (after the CGS region at kMaxVec..2kMaxVec)
+constexpr int kSlotRitz = 2 * kMaxVec;            // |res|^2, |corr|^2, d_j (k), Gram row (k)
+constexpr int kSlotOrth1 = kSlotRitz + 2 * kMaxVec + 4;   // e_j (k)
+constexpr int kSlotOrth2 = kSlotOrth1 + kMaxVec + 4;      // |cand|^2
+
+int sm_count() {
+    int dev = 0, v = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    CUDA_CHECK(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+    return v;
+}
+
+// One fused pass (k_dav_stream<MODE>) over the ns streams, its nred
+// reductions finalized (fixed order) and allreduced into device slots
+// [slot, slot + nred).  Stream bases must be 16-byte aligned.
+// Pipeline shape of the fused passes: threads per CTA, CTAs per SM, stages
+// (DETCI_DAV_CFG="threads,ctas,stages" overrides the default 512,1,3).
+struct StreamCfg {
+    int threads = 512, ctas = 1, stages = 3;
+};
+StreamCfg stream_cfg() {
+    StreamCfg c;
+    if (const char* e = std::getenv("DETCI_DAV_CFG")) {
+        int t = 0, k = 0, s = 0;
+        if (std::sscanf(e, "%d,%d,%d", &t, &k, &s) == 3 && (t == 256 || t == 512) && k >= 1 && k <= 4 && s >= 2 &&
+            s <= kStMaxStages) {
+            c.threads = t;
+            c.ctas = k;
+            c.stages = s;
+        }
+    }
+    return c;
+}
+
+template <int MODE>
+void stream_pass(Handle& h, StreamArgs& a, int nred, int slot) {
+    for (int s = 0; s < a.ns; ++s)
+        if (reinterpret_cast<uintptr_t>(a.s[s]) & 15u) fail(DETCI_GPU_E_ERROR, "davidson: misaligned vector");
+    static const StreamCfg cfg = stream_cfg();
+    a.nst = cfg.stages;
+    const size_t per = static_cast<size_t>(a.nst) * a.ns + 1;   // doubles per tile element (stages + probe)
+    a.T = static_cast<uint32_t>(std::min<size_t>(4096, kStSmem / cfg.ctas / 8 / per) & ~size_t{31});
+    if (a.T < 32) fail(DETCI_GPU_E_ERROR, "davidson: stream tile below 32 elements");
+    const size_t smem = per * a.T * sizeof(double);
+    const int grid = sm_count() * cfg.ctas;
+    a.partial = h.red.p;
+    if (cfg.threads == 512) {
+        ensure_dynamic_smem(reinterpret_cast<const void*>(&k_dav_stream<MODE, 512>), smem);
+        k_dav_stream<MODE, 512><<<grid, 512, smem, h.stream>>>(a);
+    } else {
+        ensure_dynamic_smem(reinterpret_cast<const void*>(&k_dav_stream<MODE, 256>), smem);
+        k_dav_stream<MODE, 256><<<grid, 256, smem, h.stream>>>(a);
+    }
+    CUDA_LAUNCH_CHECK();
+    if (nred > 0) {
+        k_finalize<<<nred, 32, 0, h.stream>>>(h.red.p, grid, nred, scalar_slot(h, slot));
+        CUDA_LAUNCH_CHECK();
+        allreduce_device(h, scalar_slot(h, slot), nred);
+    }
+}
+
+// DETCI_DAVIDSON_FUSED=0: the previous per-operation kernels (k_dot_many,
+// k_ritz, two CGS passes), kept for comparison.
+bool fused_passes() {
+    const char* e = std::getenv("DETCI_DAVIDSON_FUSED");
+    return !(e && std::string(e) == "0");
 }
 
 } // namespace
@@ -458,7 +708,10 @@ void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* re
     // subspace does not fit next to it
     // the subspace buffer is cached in the handle across solves (freeing
     // hundreds of MB per solve costs 0.1-0.4 s); a cached buffer counts as free
-    const size_t need = (2 * static_cast<size_t>(ms) + 3) * n * sizeof(double);
+    // vector stride rounded to 16 bytes (the fused passes stream each
+    // vector with 1-D TMA bulk copies)
+    const uint64_t ld = (n + 1) & ~uint64_t{1};
+    const size_t need = (2 * static_cast<size_t>(ms) + 3) * ld * sizeof(double);
     const bool grow = h.dav_store.bytes() < need;
     const bool drop_d = grow && need + (1ull << 30) > free_b + h.dav_store.bytes();
     free_b += h.dbuf.bytes() + h.dav_store.bytes();
@@ -474,13 +727,14 @@ void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* re
     if (drop_d) release_sigma_scratch(h);
     if (grow) {
         store.reset();
-        store.alloc((2 * static_cast<size_t>(ms) + 3) * n);
+        store.alloc((2 * static_cast<size_t>(ms) + 3) * ld);
     }
-    auto V = [&](int j) { return store.p + static_cast<size_t>(j) * n; };
-    auto Wv = [&](int j) { return store.p + static_cast<size_t>(ms + j) * n; };
-    double* ritz = store.p + static_cast<size_t>(2 * ms) * n;
-    double* img = ritz + n;
-    double* corr = img + n;
+    auto V = [&](int j) { return store.p + static_cast<size_t>(j) * ld; };
+    auto Wv = [&](int j) { return store.p + static_cast<size_t>(ms + j) * ld; };
+    double* ritz = store.p + static_cast<size_t>(2 * ms) * ld;
+    double* img = ritz + ld;
+    double* corr = img + ld;
+    const bool fused = fused_passes();
     const unsigned vgrid = kRedBlocks;
 
     // Initial vector (davidson.cpp:84-97).
@@ -541,6 +795,7 @@ void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* re
     bool restart_pending = false;
     double theta = 0.0;
     int status = 0, iters = 0;
+    bool ritz_fresh = false;
     std::vector<detci_dav_iter> trace;
 
     for (int iter = 0; iter < opts.max_iter; ++iter) {
@@ -557,7 +812,20 @@ void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* re
 
         const int k = k_sub;
         t0 = std::chrono::steady_clock::now();
-        {
+        if (fused) {
+            // projected row k-1: <V[k-1], W_j> in one pass (the Gram row
+            // comes out of the Ritz pass below)
+            StreamArgs pa{};
+            pa.ns = k + 1;
+            pa.k = k;
+            pa.n = n;
+            pa.s[0] = V(k - 1);
+            for (int j = 0; j < k; ++j) pa.s[1 + j] = Wv(j);
+            stream_pass<kPassProj>(h, pa, k, 0);
+            std::vector<double> dots(k);
+            read_slots(h, 0, k, dots.data());
+            for (int j = 0; j < k; ++j) proj[(k - 1) * ms + j] = dots[j];
+        } else {
             // projected row k-1 and Gram row k-1 in one pass over V[k-1]
             std::vector<const double*> ys(2 * k);
             for (int j = 0; j < k; ++j) {
@@ -575,22 +843,53 @@ void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* re
         st.subspace_solve_seconds = seconds_since(t0);
 
         t0 = std::chrono::steady_clock::now();
-        RitzArgs ra{};
-        for (int j = 0; j < k; ++j) {
-            ra.v[j] = V(j);
-            ra.w[j] = Wv(j);
-            ra.c[j] = coeffs[j];
+        // the Ritz vector and its image are materialised only when the
+        // subspace collapses onto them (or, after the loop, for the
+        // returned eigenvector)
+        const bool collapse = k_sub >= ms;
+        double rnorm = 0.0, cnorm = 0.0;
+        ritz_fresh = false;
+        if (fused) {
+            // residual, preconditioned correction, <v_j, corr> and the Gram
+            // row in one pass over V, W and the diagonal
+            StreamArgs ra{};
+            ra.ns = 2 * k + 1;
+            ra.k = k;
+            ra.n = n;
+            for (int j = 0; j < k; ++j) {
+                ra.s[j] = V(j);
+                ra.s[k + j] = Wv(j);
+                ra.c[j] = coeffs[j];
+            }
+            ra.s[2 * k] = h.diag.p;
+            ra.theta = theta;
+            ra.out = corr;
+            stream_pass<kPassRitz>(h, ra, 2 * k + 2, kSlotRitz);
+            std::vector<double> sc(2 * k + 2);
+            read_slots(h, kSlotRitz, 2 * k + 2, sc.data());
+            rnorm = std::sqrt(sc[0]);
+            cnorm = std::sqrt(sc[1]);
+            for (int j = 0; j < k; ++j) gram[(k - 1) * ms + j] = sc[2 + k + j];
         }
-        ra.k = k;
-        ra.theta = theta;
-        k_ritz<<<kRedBlocks, kRedThreads, 0, h.stream>>>(ra, h.diag.p, n, ritz, img, corr, h.red.p);
-        CUDA_LAUNCH_CHECK();
-        finalize_to(h, 2, 0);
-        double norms2[2];
-        read_slots(h, 0, 2, norms2);
-        const double rnorm = std::sqrt(norms2[0]);
-        const double cnorm = std::sqrt(norms2[1]);
 
+        if (!fused || collapse) {
+            RitzArgs ra{};
+            for (int j = 0; j < k; ++j) {
+                ra.v[j] = V(j);
+                ra.w[j] = Wv(j);
+                ra.c[j] = coeffs[j];
+            }
+            ra.k = k;
+            ra.theta = theta;
+            k_ritz<<<kRedBlocks, kRedThreads, 0, h.stream>>>(ra, h.diag.p, n, ritz, img, corr, h.red.p);
+            CUDA_LAUNCH_CHECK();
+            ritz_fresh = true;
+            finalize_to(h, 2, 0);
+            double norms2[2];
+            read_slots(h, 0, 2, norms2);
+            rnorm = std::sqrt(norms2[0]);
+            cnorm = std::sqrt(norms2[1]);
+        }
         double gdev = 0.0;
         for (int i = 0; i < k; ++i)
             for (int j = 0; j <= i; ++j)
@@ -617,7 +916,7 @@ void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* re
             status = 2;
             break;
         }
-        if (k_sub >= ms) {  // collapse (davidson.cpp:178-184)
+        if (collapse) {  // collapse (davidson.cpp:178-184)
             CUDA_CHECK(cudaMemcpyAsync(V(0), ritz, n * sizeof(double), cudaMemcpyDeviceToDevice, h.stream));
             CUDA_CHECK(cudaMemcpyAsync(Wv(0), img, n * sizeof(double), cudaMemcpyDeviceToDevice, h.stream));
             k_sub = k_img = 1;
@@ -646,6 +945,23 @@ void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* re
                 finalize_to(h, 1, 4 + t % 2);
             }
             read_slots(h, 4 + steps % 2, 1, &nrm2);
+        } else if (fused && !collapse) {
+            // classical Gram-Schmidt twice from the Ritz pass's dots: pass 1
+            // also forms the second pass's dots, pass 2 the norm
+            StreamArgs oa{};
+            oa.ns = k + 1;
+            oa.k = k;
+            oa.n = n;
+            for (int j = 0; j < k; ++j) oa.s[1 + j] = V(j);
+            oa.s[0] = corr;
+            oa.coef = scalar_slot(h, kSlotRitz + 2);
+            oa.norm2 = scalar_slot(h, kSlotRitz + 1);
+            oa.out = cand;
+            stream_pass<kPassOrth1>(h, oa, k, kSlotOrth1);
+            oa.s[0] = cand;
+            oa.coef = scalar_slot(h, kSlotOrth1);
+            stream_pass<kPassOrth2>(h, oa, 1, kSlotOrth2);
+            read_slots(h, kSlotOrth2, 1, &nrm2);
         } else {
             // classical Gram-Schmidt twice ("twice is enough"): each pass is
             // one multi-dot and one fused update, 2k + 3 vector passes
@@ -670,6 +986,18 @@ void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* re
     res->iterations = iters;
     res->energy = theta;
     if (res->eigenvector) {
+        if (!ritz_fresh && !coeffs.empty()) {   // fused passes: materialise the Ritz vector now
+            RitzArgs ra{};
+            for (int j = 0; j < static_cast<int>(coeffs.size()); ++j) {
+                ra.v[j] = V(j);
+                ra.w[j] = Wv(j);
+                ra.c[j] = coeffs[j];
+            }
+            ra.k = static_cast<int>(coeffs.size());
+            ra.theta = theta;
+            k_ritz<<<kRedBlocks, kRedThreads, 0, h.stream>>>(ra, h.diag.p, n, ritz, img, corr, h.red.p);
+            CUDA_LAUNCH_CHECK();
+        }
         const double nrm = std::sqrt(device_dot(h, ritz, ritz, n));
         k_scale_div<<<vgrid, kRedThreads, 0, h.stream>>>(ritz, n, nrm);
         CUDA_LAUNCH_CHECK();

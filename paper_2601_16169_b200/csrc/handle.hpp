@@ -159,6 +159,7 @@ struct Handle {
 
     // alpha-block partition: P = world (NCCL) or vblocks (virtual)
     std::vector<uint64_t> blk;
+    std::vector<uint32_t> slot_cut;   // measured mixed column shares (rebalance_partition), else empty
     uint64_t a0 = 0, a1 = 0;           // this rank's rows
     uint64_t max_blk = 0;
 
@@ -190,6 +191,8 @@ struct Handle {
 
     PhaseTimer* timer = nullptr;       // set while a timed sigma runs
     std::vector<double> rank_seconds;  // virtual blocks: device seconds per block-rank, last timed sigma
+    std::vector<double> rank_phase_seconds;   // the same per (rank, phase alpha/beta/mixed/combine)
+    double own_phase_seconds[4] = {};         // world > 1: this rank's phases, last timed sigma
     cudaStream_t stream = nullptr, comm_stream = nullptr;
     cudaEvent_t ev[16] = {};
     std::unique_ptr<Comm> comm;        // world > 1: NCCL or loopback (comm.hpp)
@@ -214,6 +217,7 @@ void build_scatter_tpos(Handle& h);
 // Drop the scatter D buffer and windows (re-planned against the free memory
 // at the next sigma); the Davidson solvers call it before allocating.
 void release_sigma_scratch(Handle& h);
+void rebalance_partition(Handle& h, const std::vector<double>& t);
 
 // sigma.cu
 void sigma_device(Handle& h, const double* dx, double* dy, detci_gpu_timings* tm);

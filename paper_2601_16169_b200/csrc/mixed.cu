@@ -903,6 +903,7 @@ bool multi_ring() {
 // heaviest strings (1.5x the mean at C3 / P = 8).
 std::pair<uint32_t, uint32_t> mixed_slots(const Handle& h, int g, int P) {
     const uint64_t total = static_cast<uint64_t>(h.nslices) * kWarp;
+    if (h.slot_cut.size() == static_cast<size_t>(P) + 1) return {h.slot_cut[g], h.slot_cut[g + 1]};
     const auto& pre = h.slice_prefix;
     const bool weighted = pre.size() == static_cast<size_t>(h.nslices) + 1 && pre.back() > 0;
     auto at = [&](int k) -> uint32_t {

@@ -765,7 +765,10 @@ void sigma_device(Handle& h, const double* dx, double* dy, detci_gpu_timings* ou
         double parts[5];
         tm.collect(parts);
         out->mixed_reduce_seconds = parts[4];
-        h.rank_seconds = tm.per_rank(std::max(h.world, h.vblocks) > 1 && h.world == 1 ? h.vblocks : 0);
+        const int vP = std::max(h.world, h.vblocks) > 1 && h.world == 1 ? h.vblocks : 0;
+        h.rank_seconds = tm.per_rank(vP);
+        h.rank_phase_seconds = tm.per_rank_phase(vP);
+        for (int q = 0; q < 4; ++q) h.own_phase_seconds[q] = parts[q];
         float ms = 0.f;
         CUDA_CHECK(cudaEventElapsedTime(&ms, t0, t1));
         out->alpha_seconds = parts[0];

@@ -66,6 +66,17 @@ struct PhaseTimer {
         }
         return t;
     }
+    // the same by phase: t[rank * 4 + phase], phases 0-3
+    std::vector<double> per_rank_phase(int P) {
+        std::vector<double> t(4 * static_cast<size_t>(std::max(P, 0)), 0.0);
+        for (size_t i = 0; i < ev.size(); ++i) {
+            if (rk[i] < 0 || rk[i] >= P || cat[i] == 4) continue;
+            float ms = 0.f;
+            CUDA_CHECK(cudaEventElapsedTime(&ms, ev[i].first, ev[i].second));
+            t[4 * static_cast<size_t>(rk[i]) + cat[i]] += ms * 1e-3;
+        }
+        return t;
+    }
 };
 
 using Ptrs = std::array<const double*, kMaxM>;

@@ -122,10 +122,23 @@ class GpuBasis:
         self._check(self._lib.detci_gpu_set_integrals(self._h, float(core), _ptr(h1, C.c_double),
                                                       _ptr(eri, C.c_double)))
         self._check(self._lib.detci_gpu_build_basis(self._h))
+        self._query_rows()
+
+    def _query_rows(self) -> None:
         b, e, nb = C.c_uint64(), C.c_uint64(), C.c_uint64()
         self._check(self._lib.detci_gpu_local_rows(self._h, C.byref(b), C.byref(e), C.byref(nb)))
         self.row_begin, self.row_end = b.value, e.value
         self.local_dim = (e.value - b.value) * nb.value
+
+    def rebalance(self, rounds: int = 1) -> float:
+        """Measured rebalance of the alpha-row blocks and mixed column
+        shares (detci_gpu_rebalance; collective with several ranks).  Returns
+        the slowest/mean rank ratio measured before rebalancing; the local
+        row range may change (row_begin, row_end, local_dim are refreshed)."""
+        r = C.c_double(1.0)
+        self._check(self._lib.detci_gpu_rebalance(self._h, int(rounds), C.byref(r)))
+        self._query_rows()
+        return r.value
 
     # -- plumbing -----------------------------------------------------------
     def _check(self, code: int, use_handle: bool = True) -> None:
@@ -210,6 +223,15 @@ class GpuBasis:
         buf = (C.c_double * 64)()
         self._check(self._lib.detci_gpu_rank_seconds(self._h, buf, 64, C.byref(cnt)))
         return [buf[i] for i in range(min(cnt.value, 64))]
+
+    def rank_phase_seconds(self) -> List[List[float]]:
+        """rank_seconds split by phase: [alpha, beta, mixed, combine] per
+        block-rank."""
+        cnt = C.c_int()
+        buf = (C.c_double * 256)()
+        self._check(self._lib.detci_gpu_rank_phase_seconds(self._h, buf, 256, C.byref(cnt)))
+        n = min(cnt.value, 256) // 4
+        return [[buf[4 * r + q] for q in range(4)] for r in range(n)]
 
     def linear_operator(self) -> Callable[[np.ndarray, np.ndarray], None]:
         """LinearOperator (davidson.hpp:28): y = H x on host arrays."""

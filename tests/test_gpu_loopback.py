@@ -168,3 +168,48 @@ def test_loopback_davidson_capacity_is_collective():
     res, errs = run_ranks(2, ints, s, s, body, timeout=120, per_rank={1: {"memory_budget_bytes": 400_000}})
     assert isinstance(errs[1], errors.CapacityError), errs
     assert type(errs[0]) is errors.Error and "another rank failed" in str(errs[0])
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_loopback_rebalance_then_sigma_and_davidson(c1, P):
+    """The measured rebalance is collective (per-rank phase times are
+    all-reduced, every rank cuts the same partition): after two rounds the
+    ranks still tile the rows, sigma matches one GPU and the reference rows,
+    and Davidson gives the single-GPU energy."""
+    ints, a, b, rows, x, y1 = c1
+    nb = len(b)
+    with detci.GpuBasis(ints.norbs, a, b, ints.core, ints.h1, ints.eri) as basis:
+        one = detci.davidson_solve(basis, want_vector=False)
+
+    def body(r, basis):
+        before = (basis.row_begin, basis.row_end)
+        ratio = basis.rebalance(2)
+        y = detci.matvec(basis, local_slice(x, basis, nb))
+        e = detci.davidson_solve(basis, want_vector=False).energy
+        return basis.row_begin, basis.row_end, y, e, ratio, before
+
+    res, errs = run_ranks(P, ints, a, b, body, weighted_partition=True)
+    check(errs)
+    res.sort(key=lambda t: t[0])
+    assert res[0][0] == 0 and res[-1][1] == len(a)
+    assert all(res[i][1] == res[i + 1][0] for i in range(P - 1))
+    assert all(t[4] >= 1.0 for t in res) and len({t[4] for t in res}) == 1   # one agreed measurement
+    y = np.concatenate([t[2] for t in res])
+    assert rel_diff(y, y1) <= 1e-12
+    rr = rows["rows"].astype(np.int64)
+    assert rel_diff(y.reshape(len(a), -1)[rr], rows["sigma_rows"]) <= 1e-12
+    assert len({t[3] for t in res}) == 1 and abs(res[0][3] - one.energy) <= 1e-10
+
+
+def test_virtual_blocks_rebalance(c1):
+    """Virtual blocks: the rebalance re-cuts rows and column shares from the
+    per-block timings; sigma is unchanged (1e-12) for both schedules' data."""
+    ints, a, b, rows, x, y1 = c1
+    with detci.GpuBasis(ints.norbs, a, b, ints.core, ints.h1, ints.eri,
+                        detci.BasisOptions(virtual_blocks=4, weighted_partition=True)) as basis:
+        ratio = basis.rebalance(2)
+        assert ratio >= 1.0
+        y = detci.matvec(basis, x, timings={})
+        assert rel_diff(y, y1) <= 1e-12
+        ph = basis.rank_phase_seconds()
+        assert len(ph) == 4 and all(len(r) == 4 and r[0] > 0 and r[2] > 0 for r in ph)
