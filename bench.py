@@ -248,6 +248,10 @@ def run_gpu_arm(args):
         opts = detci.BasisOptions(device=local_rank, rank=rank, world_size=world, nccl_id=nccl_id,
                                   weighted_partition=world > 1)
         basis = detci.GpuBasis(ints.norbs, a, b, ints.core, ints.h1, ints.eri, opts)
+        if world > 1:
+            # measured rebalance of the row blocks and column shares
+            # (detci_gpu_rebalance, collective), part of the build
+            basis.balance_before = basis.rebalance(2)
         return ints, a, b, basis, time.time() - t_build
 
     def measure(cfg, basis, na, nb, steps, warmup, with_clocks=False, pageable=False):
@@ -580,7 +584,7 @@ def run_gpu_arm(args):
                        "parallelism": (f"alpha-block ring x{world} (NCCL send/recv)"
                                        if os.environ.get("DETCI_MULTI") == "ring" else
                                        f"alpha blocks x{world}: NCCL allgather of C, beta-column share of the "
-                                       f"mixed term, point-to-point exchange") if world > 1 else "single GPU",
+                                       f"mixed term, point-to-point exchange; measured rebalance, 2 rounds") if world > 1 else "single GPU",
                        "build_seconds": build_s, "sigma_s_per_iter": per_step,
                        "phase_seconds": split, "parity_rows_max_rel_err": main["parity_rows_max_rel_err"],
                        "parity_rows_checked": main["parity_rows_checked"]},

@@ -8,7 +8,7 @@
 //
 //   detci_gpu run --integrals F --dets D [--method gpu|stored|matrix_free]
 //       [--devices N] [--transport nccl|loopback] [--virtual-blocks V]
-//       [--bit-length B] [--shuffle]
+//       [--balance-rounds R] [--bit-length B] [--shuffle]
 //       [--seed S] [--tol T] [--max-iter N] [--max-subspace K]
 //       [--memory-budget BYTES] [--workers W] [--format text|json]
 //       [--no-timings] [--out PATH]
@@ -18,7 +18,8 @@
 // and the device Davidson.  stored: the device CSR (build_stored_matrix
 // layout) behind the same device Davidson.  --devices N > 1 runs one host
 // thread per GPU, each with its own handle and an NCCL communicator over the
-// N devices (alpha blocks + C ring); rank 0 reports.  --transport loopback
+// N devices (alpha blocks + C allgather / column-share exchange), cut by R
+// (default 2) rounds of the measured rebalance; rank 0 reports.  --transport loopback
 // runs the N ranks as threads on ONE GPU over the in-process transport (the
 // same rank code, for single-GPU machines).  Exit codes follow the reference
 // CLI (tools/detci.cpp:32-34, 59-63): 0 converged, 1 error (message on
@@ -55,6 +56,7 @@ struct GpuConfig {
     int devices = 1;
     int virtual_blocks = 1;
     std::string transport = "nccl";   // nccl | loopback
+    int balance_rounds = 2;           // measured rebalance rounds (devices > 1)
 };
 
 constexpr int kExitOk = 0, kExitError = 1, kExitNotConverged = 2;   // tools/detci.cpp:32-34
@@ -82,6 +84,7 @@ GpuRun run_rank(const RunConfig& cfg, const GpuConfig& g, int norbs, const std::
     o.nccl_id = nccl_id;
     o.virtual_blocks = g.virtual_blocks;
     o.memory_budget_bytes = 0;
+    o.balance_rounds = g.devices > 1 ? g.balance_rounds : 0;
     auto t0 = std::chrono::steady_clock::now();
     gpu::DeviceBasis dev(norbs, a, b, table, o);
     out.build_seconds = since(t0);
@@ -103,7 +106,8 @@ GpuRun run_rank(const RunConfig& cfg, const GpuConfig& g, int norbs, const std::
 
 std::string usage() {
     return "usage: detci_gpu run --integrals F --dets D [--method gpu|stored|matrix_free] [--devices N]\n"
-           "       [--transport nccl|loopback] [--virtual-blocks V] [--bit-length B] [--shuffle] [--seed S]\n"
+           "       [--transport nccl|loopback] [--virtual-blocks V] [--balance-rounds R] [--bit-length B]\n"
+           "       [--shuffle] [--seed S]\n"
            "       [--tol T] [--max-iter N]\n"
            "       [--max-subspace K] [--memory-budget BYTES] [--workers W] [--format text|json]\n"
            "       [--no-timings] [--out PATH]\n";
@@ -132,6 +136,7 @@ int main(int argc, char** argv) {
             else if (k == "--devices") g.devices = std::stoi(val());
             else if (k == "--virtual-blocks") g.virtual_blocks = std::stoi(val());
             else if (k == "--transport") g.transport = val();
+            else if (k == "--balance-rounds") g.balance_rounds = std::stoi(val());
             else if (k == "--bit-length") cfg.bit_length = std::stoi(val());
             else if (k == "--shuffle") cfg.shuffle = true;
             else if (k == "--seed") cfg.seed = std::stoull(val());

@@ -69,6 +69,9 @@ struct DeviceOptions {
     // > 0: the world_size ranks are host threads of this process over the
     // loopback transport (group id), not NCCL (detci_gpu_create_loopback)
     std::uint64_t loopback_group = 0;
+    // > 0: rounds of the measured rebalance after the build (world_size or
+    // virtual_blocks > 1; detci_gpu_rebalance)
+    int balance_rounds = 0;
 };
 
 class DeviceBasis {
@@ -113,6 +116,7 @@ private:
                             eri[((p * nn + q) * nn + r) * nn + s] = table.two_electron(p, q, r, s);
             rethrow(detci_gpu_set_integrals(h_, table.core_energy(), h1.data(), eri.data()), h_);
             rethrow(detci_gpu_build_basis(h_), h_);
+            if (o.balance_rounds > 0) rethrow(detci_gpu_rebalance(h_, o.balance_rounds, nullptr), h_);
             std::uint64_t nb = 0;
             rethrow(detci_gpu_local_rows(h_, &row_begin_, &row_end_, &nb), h_);
             local_dim_ = (row_end_ - row_begin_) * nb;
