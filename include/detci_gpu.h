@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define DETCI_GPU_ABI_VERSION 2
+#define DETCI_GPU_ABI_VERSION 3
 
 enum detci_gpu_status {
     DETCI_GPU_OK = 0,
@@ -163,12 +163,24 @@ int detci_gpu_nccl_unique_id(uint8_t out[128]);
 
 /* ---- inputs ---------------------------------------------------------------
  * Channel strings: one uint64 occupation mask per string, bit p = spatial
- * orbital p (norbs <= 64; wider systems -> DETCI_GPU_E_UNSUPPORTED).  Global
- * lists on every rank.  Errors follow prepare_channel/index_strings: empty
- * list, bits beyond norbs or inconsistent popcounts -> E_INPUT.  Duplicates
- * are reported by detci_gpu_build_basis (as generate_singles does). */
+ * orbital p (norbs <= 64).  Global lists on every rank.  Errors follow
+ * prepare_channel/index_strings: empty list, bits beyond norbs or
+ * inconsistent popcounts -> E_INPUT.  Duplicates are reported by
+ * detci_gpu_build_basis (as generate_singles does).
+ * Replaces Basis::alpha_strings / beta_strings (basis.hpp:40-60) for one-word
+ * packings. */
 int detci_gpu_set_strings(detci_gpu_handle* h, int norbs, const uint64_t* alpha, size_t na,
                           const uint64_t* beta, size_t nb);
+
+/* The same for norbs <= 128: `words` (1 or 2) consecutive uint64 per string,
+ * word w holding orbitals 64w .. 64w+63 (the word order of the reference's
+ * BitString, bitstring.hpp:33-51, at bit_length 64).  The reference accepts
+ * up to kMaxKernelBits = 256 spin-orbitals (slater_condon.hpp:26,
+ * basis.cpp:83-87); norbs > 128 -> E_INPUT.  Systems with norbs > 64 run the
+ * scatter mixed kernel only: DETCI_MIXED=gather or 4-vector blocks ->
+ * E_UNSUPPORTED. */
+int detci_gpu_set_strings_words(detci_gpu_handle* h, int norbs, int words, const uint64_t* alpha,
+                                size_t na, const uint64_t* beta, size_t nb);
 
 /* h1: norbs^2 row-major; eri: norbs^4 dense chemist (pq|rs), 8-fold symmetric. */
 int detci_gpu_set_integrals(detci_gpu_handle* h, double core, const double* h1,

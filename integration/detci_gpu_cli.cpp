@@ -216,9 +216,9 @@ int main(int argc, char** argv) {
                     if (e) std::rethrow_exception(e);
             }
             const GpuRun& r0 = runs[0];
-            report.dimension = a.size() * b.size();
-            report.n_alpha = a.size();
-            report.n_beta = b.size();
+            report.dimension = list.alpha.size() * list.beta.size();
+            report.n_alpha = list.alpha.size();
+            report.n_beta = list.beta.size();
             report.norbs = n;
             report.timings.diag_precompute = r0.build_seconds;   // tables + diagonal, on the device
             report.timings.stored_build = r0.stored_build_seconds;

@@ -48,16 +48,21 @@ inline void rethrow(int code, const detci_gpu_handle* h) {
     }
 }
 
-/// One uint64 mask per channel string; the device path holds norbs <= 64.
+/// uint64 words per channel string on the device: 1 for norbs <= 64, 2 up
+/// to 128 (the reference itself allows kMaxKernelBits = 256 spin-orbitals).
+inline int string_words(int norbs) {
+    if (norbs > 128) throw UnsupportedError("gpu: norbs > 128 is not supported on the device path");
+    return norbs > 64 ? 2 : 1;
+}
+
+/// Channel strings as string_words(norbs) uint64 words each, word w holding
+/// orbitals 64w .. 64w+63 (from occupied_list, whatever the BitString's
+/// bit_length).
 inline std::vector<std::uint64_t> channel_masks(const std::vector<BitString>& strings, int norbs) {
-    if (norbs > 64) throw UnsupportedError("gpu: norbs > 64 is not supported on the device path");
-    std::vector<std::uint64_t> out;
-    out.reserve(strings.size());
-    for (const BitString& s : strings) {
-        std::uint64_t m = 0;
-        for (int i : occupied_list(s)) m |= std::uint64_t{1} << i;
-        out.push_back(m);
-    }
+    const int w = string_words(norbs);
+    std::vector<std::uint64_t> out(strings.size() * w, 0);
+    for (std::size_t k = 0; k < strings.size(); ++k)
+        for (int i : occupied_list(strings[k])) out[k * w + i / 64] |= std::uint64_t{1} << (i % 64);
     return out;
 }
 
@@ -104,7 +109,8 @@ private:
         if (o.loopback_group) rethrow(detci_gpu_create_loopback(&d, o.loopback_group, &h_), nullptr);
         else rethrow(detci_gpu_create(&d, &h_), nullptr);
         try {
-            rethrow(detci_gpu_set_strings(h_, n, a.data(), a.size(), b.data(), b.size()), h_);
+            const int w = string_words(n);
+            rethrow(detci_gpu_set_strings_words(h_, n, w, a.data(), a.size() / w, b.data(), b.size() / w), h_);
             const std::size_t nn = static_cast<std::size_t>(n);
             std::vector<double> h1(nn * nn), eri(nn * nn * nn * nn);
             for (int p = 0; p < n; ++p)

@@ -72,6 +72,8 @@ class RefLib:
         L.ref_generate_table.argtypes = [u64p, C.c_long, C.c_int, C.c_int, u32p, u64p, u32p, u64p]
         L.ref_basis_create.argtypes = [vp, u64p, C.c_long, u64p, C.c_long, C.c_int, C.c_int, C.c_uint64, C.c_int,
                                        C.POINTER(vp)]
+        L.ref_basis_create_words.argtypes = [vp, C.c_int, u64p, C.c_long, u64p, C.c_long, C.c_int, C.c_int,
+                                             C.c_uint64, C.c_int, C.POINTER(vp)]
         L.ref_basis_free.argtypes = [vp]
         L.ref_basis_stats.argtypes = [vp, dp, C.POINTER(C.c_int)]
         L.ref_basis_diag.argtypes = [vp, dp]
@@ -200,6 +202,17 @@ class RefTable:
         h = vp()
         self.ref.check(self.ref.lib.ref_basis_create(self.h, _p(a, C.c_uint64), len(a), _p(b, C.c_uint64), len(b),
                                                      bit_length, int(cache), budget, workers, C.byref(h)))
+        return RefBasis(self.ref, h, len(a), len(b))
+
+    def basis_words(self, alpha, beta, bit_length=0, cache=True, budget=8 << 30, workers=0) -> "RefBasis":
+        """Strings as (n, words) uint64 arrays (norbs > 64)."""
+        a = np.ascontiguousarray(alpha, dtype=np.uint64)
+        b = np.ascontiguousarray(beta, dtype=np.uint64)
+        words = 1 if a.ndim == 1 else a.shape[1]
+        h = vp()
+        self.ref.check(self.ref.lib.ref_basis_create_words(self.h, words, _p(a, C.c_uint64), len(a),
+                                                           _p(b, C.c_uint64), len(b), bit_length, int(cache),
+                                                           budget, workers, C.byref(h)))
         return RefBasis(self.ref, h, len(a), len(b))
 
 

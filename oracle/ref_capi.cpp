@@ -88,6 +88,14 @@ BitString mask_to_string(std::uint64_t mask, int norbs) {
     return from_occupied(occ, make_packing(norbs, norbs));
 }
 
+// `words` uint64 per string, word w = orbitals 64w .. 64w+63 (norbs <= 128)
+BitString words_to_string(const std::uint64_t* w, int words, int norbs) {
+    std::vector<int> occ;
+    for (int i = 0; i < norbs && i < 64 * words; ++i)
+        if ((w[i / 64] >> (i % 64)) & 1u) occ.push_back(i);
+    return from_occupied(occ, make_packing(norbs, norbs));
+}
+
 std::uint64_t string_to_mask(const BitString& s) {
     std::uint64_t m = 0;
     for (int i : occupied_list(s)) m |= std::uint64_t{1} << i;
@@ -266,6 +274,24 @@ int ref_basis_create(void* tp, const std::uint64_t* alpha, long na, const std::u
         std::vector<BitString> a, b;
         for (long i = 0; i < na; ++i) a.push_back(mask_to_string(alpha[i], t->norbs()));
         for (long i = 0; i < nb; ++i) b.push_back(mask_to_string(beta[i], t->norbs()));
+        BasisOptions o;
+        o.bit_length = bit_length;
+        o.cache = cache != 0;
+        o.memory_budget_bytes = budget;
+        o.workers = workers;
+        *out = new Basis(build_basis(std::move(a), std::move(b), *t, o));
+    })
+}
+
+// Multi-word variant of ref_basis_create (norbs up to 128 here; the
+// reference itself allows kMaxKernelBits = 256 spin-orbitals).
+int ref_basis_create_words(void* tp, int words, const std::uint64_t* alpha, long na, const std::uint64_t* beta,
+                           long nb, int bit_length, int cache, std::uint64_t budget, int workers, void** out) {
+    GUARD({
+        const auto* t = static_cast<IntegralTable*>(tp);
+        std::vector<BitString> a, b;
+        for (long i = 0; i < na; ++i) a.push_back(words_to_string(alpha + i * words, words, t->norbs()));
+        for (long i = 0; i < nb; ++i) b.push_back(words_to_string(beta + i * words, words, t->norbs()));
         BasisOptions o;
         o.bit_length = bit_length;
         o.cache = cache != 0;

@@ -117,6 +117,7 @@ SIGNATURES = {
     "detci_gpu_last_error": (C.c_char_p, [vp]),
     "detci_gpu_nccl_unique_id": (C.c_int, [u8p]),
     "detci_gpu_set_strings": (C.c_int, [vp, C.c_int, u64p, C.c_size_t, u64p, C.c_size_t]),
+    "detci_gpu_set_strings_words": (C.c_int, [vp, C.c_int, C.c_int, u64p, C.c_size_t, u64p, C.c_size_t]),
     "detci_gpu_set_integrals": (C.c_int, [vp, C.c_double, dp, dp]),
     "detci_gpu_build_basis": (C.c_int, [vp]),
     "detci_gpu_helper_size": (C.c_int, [vp, C.c_int, C.c_int, u64p]),

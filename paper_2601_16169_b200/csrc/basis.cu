@@ -59,16 +59,18 @@ constexpr int kPairBlock = 512;   // 16 warps = 16 source rows per CTA
 // come out ascending by construction: a warp tests 32 consecutive j, and a
 // ballot + prefix popcount compacts the hits in order.  Pass 1 counts,
 // pass 2 fills at the scanned offsets.
-template <bool kFill>
+// kWide: norbs > 64, the high words of the strings in `shi`.
+template <bool kFill, bool kWide>
 __global__ void __launch_bounds__(kPairBlock)
-k_pair_scan(const uint64_t* __restrict__ s, uint32_t n, uint32_t* __restrict__ len_s,
+k_pair_scan(const uint64_t* __restrict__ s, const uint64_t* __restrict__ shi, uint32_t n, uint32_t* __restrict__ len_s,
             uint32_t* __restrict__ len_d, const uint64_t* __restrict__ off_s,
             const uint64_t* __restrict__ off_d, uint32_t* __restrict__ flat_s,
             uint32_t* __restrict__ flat_d, unsigned int* __restrict__ dup_index) {
-    __shared__ uint64_t tile[kPairTile];
+    __shared__ uint64_t tile[kWide ? 2 : 1][kPairTile];
     const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
     const uint32_t i = blockIdx.x * (kPairBlock / kWarp) + warp;
     const uint64_t si = i < n ? s[i] : 0ull;
+    const uint64_t si_hi = kWide && i < n ? shi[i] : 0ull;
     const unsigned lt_mask = (1u << lane) - 1u;
     uint32_t cs = 0, cd = 0;
     uint64_t base_s = 0, base_d = 0;
@@ -79,12 +81,16 @@ k_pair_scan(const uint64_t* __restrict__ s, uint32_t n, uint32_t* __restrict__ l
     for (uint32_t t0 = 0; t0 < n; t0 += kPairTile) {
         const uint32_t tn = min(static_cast<uint32_t>(kPairTile), n - t0);
         __syncthreads();
-        for (uint32_t k = threadIdx.x; k < tn; k += kPairBlock) tile[k] = s[t0 + k];
+        for (uint32_t k = threadIdx.x; k < tn; k += kPairBlock) {
+            tile[0][k] = s[t0 + k];
+            if (kWide) tile[kWide ? 1 : 0][k] = shi[t0 + k];
+        }
         __syncthreads();
         if (i >= n) continue;
         for (uint32_t k = 0; k < tn; k += kWarp) {
             const uint32_t kk = k + lane;
-            const int d = kk < tn ? __popcll(si ^ tile[kk]) : -1;
+            const int d = kk < tn ? __popcll(si ^ tile[0][kk]) + (kWide ? __popcll(si_hi ^ tile[kWide ? 1 : 0][kk]) : 0)
+                                  : -1;
             const unsigned bs = __ballot_sync(0xffffffffu, d == 2);
             const unsigned bd = __ballot_sync(0xffffffffu, d == 4);
             if (kFill) {
@@ -156,7 +162,7 @@ __global__ void k_tpos(const uint32_t* __restrict__ flat, const uint64_t* __rest
 }
 
 // Same-spin pair tables, one warp per source row, lanes over entries.
-__global__ void k_pair_tables(int kind, const uint64_t* __restrict__ s, uint32_t n,
+__global__ void k_pair_tables(int kind, const uint64_t* __restrict__ s, const uint64_t* __restrict__ shi, uint32_t n,
                               const uint32_t* __restrict__ flat, const uint64_t* __restrict__ off,
                               const uint32_t* __restrict__ len, const double* __restrict__ h1,
                               const double* __restrict__ eri, int norbs, double* __restrict__ pv,
@@ -164,28 +170,28 @@ __global__ void k_pair_tables(int kind, const uint64_t* __restrict__ s, uint32_t
     const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
     const int lane = threadIdx.x % kWarp;
     if (i >= n) return;
-    const uint64_t si = s[i];
+    const Bits si = load_bits(s, shi, i);
     const uint64_t o = off[i];
     for (uint32_t k = lane; k < len[i]; k += kWarp) {
-        const PairEntry e = make_pair_entry(kind, si, s[flat[o + k]], h1, eri, norbs);
+        const PairEntry e = make_pair_entry(kind, si, load_bits(s, shi, flat[o + k]), h1, eri, norbs);
         pv[o + k] = e.v;
         if (kind == 0) pab[o + k] = e.ab_sign;
     }
 }
 
 // J[t * n + i] = sum_{r in s_i} (p q | r r), t = tri(p, q), p > q.
-__global__ void k_jtable(const uint64_t* __restrict__ s, uint32_t n,
+__global__ void k_jtable(const uint64_t* __restrict__ s, const uint64_t* __restrict__ shi, uint32_t n,
                          const double* __restrict__ eri, int norbs, double* __restrict__ J) {
     const uint32_t t = blockIdx.y;
     int p = 1;
     while ((p + 1) * p / 2 <= static_cast<int>(t)) ++p;
     const int q = static_cast<int>(t) - p * (p - 1) / 2;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        uint64_t bits = s[i];
+        Bits bits = load_bits(s, shi, i);
         double acc = 0.0;
-        while (bits) {
-            const int r = __ffsll(static_cast<long long>(bits)) - 1;
-            bits &= bits - 1;
+        while (any(bits)) {
+            const int r = lowest(bits);
+            bits = drop_lowest(bits);
             acc += eri_at(eri, norbs, p, q, r, r);
         }
         J[static_cast<size_t>(t) * n + i] = acc;
@@ -193,22 +199,21 @@ __global__ void k_jtable(const uint64_t* __restrict__ s, uint32_t n,
 }
 
 // Diagonal pieces: E[i] = sum_{p in s} h_pp + sum_{p<q in s} [(pp|qq) - (pq|qp)].
-__global__ void k_string_energy(const uint64_t* __restrict__ s, uint32_t n,
+__global__ void k_string_energy(const uint64_t* __restrict__ s, const uint64_t* __restrict__ shi, uint32_t n,
                                 const double* __restrict__ h1, const double* __restrict__ eri,
                                 int norbs, double* __restrict__ E) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const uint64_t si = s[i];
+    Bits a = load_bits(s, shi, i);
     double acc = 0.0;
-    uint64_t a = si;
-    while (a) {
-        const int p = __ffsll(static_cast<long long>(a)) - 1;
-        a &= a - 1;
+    while (any(a)) {
+        const int p = lowest(a);
+        a = drop_lowest(a);
         acc += h1[p * norbs + p];
-        uint64_t b = a;
-        while (b) {
-            const int q = __ffsll(static_cast<long long>(b)) - 1;
-            b &= b - 1;
+        Bits b = a;
+        while (any(b)) {
+            const int q = lowest(b);
+            b = drop_lowest(b);
             acc += eri_at(eri, norbs, p, p, q, q) - eri_at(eri, norbs, p, q, q, p);
         }
     }
@@ -216,16 +221,16 @@ __global__ void k_string_energy(const uint64_t* __restrict__ s, uint32_t n,
 }
 
 // U[p * nb + ib] = sum_{q in B_ib} (pp|qq): the opposite-spin Coulomb part.
-__global__ void k_u_table(const uint64_t* __restrict__ sb, uint32_t nb,
+__global__ void k_u_table(const uint64_t* __restrict__ sb, const uint64_t* __restrict__ sbhi, uint32_t nb,
                           const double* __restrict__ eri, int norbs, double* __restrict__ U) {
     const uint32_t ib = blockIdx.x * blockDim.x + threadIdx.x;
     const int p = blockIdx.y;
     if (ib >= nb) return;
-    uint64_t b = sb[ib];
+    Bits b = load_bits(sb, sbhi, ib);
     double acc = 0.0;
-    while (b) {
-        const int q = __ffsll(static_cast<long long>(b)) - 1;
-        b &= b - 1;
+    while (any(b)) {
+        const int q = lowest(b);
+        b = drop_lowest(b);
         acc += eri_at(eri, norbs, p, p, q, q);
     }
     U[static_cast<size_t>(p) * nb + ib] = acc;
@@ -233,17 +238,17 @@ __global__ void k_u_table(const uint64_t* __restrict__ sb, uint32_t nb,
 
 // diag[ia, ib] = core + E_A[ia] + E_B[ib] + sum_{p in A} U[p][ib]
 // (zero_excite_words, slater_condon.cpp:23-39, regrouped by channel).
-__global__ void k_diag(const uint64_t* __restrict__ sa, const double* __restrict__ EA,
+__global__ void k_diag(const uint64_t* __restrict__ sa, const uint64_t* __restrict__ sahi, const double* __restrict__ EA,
                        uint32_t nloc, const double* __restrict__ EB, const double* __restrict__ U,
                        uint32_t nb, double core, double* __restrict__ diag) {
     const uint32_t ib = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t ia = blockIdx.y;
     if (ib >= nb || ia >= nloc) return;
-    uint64_t a = sa[ia];
+    Bits a = load_bits(sa, sahi, ia);
     double x = 0.0;
-    while (a) {
-        const int p = __ffsll(static_cast<long long>(a)) - 1;
-        a &= a - 1;
+    while (any(a)) {
+        const int p = lowest(a);
+        a = drop_lowest(a);
         x += U[static_cast<size_t>(p) * nb + ib];
     }
     diag[static_cast<size_t>(ia) * nb + ib] = core + EA[ia] + EB[ib] + x;
@@ -268,8 +273,13 @@ void build_helper_lists(Handle& h, int c) {
         t.offset[k].alloc(static_cast<size_t>(n) + 1);  // [n] holds the total
     }
     const unsigned grid = (n + kPairBlock / kWarp - 1) / (kPairBlock / kWarp);
-    k_pair_scan<false><<<grid, kPairBlock, 0, h.stream>>>(t.strings.p, n, t.len[0].p, t.len[1].p,
-                                                          nullptr, nullptr, nullptr, nullptr, dup.p);
+    if (t.hi())
+        k_pair_scan<false, true><<<grid, kPairBlock, 0, h.stream>>>(t.strings.p, t.hi(), n, t.len[0].p, t.len[1].p,
+                                                                    nullptr, nullptr, nullptr, nullptr, dup.p);
+    else
+        k_pair_scan<false, false><<<grid, kPairBlock, 0, h.stream>>>(t.strings.p, nullptr, n, t.len[0].p,
+                                                                     t.len[1].p, nullptr, nullptr, nullptr, nullptr,
+                                                                     dup.p);
     CUDA_LAUNCH_CHECK();
     unsigned int dup_host = none;
     CUDA_CHECK(cudaMemcpyAsync(&dup_host, dup.p, sizeof(dup_host), cudaMemcpyDeviceToHost, h.stream));
@@ -284,9 +294,14 @@ void build_helper_lists(Handle& h, int c) {
         fail(DETCI_GPU_E_INPUT, "excitation tables: duplicate string at index " +
                                     std::to_string(dup_host));
     for (int k = 0; k < 2; ++k) t.flat[k].alloc(std::max<uint64_t>(t.nflat[k], 1));
-    k_pair_scan<true><<<grid, kPairBlock, 0, h.stream>>>(t.strings.p, n, nullptr, nullptr,
-                                                         t.offset[0].p, t.offset[1].p, t.flat[0].p,
-                                                         t.flat[1].p, nullptr);
+    if (t.hi())
+        k_pair_scan<true, true><<<grid, kPairBlock, 0, h.stream>>>(t.strings.p, t.hi(), n, nullptr, nullptr,
+                                                                   t.offset[0].p, t.offset[1].p, t.flat[0].p,
+                                                                   t.flat[1].p, nullptr);
+    else
+        k_pair_scan<true, false><<<grid, kPairBlock, 0, h.stream>>>(t.strings.p, nullptr, n, nullptr, nullptr,
+                                                                    t.offset[0].p, t.offset[1].p, t.flat[0].p,
+                                                                    t.flat[1].p, nullptr);
     CUDA_LAUNCH_CHECK();
     for (int k = 0; k < 2; ++k) {
         t.h_len[k].resize(n);
@@ -303,7 +318,7 @@ void build_pair_tables(Handle& h, int c) {
         t.pv[k].alloc(m);
         if (k == 0) t.pab.alloc(m);
         const unsigned grid = (n * kWarp + 255) / 256;
-        k_pair_tables<<<grid, 256, 0, h.stream>>>(k, t.strings.p, n, t.flat[k].p,
+        k_pair_tables<<<grid, 256, 0, h.stream>>>(k, t.strings.p, t.hi(), n, t.flat[k].p,
                                                   t.offset[k].p, t.len[k].p, h.d_h1.p, h.d_eri.p,
                                                   h.norbs, t.pv[k].p, t.pab.p);
         CUDA_LAUNCH_CHECK();
@@ -312,7 +327,7 @@ void build_pair_tables(Handle& h, int c) {
     t.J.alloc(std::max<size_t>(static_cast<size_t>(ntri) * n, 1));
     if (ntri > 0) {
         dim3 grid(std::min<uint32_t>((n + 255) / 256, 64), ntri);
-        k_jtable<<<grid, 256, 0, h.stream>>>(t.strings.p, n, h.d_eri.p, h.norbs, t.J.p);
+        k_jtable<<<grid, 256, 0, h.stream>>>(t.strings.p, t.hi(), n, h.d_eri.p, h.norbs, t.J.p);
         CUDA_LAUNCH_CHECK();
     }
 }
@@ -378,7 +393,9 @@ void build_mixed_sell(Handle& h, SellTable& st, int M, int format) {
     const uint32_t max_seg = st.double_buffer ? double_seg : single_seg;
     st.nseg = (nb + max_seg - 1) / max_seg;
     if (st.nseg > 16) fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: more than 16 column segments");
-    if (2 * nn >= (1u << 14)) fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: +-W index exceeds 14 bits");
+    if (format == 1 && 2 * nn >= (1u << 14)) fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: +-W index exceeds 14 bits");
+    if (format == 2 && pair_count(n) >= (1u << 13))
+        fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: pair-ERI column exceeds 13 bits");
     // weight of a V/W bank conflict in the schedule: the scatter kernel reads
     // V once per output row (~8 per C gather on average)
     const int wv = format == 2 ? 8 : 1;
@@ -419,6 +436,8 @@ void build_mixed_sell(Handle& h, SellTable& st, int M, int format) {
     }
     std::vector<uint32_t> sell(std::max<uint64_t>(total, 1), 0);
     const std::vector<uint64_t>& bs = b.h_strings;
+    const std::vector<uint64_t>& bs_hi = b.h_strings_hi;
+    auto bstr = [&](uint32_t i) { return Bits(bs[i], bs_hi.empty() ? 0ull : bs_hi[i]); };
 
     #pragma omp parallel for schedule(dynamic, 4)
     for (int64_t sl = 0; sl < static_cast<int64_t>(nslices); ++sl) {
@@ -434,7 +453,7 @@ void build_mixed_sell(Handle& h, SellTable& st, int M, int format) {
                 for (uint32_t k = 0; k < deg[ib]; ++k) {
                     const uint32_t jb = flat[off[ib] + k];
                     if (jb / seg_cols != g) continue;
-                    const MixedMove mv = mixed_move(bs[ib], bs[jb], n);
+                    const MixedMove mv = mixed_move(bstr(ib), bstr(jb), n);
                     // format 2: the pair-ERI column tri(pb, qb) (V rows are
                     // pair-ERI rows); format 1: the +-W index
                     const uint32_t pcol = tri_index(static_cast<int>(mv.cd) / n, static_cast<int>(mv.cd) % n);
@@ -667,11 +686,11 @@ void build_diag(Handle& h) {
     EA.alloc(na);
     EB.alloc(nb);
     U.alloc(static_cast<size_t>(h.norbs) * nb);
-    k_string_energy<<<(na + 255) / 256, 256, 0, h.stream>>>(h.ch[0].strings.p, na, h.d_h1.p,
+    k_string_energy<<<(na + 255) / 256, 256, 0, h.stream>>>(h.ch[0].strings.p, h.ch[0].hi(), na, h.d_h1.p,
                                                             h.d_eri.p, h.norbs, EA.p);
-    k_string_energy<<<(nb + 255) / 256, 256, 0, h.stream>>>(h.ch[1].strings.p, nb, h.d_h1.p,
+    k_string_energy<<<(nb + 255) / 256, 256, 0, h.stream>>>(h.ch[1].strings.p, h.ch[1].hi(), nb, h.d_h1.p,
                                                             h.d_eri.p, h.norbs, EB.p);
-    k_u_table<<<dim3((nb + 255) / 256, h.norbs), 256, 0, h.stream>>>(h.ch[1].strings.p, nb,
+    k_u_table<<<dim3((nb + 255) / 256, h.norbs), 256, 0, h.stream>>>(h.ch[1].strings.p, h.ch[1].hi(), nb,
                                                                       h.d_eri.p, h.norbs, U.p);
     CUDA_LAUNCH_CHECK();
     const uint32_t nloc = static_cast<uint32_t>(h.nloc());
@@ -679,7 +698,8 @@ void build_diag(Handle& h) {
     for (uint32_t r0 = 0; r0 < nloc; r0 += 65535) {
         const uint32_t rows = std::min<uint32_t>(65535, nloc - r0);
         k_diag<<<dim3((nb + 255) / 256, rows), 256, 0, h.stream>>>(
-            h.ch[0].strings.p + h.a0 + r0, EA.p + h.a0 + r0, rows, EB.p, U.p, nb, h.core,
+            h.ch[0].strings.p + h.a0 + r0, h.ch[0].hi() ? h.ch[0].hi() + h.a0 + r0 : nullptr, EA.p + h.a0 + r0,
+            rows, EB.p, U.p, nb, h.core,
             h.diag.p + static_cast<size_t>(r0) * nb);
         CUDA_LAUNCH_CHECK();
     }
@@ -711,6 +731,8 @@ size_t estimate_bytes(const Handle& h) {
 const SellTable& mixed_table(Handle& h, int M) {
     const int idx = M == 1 ? 0 : (M == 2 ? 1 : 2);
     SellTable& t = h.sell_m[idx];
+    if (h.norbs > 64)   // its +-W tables hold one uint64 per string move
+        fail(DETCI_GPU_E_UNSUPPORTED, "mixed term: norbs > 64 runs on the scatter kernel only (M <= 2)");
     if (!t.built) build_mixed_sell(h, t, M, 1);
     return t;
 }

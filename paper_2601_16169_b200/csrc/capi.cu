@@ -194,31 +194,51 @@ void detci_gpu_destroy(detci_gpu_handle* hh) {
 
 int detci_gpu_set_strings(detci_gpu_handle* hh, int norbs, const uint64_t* alpha, size_t na,
                           const uint64_t* beta, size_t nb) {
+    return detci_gpu_set_strings_words(hh, norbs, 1, alpha, na, beta, nb);
+}
+
+int detci_gpu_set_strings_words(detci_gpu_handle* hh, int norbs, int words, const uint64_t* alpha, size_t na,
+                                const uint64_t* beta, size_t nb) {
     return guarded(hh, [&] {
         require(hh != nullptr, DETCI_GPU_E_INPUT, "set_strings: null handle");
         Handle& h = hh->h;
         require(norbs >= 1, DETCI_GPU_E_INPUT, "set_strings: norbs must be positive");
         // Reference limit is kMaxKernelBits = 256 spin-orbitals (basis.cpp:83-87);
-        // the device kernels hold one uint64 per channel string.
+        // the device strings are one or two uint64 words per channel.
         require(2 * norbs <= 256, DETCI_GPU_E_INPUT,
                 "build_basis: " + std::to_string(2 * norbs) + " spin-orbitals exceed the kernel limit of 256");
-        require(norbs <= 64, DETCI_GPU_E_UNSUPPORTED, "set_strings: norbs > 64 is not supported on the GPU path");
+        require(words == 1 || words == 2, DETCI_GPU_E_INPUT, "set_strings: words must be 1 or 2");
+        require(norbs <= 64 * words, DETCI_GPU_E_INPUT,
+                "set_strings: " + std::to_string(norbs) + " orbitals need " + std::to_string((norbs + 63) / 64) +
+                    " words per string");
+        require(norbs <= 64 || mixed_scatter_enabled(), DETCI_GPU_E_UNSUPPORTED,
+                "set_strings: norbs > 64 needs the scatter mixed kernel (DETCI_MIXED=gather is set)");
         require(h.have_ints == false || norbs == h.norbs, DETCI_GPU_E_INPUT,
                 "set_strings: norbs does not match the integrals");
         const char* names[2] = {"alpha", "beta"};
         const uint64_t* src[2] = {alpha, beta};
         const size_t cnt[2] = {na, nb};
-        const uint64_t allowed = norbs == 64 ? ~0ull : ((1ull << norbs) - 1);
+        // allowed bits per word
+        uint64_t allowed[2] = {0, 0};
+        for (int w = 0; w < 2; ++w) {
+            const int bits = std::max(0, std::min(64, norbs - 64 * w));
+            allowed[w] = bits == 64 ? ~0ull : ((1ull << bits) - 1);
+        }
+        const bool wide = norbs > 64;
         for (int c = 0; c < 2; ++c) {
             require(cnt[c] > 0 && src[c] != nullptr, DETCI_GPU_E_INPUT,
                     std::string("build_basis: empty ") + names[c] + " string list");
             require(cnt[c] < (1ull << 31), DETCI_GPU_E_UNSUPPORTED, "set_strings: more than 2^31 strings");
             int ne = -1;
             for (size_t i = 0; i < cnt[c]; ++i) {
-                require((src[c][i] & ~allowed) == 0, DETCI_GPU_E_INPUT,
-                        std::string("build_basis: ") + names[c] + " string " + std::to_string(i) +
-                            " has wrong orbital count");
-                const int pc = __builtin_popcountll(src[c][i]);
+                int pc = 0;
+                for (int w = 0; w < words; ++w) {
+                    const uint64_t x = src[c][i * words + w];
+                    require((x & ~allowed[w]) == 0, DETCI_GPU_E_INPUT,
+                            std::string("build_basis: ") + names[c] + " string " + std::to_string(i) +
+                                " has wrong orbital count");
+                    pc += __builtin_popcountll(x);
+                }
                 if (ne < 0) ne = pc;
                 require(pc == ne, DETCI_GPU_E_INPUT,
                         std::string("build_basis: inconsistent electron count in ") + names[c] +
@@ -232,15 +252,32 @@ int detci_gpu_set_strings(detci_gpu_handle* hh, int norbs, const uint64_t* alpha
         for (int c = 0; c < 2; ++c) {
             ChannelTables& t = h.ch[c];
             t.n = cnt[c];
-            t.h_strings.assign(src[c], src[c] + cnt[c]);
+            t.h_strings.resize(t.n);
+            t.h_strings_hi.assign(wide ? t.n : 0, 0ull);
+            for (size_t i = 0; i < t.n; ++i) {
+                t.h_strings[i] = src[c][i * words];
+                if (wide) t.h_strings_hi[i] = src[c][i * words + 1];
+            }
             t.strings.alloc(t.n);
-            copy_sync(t.strings.p, t.h_strings.data(), t.n * sizeof(uint64_t),
-                                  cudaMemcpyHostToDevice, h.stream);
+            copy_sync(t.strings.p, t.h_strings.data(), t.n * sizeof(uint64_t), cudaMemcpyHostToDevice, h.stream);
             // exclusive prefix parities P(s) for eps(A,B) = popc(A & P(B)) & 1
-            std::vector<uint64_t> pre(t.n);
-            for (size_t i = 0; i < t.n; ++i) pre[i] = prefix_parity(t.h_strings[i]);
+            std::vector<uint64_t> pre(t.n), pre_hi(wide ? t.n : 0);
+            for (size_t i = 0; i < t.n; ++i) {
+                const Bits p = prefix_parity(Bits(t.h_strings[i], wide ? t.h_strings_hi[i] : 0ull));
+                pre[i] = p.lo;
+                if (wide) pre_hi[i] = p.hi;
+            }
             t.prefix.alloc(t.n);
             copy_sync(t.prefix.p, pre.data(), t.n * sizeof(uint64_t), cudaMemcpyHostToDevice, h.stream);
+            if (wide) {
+                t.strings_hi.alloc(t.n);
+                t.prefix_hi.alloc(t.n);
+                copy_sync(t.strings_hi.p, t.h_strings_hi.data(), t.n * 8, cudaMemcpyHostToDevice, h.stream);
+                copy_sync(t.prefix_hi.p, pre_hi.data(), t.n * 8, cudaMemcpyHostToDevice, h.stream);
+            } else {
+                t.strings_hi.reset();
+                t.prefix_hi.reset();
+            }
         }
         h.have_strings = true;
     });

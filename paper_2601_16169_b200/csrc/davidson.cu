@@ -400,6 +400,192 @@ k_dav_stream(const StreamArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Register-dot variant of the fused passes (default for k <= 24).  Same
+// streams, same TMA ring, but one thread owns one element of the tile and
+// keeps every dot of the pass in registers (KMAX accumulators), so a tile
+// costs one barrier and 2k + 1 (Ritz) / k + 1 shared-memory loads per
+// element instead of the element phase + probe + warp-per-vector dot phase
+// (5k + 1 / 3k + 1 loads, three barriers).  The bulk copies of a stage are
+// issued by the 32 lanes of warp 0 (one elected thread issued ns copies
+// serially before).  Dots are reduced once per CTA at the end: per warp by
+// shuffles, then over warps in warp order into the per-CTA partials (fixed
+// order, so the solve stays bitwise reproducible).
+//   kPassOrth1 additionally reduces |cand|^2 into partial slot k, and
+//   kPassOrth2 writes cand / nu with nu^2 = |cand1|^2 - sum e_j^2 (exact for
+//   an orthonormal V; the host checks it against the directly reduced
+//   |cand2|^2 and rescales in the rare case they disagree), which removes
+//   the normalisation pass.
+// ---------------------------------------------------------------------------
+constexpr int kRsThreads = 256;
+
+template <int MODE, int KMAX>
+__global__ void __launch_bounds__(kRsThreads, 1)
+k_dav_stream_r(const StreamArgs a) {
+    constexpr int kWarps = kRsThreads / 32;
+    constexpr int kVals = 2 + 2 * KMAX;
+    const int kStStages = a.nst;
+    extern __shared__ __align__(16) double st_smem[];
+    __shared__ uint64_t bars[kStMaxStages];
+    __shared__ double s_coef[KMAX];
+    __shared__ double s_red[kWarps][kVals];
+    const uint32_t T = a.T;
+    const int ns = a.ns, k = a.k;
+    const uint32_t tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
+    const uint64_t ntiles = (a.n + T - 1) / T;
+    const uint32_t my_tiles = blockIdx.x < ntiles
+                                  ? static_cast<uint32_t>((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x)
+                                  : 0u;
+    auto tile_base = [&](uint32_t it) { return (static_cast<uint64_t>(it) * gridDim.x + blockIdx.x) * T; };
+    auto tile_cnt = [&](uint32_t it) { const uint64_t rem = a.n - tile_base(it); return static_cast<uint32_t>(rem < T ? rem : T); };
+    auto stage = [&](uint32_t st) { return st_smem + static_cast<size_t>(st) * ns * T; };
+    auto issue = [&](uint32_t it) {   // warp 0
+        const uint32_t st = it % kStStages, bytes = (tile_cnt(it) * 8u) & ~15u;
+        if (lane == 0) mbar_arrive_expect_tx(&bars[st], bytes * static_cast<uint32_t>(ns));
+        __syncwarp();
+        if (bytes)
+            for (int s = static_cast<int>(lane); s < ns; s += 32)
+                bulk_g2s(stage(st) + static_cast<size_t>(s) * T, a.s[s] + tile_base(it), bytes, &bars[st]);
+    };
+    if (tid == 0) {
+        for (int s = 0; s < kStStages; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    if (warp == 0)
+        for (uint32_t it = 0; it < my_tiles && it < static_cast<uint32_t>(kStStages); ++it) issue(it);
+    if (MODE == kPassOrth1 || MODE == kPassOrth2)
+        for (int j = tid; j < k; j += kRsThreads) s_coef[j] = a.coef[j];
+    __syncthreads();
+
+    double scale = 1.0;
+    if (MODE == kPassOrth1) scale = 1.0 / sqrt(*a.norm2);
+    if (MODE == kPassOrth2) {
+        // nu^2 = |cand1|^2 - sum_j e_j^2 (cand1 = this pass's input)
+        double e2 = 0.0;
+        for (int j = 0; j < k; ++j) e2 += s_coef[j] * s_coef[j];
+        const double nu2 = *a.norm2 - e2;
+        scale = nu2 > 0.0 ? 1.0 / sqrt(nu2) : 1.0;
+    }
+    double r1 = 0.0, r2 = 0.0;
+    double acc[KMAX], acc2[KMAX];
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) acc[j] = acc2[j] = 0.0;
+
+#pragma unroll 1
+    for (uint32_t it = 0; it < my_tiles; ++it) {
+        const uint32_t st = it % kStStages;
+        const uint32_t cnt = tile_cnt(it);
+        const uint64_t base = tile_base(it);
+        const double* const S = stage(st);
+        mbar_wait(&bars[st], (it / kStStages) & 1u);
+        if (cnt & 1u) {   // the bulk copies moved 16-byte multiples
+            if (static_cast<int>(tid) < ns)
+                const_cast<double*>(S)[static_cast<size_t>(tid) * T + cnt - 1] = a.s[tid][base + cnt - 1];
+            __syncthreads();
+        }
+        for (uint32_t i = tid; i < cnt; i += kRsThreads) {
+            if constexpr (MODE == kPassRitz) {
+                double vr[KMAX];
+                double r = 0.0, m = 0.0;
+#pragma unroll
+                for (int j = 0; j < KMAX; ++j)
+                    if (j < k) {
+                        vr[j] = S[static_cast<size_t>(j) * T + i];
+                        r = fma(a.c[j], vr[j], r);
+                        m = fma(a.c[j], S[static_cast<size_t>(k + j) * T + i], m);
+                    }
+                const double res = m - a.theta * r;
+                double denom = S[static_cast<size_t>(2 * k) * T + i] - a.theta;
+                if (fabs(denom) < 1e-8) denom = copysign(1e-8, denom);
+                const double cr = res / denom;
+                a.out[base + i] = cr;
+                r1 = fma(res, res, r1);
+                r2 = fma(cr, cr, r2);
+                const double last = S[static_cast<size_t>(k - 1) * T + i];
+#pragma unroll
+                for (int j = 0; j < KMAX; ++j)
+                    if (j < k) {
+                        acc[j] = fma(vr[j], cr, acc[j]);
+                        acc2[j] = fma(vr[j], last, acc2[j]);
+                    }
+            } else if constexpr (MODE == kPassProj) {
+                const double x = S[i];
+#pragma unroll
+                for (int j = 0; j < KMAX; ++j)
+                    if (j < k) acc[j] = fma(S[static_cast<size_t>(1 + j) * T + i], x, acc[j]);
+            } else {
+                double vr[KMAX];
+                double x = S[i];
+#pragma unroll
+                for (int j = 0; j < KMAX; ++j)
+                    if (j < k) {
+                        vr[j] = S[static_cast<size_t>(1 + j) * T + i];
+                        x = fma(-s_coef[j], vr[j], x);
+                    }
+                r2 = fma(x, x, r2);   // Orth1: |corr - sum d v|^2 (scaled below); Orth2: |cand2|^2
+                x *= scale;
+                a.out[base + i] = x;
+                if constexpr (MODE == kPassOrth1) {
+#pragma unroll
+                    for (int j = 0; j < KMAX; ++j)
+                        if (j < k) acc[j] = fma(vr[j], x, acc[j]);
+                }
+            }
+        }
+        __syncthreads();   // stage consumed
+        if (warp == 0 && it + kStStages < my_tiles) {
+            fence_proxy_async_smem();
+            issue(it + kStStages);
+        }
+    }
+    if (MODE == kPassOrth1) r2 *= scale * scale;
+
+    // Per-CTA partials, layout as k_dav_stream: kPassRitz [0] |res|^2,
+    // [1] |corr|^2, [2 + j] <v_j, corr>, [2 + k + j] <v_{k-1}, v_j>;
+    // kPassProj [j]; kPassOrth1 [j] and [k] |cand1|^2; kPassOrth2 [0] |cand2|^2.
+    auto wsum = [&](double v) {
+        for (int s = 16; s > 0; s >>= 1) v += __shfl_down_sync(0xffffffffu, v, s);
+        return v;
+    };
+    int nv = 0;
+    auto put = [&](int slot, double v) {
+        v = wsum(v);
+        if (lane == 0) s_red[warp][slot] = v;
+    };
+    if constexpr (MODE == kPassRitz) {
+        put(0, r1);
+        put(1, r2);
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j)
+            if (j < k) {
+                put(2 + j, acc[j]);
+                put(2 + k + j, acc2[j]);
+            }
+        nv = 2 + 2 * k;
+    } else if constexpr (MODE == kPassProj) {
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j)
+            if (j < k) put(j, acc[j]);
+        nv = k;
+    } else if constexpr (MODE == kPassOrth1) {
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j)
+            if (j < k) put(j, acc[j]);
+        put(k, r2);
+        nv = k + 1;
+    } else {
+        put(0, r2);
+        nv = 1;
+    }
+    __syncthreads();
+    for (int v = tid; v < nv; v += kRsThreads) {
+        double s = 0.0;
+        for (int w = 0; w < kWarps; ++w) s += s_red[w][v];
+        a.partial[static_cast<size_t>(v) * gridDim.x + blockIdx.x] = s;
+    }
+}
+
 __global__ void k_scale_div(double* __restrict__ x, uint64_t n, double divisor) {
     TILE_LOOP(i0, n) {
         double v[kU];
@@ -544,12 +730,44 @@ StreamCfg stream_cfg() {
     return c;
 }
 
+// DETCI_DAV_STREAM=warp: the warp-per-vector dot phase (k_dav_stream) for
+// every k; default: the register-dot kernel (k_dav_stream_r) for k <= 24.
+constexpr int kRsMaxK = 24;
+bool register_stream(int k) {
+    static const bool warp = [] {
+        const char* e = std::getenv("DETCI_DAV_STREAM");
+        return e && std::string(e) == "warp";
+    }();
+    return !warp && k <= kRsMaxK;
+}
+
 template <int MODE>
 void stream_pass(Handle& h, StreamArgs& a, int nred, int slot) {
     for (int s = 0; s < a.ns; ++s)
         if (reinterpret_cast<uintptr_t>(a.s[s]) & 15u) fail(DETCI_GPU_E_ERROR, "davidson: misaligned vector");
     static const StreamCfg cfg = stream_cfg();
     a.nst = cfg.stages;
+    if (register_stream(a.k)) {
+        a.T = static_cast<uint32_t>(std::min<size_t>(4096, kStSmem / 8 / (static_cast<size_t>(a.nst) * a.ns)) &
+                                    ~size_t{31});
+        if (a.T < 32) fail(DETCI_GPU_E_ERROR, "davidson: stream tile below 32 elements");
+        const size_t smem = static_cast<size_t>(a.nst) * a.ns * a.T * sizeof(double);
+        const int grid = sm_count();
+        a.partial = h.red.p;
+        auto go = [&](auto kern) {
+            ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
+            kern<<<grid, kRsThreads, smem, h.stream>>>(a);
+        };
+        if (a.k <= 8) go(&k_dav_stream_r<MODE, 8>);
+        else go(&k_dav_stream_r<MODE, kRsMaxK>);
+        CUDA_LAUNCH_CHECK();
+        if (nred > 0) {
+            k_finalize<<<nred, 32, 0, h.stream>>>(h.red.p, grid, nred, scalar_slot(h, slot));
+            CUDA_LAUNCH_CHECK();
+            allreduce_device(h, scalar_slot(h, slot), nred);
+        }
+        return;
+    }
     const size_t per = static_cast<size_t>(a.nst) * a.ns + 1;   // doubles per tile element (stages + probe)
     a.T = static_cast<uint32_t>(std::min<size_t>(4096, kStSmem / cfg.ctas / 8 / per) & ~size_t{31});
     if (a.T < 32) fail(DETCI_GPU_E_ERROR, "davidson: stream tile below 32 elements");
@@ -931,6 +1149,7 @@ void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* re
         // V[k_sub] (orthonormalize, davidson.cpp:43-57)
         double* cand = V(k_sub);
         double nrm2 = 0.0;
+        bool prenormalised = false;
         if (ortho_mgs()) {
             // the reference's 2-pass modified Gram-Schmidt, one projection per kernel
             const int steps = 2 * k_sub;
@@ -957,11 +1176,32 @@ void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* re
             oa.coef = scalar_slot(h, kSlotRitz + 2);
             oa.norm2 = scalar_slot(h, kSlotRitz + 1);
             oa.out = cand;
-            stream_pass<kPassOrth1>(h, oa, k, kSlotOrth1);
+            const bool reg = register_stream(k);
+            // the register kernel also reduces |cand1|^2 (slot k) and
+            // writes the normalised candidate in pass 2
+            stream_pass<kPassOrth1>(h, oa, reg ? k + 1 : k, kSlotOrth1);
             oa.s[0] = cand;
             oa.coef = scalar_slot(h, kSlotOrth1);
+            oa.norm2 = scalar_slot(h, kSlotOrth1 + k);
             stream_pass<kPassOrth2>(h, oa, 1, kSlotOrth2);
-            read_slots(h, kSlotOrth2, 1, &nrm2);
+            if (reg) {
+                std::vector<double> sl(k + 1);
+                read_slots(h, kSlotOrth1, k + 1, sl.data());
+                read_slots(h, kSlotOrth2, 1, &nrm2);
+                double nu2 = sl[k];
+                for (int j = 0; j < k; ++j) nu2 -= sl[j] * sl[j];
+                const double nu_a = nu2 > 0.0 ? std::sqrt(nu2) : 1.0;
+                const double nu_d = std::sqrt(nrm2);
+                // cand holds cand2 / nu_a; the reference divides by the
+                // directly computed norm (davidson.cpp:54-56)
+                if (nu_d >= 1e-10 && std::fabs(nu_a / nu_d - 1.0) > 1e-12) {
+                    k_scale_div<<<vgrid, kRedThreads, 0, h.stream>>>(cand, n, nu_d / nu_a);
+                    CUDA_LAUNCH_CHECK();
+                }
+                prenormalised = true;
+            } else {
+                read_slots(h, kSlotOrth2, 1, &nrm2);
+            }
         } else {
             // classical Gram-Schmidt twice ("twice is enough"): each pass is
             // one multi-dot and one fused update, 2k + 3 vector passes
@@ -976,8 +1216,10 @@ void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* re
             status = 2;
             break;
         }
-        k_scale_div<<<vgrid, kRedThreads, 0, h.stream>>>(cand, n, norm);
-        CUDA_LAUNCH_CHECK();
+        if (!prenormalised) {
+            k_scale_div<<<vgrid, kRedThreads, 0, h.stream>>>(cand, n, norm);
+            CUDA_LAUNCH_CHECK();
+        }
         ++k_sub;
     }
 

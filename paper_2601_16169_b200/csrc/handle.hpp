@@ -76,6 +76,13 @@ struct ChannelTables {
     std::vector<uint64_t> h_strings;
     DevBuf<uint64_t> strings;
     DevBuf<uint64_t> prefix;           // prefix_parity(strings[i]) (eps sign)
+    // norbs > 64: orbitals 64..127 of each string and of its prefix parity
+    // (empty otherwise; kernels read them through load_bits)
+    std::vector<uint64_t> h_strings_hi;
+    DevBuf<uint64_t> strings_hi;
+    DevBuf<uint64_t> prefix_hi;
+    const uint64_t* hi() const { return strings_hi.p; }
+    const uint64_t* prefix_hi_p() const { return prefix_hi.p; }
     // kind 0 = singles, 1 = doubles
     DevBuf<uint32_t> flat[2];
     DevBuf<uint64_t> offset[2];
@@ -257,5 +264,18 @@ double smallest_eigenpair(const std::vector<double>& lower, int ld, int k, std::
 void jacobi_eigen(const std::vector<double>& lower, int ld, int k, std::vector<double>& evals,
                   std::vector<double>& vecs);
 void davidson_roots_device(Handle& h, const detci_dav_block_opts& opts, detci_dav_block_result* res);
+
+// Strings of the eps sign eps(A_r, B_c) for local rows from `row` on: alpha
+// strings and beta prefix parities, high words null for norbs <= 64.
+struct EpsRows {
+    const uint64_t* a;
+    const uint64_t* a_hi;
+    const uint64_t* b;
+    const uint64_t* b_hi;
+};
+inline EpsRows eps_rows(const Handle& h, uint64_t row) {
+    return EpsRows{h.ch[0].strings.p + row, h.ch[0].hi() ? h.ch[0].hi() + row : nullptr, h.ch[1].prefix.p,
+                   h.ch[1].prefix_hi_p()};
+}
 
 } // namespace detci_gpu

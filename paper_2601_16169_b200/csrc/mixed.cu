@@ -255,6 +255,7 @@ struct ScatterArgs {
     const uint2* items;         // (ja, kbeg | cnt << 24)
     uint32_t nparts, nslices, nb, seg_cols, nseg, vpitch;
     const uint64_t* alpha;
+    const uint64_t* alpha_hi;   // norbs > 64 (else null)
     const uint32_t* sa_flat;
     const uint64_t* sa_off;
     const uint32_t* tpos;
@@ -275,11 +276,11 @@ struct ScatterArgs {
 // matrix: V[tri(pb, qb)] = (pa qa|pb qb).
 __device__ __forceinline__ void scatter_row(const ScatterArgs& a, uint32_t ja, uint64_t oja, uint32_t pos,
                                             uint64_t& vr, uint64_t& dr) {
-    const uint64_t Aj = a.alpha[ja];
+    const Bits Aj = load_bits(a.alpha, a.alpha_hi, ja);
     const uint32_t ia = a.sa_flat[oja + pos];
-    const uint64_t Ak = a.alpha[ia];
-    const int pa = __ffsll(static_cast<long long>(Ak & ~Aj)) - 1;
-    const int qa = __ffsll(static_cast<long long>(Aj & ~Ak)) - 1;
+    const Bits Ak = load_bits(a.alpha, a.alpha_hi, ia);
+    const int pa = lowest(Ak & ~Aj);
+    const int qa = lowest(Aj & ~Ak);
     vr = static_cast<uint64_t>(tri_index(pa, qa)) * a.vpitch |
          static_cast<uint64_t>(mixed_alpha_parity(Ak, pa, qa)) << 63;
     dr = a.w_lo ? a.w_base[ia] + a.tpos[oja + pos] - a.w_lo[ia] : a.sa_off[ia] + a.tpos[oja + pos] - a.d_base;
@@ -417,7 +418,7 @@ __device__ __forceinline__ void scatter_pass(const ScatterArgs& a, double* vsub,
 #pragma unroll
             for (int v = 0; v < M; ++v)
                 c[v] = xor_sign(*reinterpret_cast<const double*>(cbv[v] + co), e & 0x80000000u);
-            const char* vp = vb + ((e >> 15) & 0x7ff8u);
+            const char* vp = vb + ((e >> 15) & 0xfff8u);
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 const double w = *reinterpret_cast<const double*>(vp + k * vstride);
@@ -536,6 +537,8 @@ struct ReduceArgs {
     const uint32_t* sa_len;
     const uint64_t* alpha;
     const uint64_t* beta_prefix;
+    const uint64_t* alpha_hi;         // norbs > 64 (else null)
+    const uint64_t* beta_prefix_hi;
     const uint32_t* perm;
     double* Y;                  // row ia at Y + (ia - y_row0) * ldy (accumulate, by perm)
     size_t ldy;
@@ -583,7 +586,8 @@ k_mixed_reduce(const ReduceArgs a) {
     }
     for (; p < hi; ++p) s += __ldcs(d + static_cast<size_t>(p - lo) * a.ldd);
     const uint32_t ib = a.perm[slot];
-    const uint32_t flip = static_cast<uint32_t>(__popcll(a.alpha[ia] & a.beta_prefix[ib]));
+    const uint32_t flip = static_cast<uint32_t>(
+        eps_parity(load_bits(a.alpha, a.alpha_hi, ia), load_bits(a.beta_prefix, a.beta_prefix_hi, ib)));
     if (a.T) {
         double& t = a.T[static_cast<size_t>(ia - a.y_row0) * a.ldt + (slot - a.slot0)];
         t = a.t_accumulate ? t + flip_sign(s, flip) : flip_sign(s, flip);
@@ -827,6 +831,7 @@ void launch_mixed_scatter(Handle& h, int g, int P, int b, const Ptrs& Cb, uint32
         a.nseg = t.nseg;
         a.vpitch = vpitch;
         a.alpha = h.ch[0].strings.p;
+        a.alpha_hi = h.ch[0].hi();
         a.sa_flat = h.ch[0].flat[0].p;
         a.sa_off = h.ch[0].offset[0].p;
         a.tpos = h.tpos.p;
@@ -879,6 +884,8 @@ void launch_mixed_scatter(Handle& h, int g, int P, int b, const Ptrs& Cb, uint32
             r.sa_len = h.ch[0].len[0].p;
             r.alpha = a.alpha;
             r.beta_prefix = h.ch[1].prefix.p;
+            r.alpha_hi = a.alpha_hi;
+            r.beta_prefix_hi = h.ch[1].prefix_hi_p();
             r.perm = h.sell_perm.p;
             r.Y = y_loc[v];
             r.ldy = h.nb();

@@ -39,10 +39,11 @@ struct SSR {
 // Epilogue shared by both same-spin variants: eps sign, then write,
 // accumulate, or diag * Cself + acc.
 template <int M>
-__device__ __forceinline__ void samespin_store(const SameSpinArgs& a, uint64_t arow, uint32_t r, uint32_t c,
+__device__ __forceinline__ void samespin_store(const SameSpinArgs& a, Bits arow, uint32_t r, uint32_t c,
                                                const double (&acc)[M]) {
     const size_t yi = static_cast<size_t>(r) * a.ldy + c;
-    const uint32_t flip = a.eps_row ? static_cast<uint32_t>(__popcll(arow & a.eps_col[c])) : 0u;
+    const uint32_t flip =
+        a.eps_row ? static_cast<uint32_t>(eps_parity(arow, load_bits(a.eps_col, a.eps_col_hi, c))) : 0u;
 #pragma unroll
     for (int vv = 0; vv < M; ++vv) {
         const double v = flip_sign(acc[vv], flip);
@@ -146,7 +147,7 @@ k_samespin(const SameSpinArgs a, uint32_t chunk0) {
         }
     }
 
-    const uint64_t arow = a.eps_row ? a.eps_row[row] : 0;
+    const Bits arow = a.eps_row ? load_bits(a.eps_row, a.eps_row_hi, row) : Bits();
 #pragma unroll
     for (int q = 0; q < R; ++q) {
         const uint32_t c = col0 + q * kSSBlock;
@@ -294,7 +295,7 @@ k_samespin_g(const SameSpinArgs a, uint32_t chunk0, uint32_t ngroups) {
         }
     }
 
-    const uint64_t arow = a.eps_row ? a.eps_row[row] : 0;
+    const Bits arow = a.eps_row ? load_bits(a.eps_row, a.eps_row_hi, row) : Bits();
 #pragma unroll
     for (int q = 0; q < R; ++q) {
         const uint32_t c = kV2 ? chunk * (kWarp * R) + (q / 2) * 2 * kWarp + 2 * lane + (q % 2) : col0 + q * kWarp;
@@ -411,6 +412,8 @@ void launch_alpha(const Handle& h, const Ptrs& Cb, uint32_t b0, uint32_t b1, con
     fill_lists(s, h.ch[0]);
     s.eps_row = h.ch[0].strings.p;
     s.eps_col = h.ch[1].prefix.p;
+    s.eps_row_hi = h.ch[0].hi();
+    s.eps_col_hi = h.ch[1].prefix_hi_p();
     s.diag = first ? h.diag.p + (a0 - h.a0) * h.nb() : nullptr;
     s.accumulate = (first && !add_to_y) ? 0 : 1;   // first && add_to_y: y += diag*C + alpha
     launch_samespin<M>(s, h.stream);

@@ -57,19 +57,22 @@ constexpr int kTile = 32;
 //   xs[r * ldx + c] = eps x      (if xs)     xsT[c * ldt + r] = eps x (if xsT)
 __global__ void k_eps_transpose(const double* __restrict__ x, size_t ldx, double* __restrict__ xs,
                                 double* __restrict__ xsT, size_t ldt, uint32_t rows, uint32_t cols,
-                                const uint64_t* __restrict__ a_str, const uint64_t* __restrict__ b_pre) {
+                                const EpsRows e) {
     __shared__ double tile[kTile][kTile + 1];
-    __shared__ uint64_t s_a[kTile];
+    __shared__ uint64_t s_a[2][kTile];
     const uint32_t c0 = blockIdx.x * kTile, r0 = blockIdx.y * kTile;
     const uint32_t cc = c0 + threadIdx.x;
-    const uint64_t pb = cc < cols ? b_pre[cc] : 0;
-    if (threadIdx.y == 0 && r0 + threadIdx.x < rows) s_a[threadIdx.x] = a_str[r0 + threadIdx.x];
+    const Bits pb = cc < cols ? load_bits(e.b, e.b_hi, cc) : Bits();
+    if (threadIdx.y == 0 && r0 + threadIdx.x < rows) {
+        s_a[0][threadIdx.x] = e.a[r0 + threadIdx.x];
+        s_a[1][threadIdx.x] = e.a_hi ? e.a_hi[r0 + threadIdx.x] : 0ull;
+    }
     __syncthreads();
     for (uint32_t y = threadIdx.y; y < kTile; y += blockDim.y) {
         const uint32_t rr = r0 + y;
         if (rr < rows && cc < cols) {
             const size_t i = static_cast<size_t>(rr) * ldx + cc;
-            const double v = flip_sign(x[i], static_cast<uint32_t>(__popcll(s_a[y] & pb)));
+            const double v = flip_sign(x[i], static_cast<uint32_t>(eps_parity(Bits(s_a[0][y], s_a[1][y]), pb)));
             if (xs) xs[i] = v;
             tile[y][threadIdx.x] = v;
         }
@@ -85,23 +88,26 @@ __global__ void k_eps_transpose(const double* __restrict__ x, size_t ldx, double
 // dst[r * ldd + c] += eps(a_str[r], b_pre[c]) src[c * lds + r], dst rows x cols
 __global__ void k_transpose_add_eps(const double* __restrict__ src, size_t lds, double* __restrict__ dst,
                                     size_t ldd, uint32_t rows, uint32_t cols,
-                                    const uint64_t* __restrict__ a_str, const uint64_t* __restrict__ b_pre) {
+                                    const EpsRows e) {
     __shared__ double tile[kTile][kTile + 1];
-    __shared__ uint64_t s_a[kTile];
+    __shared__ uint64_t s_a[2][kTile];
     const uint32_t c0 = blockIdx.x * kTile, r0 = blockIdx.y * kTile;
     for (uint32_t y = threadIdx.y; y < kTile; y += blockDim.y) {
         const uint32_t c = c0 + y, rr = r0 + threadIdx.x;
         if (rr < rows && c < cols) tile[y][threadIdx.x] = src[static_cast<size_t>(c) * lds + rr];
     }
-    if (threadIdx.y == 0 && r0 + threadIdx.x < rows) s_a[threadIdx.x] = a_str[r0 + threadIdx.x];
+    if (threadIdx.y == 0 && r0 + threadIdx.x < rows) {
+        s_a[0][threadIdx.x] = e.a[r0 + threadIdx.x];
+        s_a[1][threadIdx.x] = e.a_hi ? e.a_hi[r0 + threadIdx.x] : 0ull;
+    }
     __syncthreads();
     const uint32_t cc = c0 + threadIdx.x;
-    const uint64_t pb = cc < cols ? b_pre[cc] : 0;
+    const Bits pb = cc < cols ? load_bits(e.b, e.b_hi, cc) : Bits();
     for (uint32_t y = threadIdx.y; y < kTile; y += blockDim.y) {
         const uint32_t rr = r0 + y;
         if (rr < rows && cc < cols)
             dst[static_cast<size_t>(rr) * ldd + cc] +=
-                flip_sign(tile[threadIdx.x][y], static_cast<uint32_t>(__popcll(s_a[y] & pb)));
+                flip_sign(tile[threadIdx.x][y], static_cast<uint32_t>(eps_parity(Bits(s_a[0][y], s_a[1][y]), pb)));
     }
 }
 
@@ -137,7 +143,7 @@ void eps_prologue(Handle& h, const Ptrs& x_loc, const MPtrs& xs_loc, bool transp
     dim3 tb(kTile, 8), tg((nb + kTile - 1) / kTile, (nloc + kTile - 1) / kTile);
     for (int v = 0; v < M; ++v) {
         k_eps_transpose<<<tg, tb, 0, h.stream>>>(x_loc[v], nb, xs_loc[v], transpose ? h.ct.p + v * block : nullptr,
-                                                 nloc, nloc, nb, h.ch[0].strings.p + a0, h.ch[1].prefix.p);
+                                                 nloc, nloc, nb, eps_rows(h, a0));
         CUDA_LAUNCH_CHECK();
     }
 }
@@ -178,7 +184,7 @@ void combine(Handle& h, const MPtrs& y_loc, uint64_t a0, uint64_t a1, PhaseTimer
     dim3 tb(kTile, 8), tg((nb + kTile - 1) / kTile, (nloc + kTile - 1) / kTile);
     for (int v = 0; v < M; ++v) {
         k_transpose_add_eps<<<tg, tb, 0, h.stream>>>(h.yt.p + v * block, nloc, y_loc[v], nb, nloc, nb,
-                                                     h.ch[0].strings.p + a0, h.ch[1].prefix.p);
+                                                     eps_rows(h, a0));
         CUDA_LAUNCH_CHECK();
     }
     tm.end(id);
@@ -575,8 +581,7 @@ bool sigma_host_pipelined(Handle& h, const double* x, double* y, detci_gpu_timin
         const uint32_t rc = static_cast<uint32_t>(r1 - r0);
         dim3 tb(kTile, 8), tg(static_cast<unsigned>((nb + kTile - 1) / kTile), (rc + kTile - 1) / kTile);
         k_eps_transpose<<<tg, tb, 0, h.stream>>>(dx + r0 * nb, nb, h.xs.p + r0 * nb, h.ct.p + r0, nloc, rc,
-                                                 static_cast<uint32_t>(nb), h.ch[0].strings.p + a0 + r0,
-                                                 h.ch[1].prefix.p);
+                                                 static_cast<uint32_t>(nb), eps_rows(h, a0 + r0));
         CUDA_LAUNCH_CHECK();
         SameSpinArgs s{};
         s.C[0] = h.ct.p + r0;
@@ -629,8 +634,7 @@ bool sigma_host_pipelined(Handle& h, const double* x, double* y, detci_gpu_timin
             const uint32_t rc = static_cast<uint32_t>(r1 - r0);
             dim3 tb(kTile, 8), tg(static_cast<unsigned>((nb + kTile - 1) / kTile), (rc + kTile - 1) / kTile);
             k_transpose_add_eps<<<tg, tb, 0, h.stream>>>(h.yt.p + r0, nloc, dy + r0 * nb, nb, rc,
-                                                         static_cast<uint32_t>(nb), h.ch[0].strings.p + a0 + r0,
-                                                         h.ch[1].prefix.p);
+                                                         static_cast<uint32_t>(nb), eps_rows(h, a0 + r0));
             CUDA_LAUNCH_CHECK();
         }
         launch_mixed_scatter<1>(h, 0, 1, 0, held, 0, static_cast<uint32_t>(h.na()), yl, a0, 2, a0 + r0, a0 + r1, wi);

@@ -99,6 +99,8 @@ struct SameSpinArgs {
     const uint32_t* pab;
     const uint64_t* eps_row;  // if set: output *= eps(eps_row[row], eps_col[col])
     const uint64_t* eps_col;
+    const uint64_t* eps_row_hi;   // norbs > 64: high words (else null)
+    const uint64_t* eps_col_hi;
     const double* diag;       // if set (write mode): Y = diag * Cself + acc
     const double* Cself[kMaxM];
     int accumulate;

@@ -56,6 +56,9 @@ struct StoredFillArgs {
     const uint64_t* sa;   // alpha strings
     const uint64_t* sb;   // beta strings
     const uint64_t* pb;   // prefix parities of the beta strings (eps)
+    const uint64_t* sa_hi;   // norbs > 64: high words (else null)
+    const uint64_t* sb_hi;
+    const uint64_t* pb_hi;
     // [channel][kind] helper lists and same-spin pair tables
     const uint32_t* flat[2][2];
     const uint64_t* off[2][2];
@@ -70,7 +73,7 @@ struct StoredFillArgs {
     double* value;
 };
 
-__device__ __forceinline__ int eps_of(uint64_t a, uint64_t pb) { return __popcll(a & pb) & 1; }
+__device__ __forceinline__ int eps_of(Bits a, Bits pb) { return eps_parity(a, pb); }
 
 // One warp per row (grid-strided over rows).
 __global__ void __launch_bounds__(256) k_stored_fill(const StoredFillArgs a) {
@@ -81,7 +84,8 @@ __global__ void __launch_bounds__(256) k_stored_fill(const StoredFillArgs a) {
     for (uint64_t I = blockIdx.x * static_cast<uint64_t>(blockDim.x / kWarp) + threadIdx.x / kWarp; I < dim;
          I += warps) {
         const uint32_t ia = static_cast<uint32_t>(I / a.nb), ib = static_cast<uint32_t>(I % a.nb);
-        const uint64_t A = a.sa[ia], B = a.sb[ib], PB = a.pb[ib];
+        const Bits A = load_bits(a.sa, a.sa_hi, ia), B = load_bits(a.sb, a.sb_hi, ib),
+                   PB = load_bits(a.pb, a.pb_hi, ib);
         const int eI = eps_of(A, PB);
         uint64_t at = a.row_offset[I];
         if (lane == 0) {
@@ -106,7 +110,7 @@ __global__ void __launch_bounds__(256) k_stored_fill(const StoredFillArgs a) {
                     const double j = a.J[1][static_cast<size_t>(ab & 0x7fffffffu) * a.nb + ib];
                     v += (ab >> 31) ? -j : j;
                 }
-                const int s = eI ^ eps_of(a.sa[ja], PB);
+                const int s = eI ^ eps_of(load_bits(a.sa, a.sa_hi, ja), PB);
                 a.col[at + pos] = static_cast<uint32_t>(static_cast<uint64_t>(ja) * a.nb + ib);
                 a.value[at + pos] = s ? -v : v;
             }
@@ -129,7 +133,7 @@ __global__ void __launch_bounds__(256) k_stored_fill(const StoredFillArgs a) {
                     const double j = a.J[0][static_cast<size_t>(ab & 0x7fffffffu) * a.na + ia];
                     v += (ab >> 31) ? -j : j;
                 }
-                const int s = eI ^ eps_of(A, a.pb[jb]);
+                const int s = eI ^ eps_of(A, load_bits(a.pb, a.pb_hi, jb));
                 a.col[at + pos] = static_cast<uint32_t>(static_cast<uint64_t>(ia) * a.nb + jb);
                 a.value[at + pos] = s ? -v : v;
             }
@@ -143,12 +147,12 @@ __global__ void __launch_bounds__(256) k_stored_fill(const StoredFillArgs a) {
             for (uint32_t t = lane; t < nsa * nsb; t += kWarp) {
                 const uint32_t ka = t / nsb, kb = t - ka * nsb;
                 const uint32_t ja = fa[ka], jb = fb[kb];
-                const uint64_t Aj = a.sa[ja];
-                const int pa = ctz64(A & ~Aj), qa = ctz64(Aj & ~A);
-                const MixedMove mv = mixed_move(B, a.sb[jb], n);
+                const Bits Aj = load_bits(a.sa, a.sa_hi, ja);
+                const int pa = lowest(A & ~Aj), qa = lowest(Aj & ~A);
+                const MixedMove mv = mixed_move(B, load_bits(a.sb, a.sb_hi, jb), n);
                 const int c = static_cast<int>(mv.cd) / n, d = static_cast<int>(mv.cd) % n;
                 const double v = mixed_weight(a.eri, n, pa, qa, c, d);
-                const int s = static_cast<int>(mv.sbit) ^ mixed_alpha_parity(A, pa, qa) ^ eI ^ eps_of(Aj, a.pb[jb]);
+                const int s = static_cast<int>(mv.sbit) ^ mixed_alpha_parity(A, pa, qa) ^ eI ^ eps_of(Aj, load_bits(a.pb, a.pb_hi, jb));
                 a.col[at + t] = static_cast<uint32_t>(static_cast<uint64_t>(ja) * a.nb + jb);
                 a.value[at + t] = s ? -v : v;
             }
@@ -221,6 +225,9 @@ void build_stored(Handle& h, uint64_t budget, uint64_t* nnz_out) {
     a.sa = h.ch[0].strings.p;
     a.sb = h.ch[1].strings.p;
     a.pb = h.ch[1].prefix.p;
+    a.sa_hi = h.ch[0].hi();
+    a.sb_hi = h.ch[1].hi();
+    a.pb_hi = h.ch[1].prefix_hi_p();
     for (int c = 0; c < 2; ++c) {
         for (int k = 0; k < 2; ++k) {
             a.flat[c][k] = h.ch[c].flat[k].p;

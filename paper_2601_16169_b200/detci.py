@@ -31,6 +31,21 @@ def _u64(a) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(a, dtype=np.uint64))
 
 
+def _string_words(a, norbs: int) -> np.ndarray:
+    """Channel strings as uint64 words: shape (n,) for norbs <= 64, (n, 2)
+    for norbs <= 128 (word w = orbitals 64w..64w+63, the BitString word
+    order, bitstring.hpp:33-51).  Accepts Python ints of any size or an
+    (n, 2) uint64 array."""
+    if norbs <= 64:
+        return _u64(a)
+    if isinstance(a, np.ndarray) and a.ndim == 2:
+        if a.shape[1] != 2:
+            raise InputError("strings: expected an (n, 2) uint64 array for norbs > 64")
+        return _u64(a)
+    mask = (1 << 64) - 1
+    return _u64([[int(x) & mask, int(x) >> 64] for x in a]).reshape(-1, 2)
+
+
 def _f64(a) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
 
@@ -109,12 +124,14 @@ class GpuBasis:
         else:
             self._check(self._lib.detci_gpu_create(C.byref(desc), C.byref(self._h)), use_handle=False)
         self.norbs = int(norbs)
-        self.alpha = _u64(alpha)
-        self.beta = _u64(beta)
+        self.alpha = _string_words(alpha, self.norbs)
+        self.beta = _string_words(beta, self.norbs)
         self.n_alpha = len(self.alpha)
         self.n_beta = len(self.beta)
-        self._check(self._lib.detci_gpu_set_strings(self._h, self.norbs, _ptr(self.alpha, C.c_uint64),
-                                                    self.n_alpha, _ptr(self.beta, C.c_uint64), self.n_beta))
+        words = 1 if self.alpha.ndim == 1 else 2
+        self._check(self._lib.detci_gpu_set_strings_words(self._h, self.norbs, words,
+                                                          _ptr(self.alpha, C.c_uint64), self.n_alpha,
+                                                          _ptr(self.beta, C.c_uint64), self.n_beta))
         h1 = _f64(h1).reshape(-1)
         eri = _f64(eri).reshape(-1)
         if h1.size != norbs ** 2 or eri.size != norbs ** 4:
