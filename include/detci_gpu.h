@@ -324,6 +324,13 @@ int detci_gpu_factorized_element(int norbs, double core, const double* h1, const
                                  uint64_t bra_alpha, uint64_t bra_beta, uint64_t ket_alpha,
                                  uint64_t ket_beta, double* out);
 
+/* The same for strings of `words` (1 or 2) uint64 each (norbs <= 128, word
+ * order as detci_gpu_set_strings_words). */
+int detci_gpu_factorized_element_words(int norbs, int words, double core, const double* h1,
+                                       const double* eri, const uint64_t* bra_alpha,
+                                       const uint64_t* bra_beta, const uint64_t* ket_alpha,
+                                       const uint64_t* ket_beta, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -74,6 +74,7 @@ class RefLib:
                                        C.POINTER(vp)]
         L.ref_basis_create_words.argtypes = [vp, C.c_int, u64p, C.c_long, u64p, C.c_long, C.c_int, C.c_int,
                                              C.c_uint64, C.c_int, C.POINTER(vp)]
+        L.ref_hij_words.argtypes = [vp, C.c_int, u64p, u64p, u64p, u64p, dp]
         L.ref_basis_free.argtypes = [vp]
         L.ref_basis_stats.argtypes = [vp, dp, C.POINTER(C.c_int)]
         L.ref_basis_diag.argtypes = [vp, dp]
@@ -189,6 +190,14 @@ class RefTable:
     def hij(self, bra_a, bra_b, ket_a, ket_b, bit_length=0) -> float:
         out = C.c_double()
         self.ref.check(self.ref.lib.ref_hij(self.h, bra_a, bra_b, ket_a, ket_b, bit_length, C.byref(out)))
+        return out.value
+
+    def hij_words(self, bra_a, bra_b, ket_a, ket_b) -> float:
+        """Reference hij for Python-int strings of up to 128 orbitals."""
+        mask = (1 << 64) - 1
+        arrs = [np.array([x & mask, x >> 64], dtype=np.uint64) for x in (bra_a, bra_b, ket_a, ket_b)]
+        out = C.c_double()
+        self.ref.check(self.ref.lib.ref_hij_words(self.h, 2, *[_p(a, C.c_uint64) for a in arrs], C.byref(out)))
         return out.value
 
     def brute_force_hij(self, bra_a, bra_b, ket_a, ket_b) -> float:

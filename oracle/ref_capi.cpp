@@ -93,7 +93,7 @@ BitString words_to_string(const std::uint64_t* w, int words, int norbs) {
     std::vector<int> occ;
     for (int i = 0; i < norbs && i < 64 * words; ++i)
         if ((w[i / 64] >> (i % 64)) & 1u) occ.push_back(i);
-    return from_occupied(occ, make_packing(norbs, norbs));
+    return from_occupied(occ, make_packing(norbs, std::min(norbs, 64)));
 }
 
 std::uint64_t string_to_mask(const BitString& s) {
@@ -494,6 +494,23 @@ int ref_hij(void* tp, std::uint64_t bra_a, std::uint64_t bra_b, std::uint64_t ke
 }
 
 // Oracle element (explicit second quantization, oracle.cpp:70-126).
+// ref_hij for strings of `words` uint64 each (norbs <= 128), interleaved at
+// bit_length 64 (multi-word determinants).
+int ref_hij_words(void* tp, int words, const std::uint64_t* bra_a, const std::uint64_t* bra_b,
+                  const std::uint64_t* ket_a, const std::uint64_t* ket_b, double* out) {
+    GUARD({
+        const auto* t = static_cast<IntegralTable*>(tp);
+        const int n = t->norbs();
+        const int bl = std::min(64, 2 * n);
+        const BitString ba = repack(words_to_string(bra_a, words, n), bl);
+        const BitString bb = repack(words_to_string(bra_b, words, n), bl);
+        const BitString ka = repack(words_to_string(ket_a, words, n), bl);
+        const BitString kb = repack(words_to_string(ket_b, words, n), bl);
+        const DirectExchange jk = build_direct_exchange(*t);
+        *out = hij(interleave(ba, bb), interleave(ka, kb), *t, jk);
+    })
+}
+
 int ref_brute_force_hij(void* tp, std::uint64_t bra_a, std::uint64_t bra_b, std::uint64_t ket_a,
                         std::uint64_t ket_b, double* out) {
     GUARD({

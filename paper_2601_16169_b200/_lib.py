@@ -151,6 +151,10 @@ SIGNATURES = {
         C.c_int,
         [C.c_int, C.c_double, dp, dp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, dp],
     ),
+    "detci_gpu_factorized_element_words": (
+        C.c_int,
+        [C.c_int, C.c_int, C.c_double, dp, dp, u64p, u64p, u64p, u64p, dp],
+    ),
     "detci_gpu_plan_partition": (
         C.c_int,
         [C.c_uint64, C.c_uint64, u32p, u32p, u32p, u32p, C.c_int, C.c_int, u64p],

@@ -86,14 +86,68 @@ __global__ void k_div(double* __restrict__ y, uint64_t n, double a) {
         y[i] /= a;
 }
 
-double host_j(const double* eri, int n, int p, int q, uint64_t spec) {
+double host_j(const double* eri, int n, int p, int q, Bits spec) {
     double acc = 0.0;
-    while (spec) {
-        const int r = __builtin_ctzll(spec);
-        spec &= spec - 1;
+    while (any(spec)) {
+        const int r = lowest(spec);
+        spec = drop_lowest(spec);
         acc += eri_at(eri, n, p, q, r, r);
     }
     return acc;
+}
+
+// <bra|H|ket> from the kernels' factorized forms (detci_gpu_factorized_element).
+double factorized_element_bits(int norbs, double core, const double* h1, const double* eri, Bits bra_a,
+                               Bits bra_b, Bits ket_a, Bits ket_b) {
+    const int da = popc(bra_a ^ ket_a) / 2;
+    const int db = popc(bra_b ^ ket_b) / 2;
+    require(popc(bra_a) == popc(ket_a) && popc(bra_b) == popc(ket_b), DETCI_GPU_E_INPUT,
+            "factorized_element: spin-nonconserving pair");
+    if (da + db > 2) return 0.0;
+    if (da == 0 && db == 0) {  // diagonal, regrouped as in k_diag
+        auto energy = [&](Bits s) {
+            double acc = 0.0;
+            for (Bits a = s; any(a);) {
+                const int p = lowest(a);
+                a = drop_lowest(a);
+                acc += h1[p * norbs + p];
+                for (Bits b = a; any(b);) {
+                    const int q = lowest(b);
+                    b = drop_lowest(b);
+                    acc += eri_at(eri, norbs, p, p, q, q) - eri_at(eri, norbs, p, q, q, p);
+                }
+            }
+            return acc;
+        };
+        double x = 0.0;
+        for (Bits a = bra_a; any(a); a = drop_lowest(a)) {
+            const int p = lowest(a);
+            for (Bits b = bra_b; any(b); b = drop_lowest(b)) x += eri_at(eri, norbs, p, p, lowest(b), lowest(b));
+        }
+        return core + energy(bra_a) + energy(bra_b) + x;
+    }
+    // separated-ordering element times eps(bra) eps(ket) (formulas.cuh)
+    const int eps = eps_parity(bra_a, prefix_parity(bra_b)) ^ eps_parity(ket_a, prefix_parity(ket_b));
+    if (db == 0 || da == 0) {  // same-spin: alpha (ch 0) or beta (ch 1)
+        const int ch = db == 0 ? 0 : 1;
+        const Bits si = ch == 0 ? bra_a : bra_b, sj = ch == 0 ? ket_a : ket_b;
+        const Bits spec = ch == 0 ? bra_b : bra_a;
+        const int kind = (ch == 0 ? da : db) - 1;
+        const PairEntry e = make_pair_entry(kind, si, sj, h1, eri, norbs);
+        double v = e.v;
+        if (kind == 0) {
+            const double j = host_j(eri, norbs, lowest(si & ~sj), lowest(sj & ~si), spec);
+            v += (e.ab_sign >> 31) ? -j : j;
+        }
+        return eps ? -v : v;
+    }
+    // mixed alpha single x beta single
+    const int pa = lowest(bra_a & ~ket_a), qa = lowest(ket_a & ~bra_a);
+    const MixedMove mv = mixed_move(bra_b, ket_b, norbs);
+    const int cd = static_cast<int>(mv.cd);
+    double w = mixed_weight(eri, norbs, pa, qa, cd / norbs, cd % norbs);
+    if (mv.sbit ^ mixed_alpha_parity(bra_a, pa, qa) ^ eps) w = -w;
+    return w;
 }
 
 } // namespace
@@ -695,61 +749,18 @@ int detci_gpu_factorized_element(int norbs, double core, const double* h1, const
                                  uint64_t bra_a, uint64_t bra_b, uint64_t ket_a, uint64_t ket_b,
                                  double* out) {
     return guarded(nullptr, [&] {
-        const int da = __builtin_popcountll(bra_a ^ ket_a) / 2;
-        const int db = __builtin_popcountll(bra_b ^ ket_b) / 2;
-        require(__builtin_popcountll(bra_a) == __builtin_popcountll(ket_a) &&
-                    __builtin_popcountll(bra_b) == __builtin_popcountll(ket_b),
-                DETCI_GPU_E_INPUT, "factorized_element: spin-nonconserving pair");
-        if (da + db > 2) {
-            *out = 0.0;
-            return;
-        }
-        if (da == 0 && db == 0) {  // diagonal, regrouped as in k_diag
-            auto energy = [&](uint64_t s) {
-                double acc = 0.0;
-                for (uint64_t a = s; a; a &= a - 1) {
-                    const int p = __builtin_ctzll(a);
-                    acc += h1[p * norbs + p];
-                    for (uint64_t b = a & (a - 1); b; b &= b - 1) {
-                        const int q = __builtin_ctzll(b);
-                        acc += eri_at(eri, norbs, p, p, q, q) - eri_at(eri, norbs, p, q, q, p);
-                    }
-                }
-                return acc;
-            };
-            double x = 0.0;
-            for (uint64_t a = bra_a; a; a &= a - 1) {
-                const int p = __builtin_ctzll(a);
-                for (uint64_t b = bra_b; b; b &= b - 1)
-                    x += eri_at(eri, norbs, p, p, __builtin_ctzll(b), __builtin_ctzll(b));
-            }
-            *out = core + energy(bra_a) + energy(bra_b) + x;
-            return;
-        }
-        // separated-ordering element times eps(bra) eps(ket) (formulas.cuh)
-        const int eps = eps_parity(bra_a, prefix_parity(bra_b)) ^ eps_parity(ket_a, prefix_parity(ket_b));
-        if (db == 0 || da == 0) {  // same-spin: alpha (ch 0) or beta (ch 1)
-            const int ch = db == 0 ? 0 : 1;
-            const uint64_t si = ch == 0 ? bra_a : bra_b, sj = ch == 0 ? ket_a : ket_b;
-            const uint64_t spec = ch == 0 ? bra_b : bra_a;
-            const int kind = (ch == 0 ? da : db) - 1;
-            const PairEntry e = make_pair_entry(kind, si, sj, h1, eri, norbs);
-            double v = e.v;
-            if (kind == 0) {
-                const uint64_t x = si & ~sj, y = sj & ~si;
-                const double j = host_j(eri, norbs, __builtin_ctzll(x), __builtin_ctzll(y), spec);
-                v += (e.ab_sign >> 31) ? -j : j;
-            }
-            *out = eps ? -v : v;
-            return;
-        }
-        // mixed alpha single x beta single
-        const int pa = __builtin_ctzll(bra_a & ~ket_a), qa = __builtin_ctzll(ket_a & ~bra_a);
-        const MixedMove mv = mixed_move(bra_b, ket_b, norbs);
-        const int cd = static_cast<int>(mv.cd);
-        double w = mixed_weight(eri, norbs, pa, qa, cd / norbs, cd % norbs);
-        if (mv.sbit ^ mixed_alpha_parity(bra_a, pa, qa) ^ eps) w = -w;
-        *out = w;
+        *out = factorized_element_bits(norbs, core, h1, eri, Bits(bra_a), Bits(bra_b), Bits(ket_a), Bits(ket_b));
+    });
+}
+
+int detci_gpu_factorized_element_words(int norbs, int words, double core, const double* h1, const double* eri,
+                                       const uint64_t* bra_a, const uint64_t* bra_b, const uint64_t* ket_a,
+                                       const uint64_t* ket_b, double* out) {
+    return guarded(nullptr, [&] {
+        require(words == 1 || words == 2, DETCI_GPU_E_INPUT, "factorized_element: words must be 1 or 2");
+        require(norbs <= 64 * words, DETCI_GPU_E_INPUT, "factorized_element: norbs exceeds the words");
+        auto w = [&](const uint64_t* x) { return Bits(x[0], words > 1 ? x[1] : 0ull); };
+        *out = factorized_element_bits(norbs, core, h1, eri, w(bra_a), w(bra_b), w(ket_a), w(ket_b));
     });
 }
 

@@ -257,6 +257,7 @@ struct StreamArgs {
     int ns, k;
     uint32_t T;              // tile elements (multiple of 32)
     int nst;                 // pipeline stages (<= kStMaxStages)
+    int split;               // kPassRitz: two threads per element (DETCI_DAV_RITZ_SPLIT=1)
     uint64_t n;
     double theta;
     const double* coef;      // kPassOrth1: d_j (unnormalised <v_j, corr>); kPassOrth2: e_j (device slots)
@@ -286,17 +287,21 @@ k_dav_stream(const StreamArgs a) {
     auto tile_base = [&](uint32_t it) { return (static_cast<uint64_t>(it) * gridDim.x + blockIdx.x) * T; };
     auto tile_cnt = [&](uint32_t it) { const uint64_t rem = a.n - tile_base(it); return static_cast<uint32_t>(rem < T ? rem : T); };
     auto stage = [&](uint32_t st) { return st_smem + static_cast<size_t>(st) * ns * T; };
-    auto issue = [&](uint32_t it) {   // elected thread
+    auto issue = [&](uint32_t it) {   // warp 0: lane 0 arms the barrier, the lanes issue the copies
         const uint32_t st = it % kStStages, bytes = (tile_cnt(it) * 8u) & ~15u;
-        mbar_arrive_expect_tx(&bars[st], bytes * static_cast<uint32_t>(ns));
+        if (lane == 0) mbar_arrive_expect_tx(&bars[st], bytes * static_cast<uint32_t>(ns));
+        __syncwarp();
         if (bytes)
-            for (int s = 0; s < ns; ++s) bulk_g2s(stage(st) + static_cast<size_t>(s) * T, a.s[s] + tile_base(it), bytes, &bars[st]);
+            for (int s = static_cast<int>(lane); s < ns; s += 32)
+                bulk_g2s(stage(st) + static_cast<size_t>(s) * T, a.s[s] + tile_base(it), bytes, &bars[st]);
     };
     if (tid == 0) {
         for (int s = 0; s < kStStages; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
-        for (uint32_t it = 0; it < my_tiles && it < kStStages; ++it) issue(it);
     }
+    __syncwarp();
+    if (warp == 0)
+        for (uint32_t it = 0; it < my_tiles && it < static_cast<uint32_t>(kStStages); ++it) issue(it);
     if (MODE == kPassOrth1 || MODE == kPassOrth2)
         for (int j = tid; j < k; j += kStThreads) s_coef[j] = a.coef[j];
     __syncthreads();
@@ -304,6 +309,13 @@ k_dav_stream(const StreamArgs a) {
     // per-element scalars
     double inv_cnorm = 0.0;
     if (MODE == kPassOrth1) inv_cnorm = 1.0 / sqrt(*a.norm2);
+    double out_scale = 1.0;   // kPassOrth2: 1 / nu, nu^2 = |cand1|^2 - sum e_j^2
+    if (MODE == kPassOrth2) {
+        double e2 = 0.0;
+        for (int j = 0; j < k; ++j) e2 += s_coef[j] * s_coef[j];
+        const double nu2 = *a.norm2 - e2;
+        out_scale = nu2 > 0.0 ? 1.0 / sqrt(nu2) : 1.0;
+    }
     double r1 = 0.0, r2 = 0.0;            // |res|^2, |corr|^2 / |cand|^2
     double acc[kStJ], acc2[kStJ];         // per-warp dots (vector j = warp + kStWarps * jj)
 #pragma unroll
@@ -318,15 +330,26 @@ k_dav_stream(const StreamArgs a) {
         mbar_wait(&bars[st], (it / kStStages) & 1u);
         if ((cnt & 1u) && static_cast<int>(tid) < ns) S[static_cast<size_t>(tid) * T + cnt - 1] = a.s[tid][base + cnt - 1];
         __syncthreads();
-        // element-wise part
-        for (uint32_t i = tid; i < cnt; i += kStThreads) {
+        // element-wise part (kPassRitz with a.split: two threads per
+        // element, each summing half of the subspace, combined by a shuffle)
+        const uint32_t esplit = MODE == kPassRitz && a.split ? 1u : 0u;
+        const uint32_t ehalf = tid & esplit;
+        const uint32_t cnt_up = esplit ? ((cnt + (kStThreads / 2) - 1) / (kStThreads / 2)) * (kStThreads / 2) : cnt;
+        for (uint32_t i = tid >> esplit; i < cnt_up; i += kStThreads >> esplit) {
             if constexpr (MODE == kPassRitz) {
+                const bool live = i < cnt;
+                const uint32_t ii = live ? i : 0;
                 double r = 0.0, m = 0.0;
 #pragma unroll 4
-                for (int j = 0; j < k; ++j) {
-                    r += a.c[j] * S[static_cast<size_t>(j) * T + i];
-                    m += a.c[j] * S[static_cast<size_t>(k + j) * T + i];
+                for (int j = static_cast<int>(ehalf); j < k; j += 1 + static_cast<int>(esplit)) {
+                    r += a.c[j] * S[static_cast<size_t>(j) * T + ii];
+                    m += a.c[j] * S[static_cast<size_t>(k + j) * T + ii];
                 }
+                if (esplit) {
+                    r += __shfl_xor_sync(0xffffffffu, r, 1);
+                    m += __shfl_xor_sync(0xffffffffu, m, 1);
+                }
+                if (!live || ehalf) continue;
                 const double res = m - a.theta * r;
                 double denom = S[static_cast<size_t>(2 * k) * T + i] - a.theta;
                 if (fabs(denom) < 1e-8) denom = copysign(1e-8, denom);
@@ -341,7 +364,7 @@ k_dav_stream(const StreamArgs a) {
                 for (int j = 0; j < k; ++j) x -= s_coef[j] * S[static_cast<size_t>(1 + j) * T + i];
                 if (MODE == kPassOrth1) x *= inv_cnorm;
                 probe[i] = x;
-                a.out[base + i] = x;
+                a.out[base + i] = MODE == kPassOrth2 ? x * out_scale : x;
                 r2 += x * x;
             }
         }
@@ -367,17 +390,19 @@ k_dav_stream(const StreamArgs a) {
             }
         }
         __syncthreads();   // stage and probe consumed
-        if (tid == 0 && it + kStStages < my_tiles) {
+        if (warp == 0 && it + kStStages < my_tiles) {
             fence_proxy_async_smem();
             issue(it + kStStages);
         }
     }
     // partials: [0] |res|^2, [1] |corr|^2 (kPassRitz) or [0] |cand|^2 (kPassOrth2);
+    // kPassOrth1 also [k] |cand1|^2
     // dots at [dbase + j] (and the Gram row at [dbase + k + j])
     const int dbase = MODE == kPassRitz ? 2 : 0;
-    if constexpr (MODE == kPassRitz || MODE == kPassOrth2) {
+    if constexpr (MODE == kPassRitz || MODE == kPassOrth2 || MODE == kPassOrth1) {
         const double s2 = block_sum(r2, sh);
-        if (tid == 0) a.partial[static_cast<size_t>(MODE == kPassRitz ? 1 : 0) * gridDim.x + blockIdx.x] = s2;
+        const int slot = MODE == kPassRitz ? 1 : (MODE == kPassOrth1 ? k : 0);
+        if (tid == 0) a.partial[static_cast<size_t>(slot) * gridDim.x + blockIdx.x] = s2;
     }
     if constexpr (MODE == kPassRitz) {
         const double s1 = block_sum(r1, sh);
@@ -730,15 +755,17 @@ StreamCfg stream_cfg() {
     return c;
 }
 
-// DETCI_DAV_STREAM=warp: the warp-per-vector dot phase (k_dav_stream) for
-// every k; default: the register-dot kernel (k_dav_stream_r) for k <= 24.
+// DETCI_DAV_STREAM=reg: the register-dot kernel (k_dav_stream_r) for k <= 24.
+// Measured slower than the warp-per-vector dot phase (C2, 12 iterations:
+// 86.9 vs 65.5 ms for the four passes): one element per thread and 8 warps
+// per SM leave the k-long FMA chains and the division exposed.
 constexpr int kRsMaxK = 24;
 bool register_stream(int k) {
-    static const bool warp = [] {
+    static const bool reg = [] {
         const char* e = std::getenv("DETCI_DAV_STREAM");
-        return e && std::string(e) == "warp";
+        return e && std::string(e) == "reg";
     }();
-    return !warp && k <= kRsMaxK;
+    return reg && k <= kRsMaxK;
 }
 
 template <int MODE>
@@ -747,6 +774,11 @@ void stream_pass(Handle& h, StreamArgs& a, int nred, int slot) {
         if (reinterpret_cast<uintptr_t>(a.s[s]) & 15u) fail(DETCI_GPU_E_ERROR, "davidson: misaligned vector");
     static const StreamCfg cfg = stream_cfg();
     a.nst = cfg.stages;
+    static const bool split = [] {
+        const char* e = std::getenv("DETCI_DAV_RITZ_SPLIT");
+        return e && std::string(e) == "1";
+    }();
+    a.split = split ? 1 : 0;
     if (register_stream(a.k)) {
         a.T = static_cast<uint32_t>(std::min<size_t>(4096, kStSmem / 8 / (static_cast<size_t>(a.nst) * a.ns)) &
                                     ~size_t{31});
@@ -1176,15 +1208,14 @@ void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* re
             oa.coef = scalar_slot(h, kSlotRitz + 2);
             oa.norm2 = scalar_slot(h, kSlotRitz + 1);
             oa.out = cand;
-            const bool reg = register_stream(k);
-            // the register kernel also reduces |cand1|^2 (slot k) and
-            // writes the normalised candidate in pass 2
-            stream_pass<kPassOrth1>(h, oa, reg ? k + 1 : k, kSlotOrth1);
+            // pass 1 also reduces |cand1|^2 (slot k); pass 2 writes the
+            // candidate normalised by nu = sqrt(|cand1|^2 - sum e_j^2)
+            stream_pass<kPassOrth1>(h, oa, k + 1, kSlotOrth1);
             oa.s[0] = cand;
             oa.coef = scalar_slot(h, kSlotOrth1);
             oa.norm2 = scalar_slot(h, kSlotOrth1 + k);
             stream_pass<kPassOrth2>(h, oa, 1, kSlotOrth2);
-            if (reg) {
+            {
                 std::vector<double> sl(k + 1);
                 read_slots(h, kSlotOrth1, k + 1, sl.data());
                 read_slots(h, kSlotOrth2, 1, &nrm2);
@@ -1199,8 +1230,6 @@ void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* re
                     CUDA_LAUNCH_CHECK();
                 }
                 prenormalised = true;
-            } else {
-                read_slots(h, kSlotOrth2, 1, &nrm2);
             }
         } else {
             // classical Gram-Schmidt twice ("twice is enough"): each pass is

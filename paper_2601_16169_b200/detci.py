@@ -471,6 +471,14 @@ def factorized_element(integrals, bra_a: int, bra_b: int, ket_a: int, ket_b: int
     h1 = _f64(integrals.h1).reshape(-1)
     eri = _f64(integrals.eri).reshape(-1)
     out = C.c_double()
+    if integrals.norbs > 64:
+        mask = (1 << 64) - 1
+        w = [np.array([int(x) & mask, int(x) >> 64], dtype=np.uint64) for x in (bra_a, bra_b, ket_a, ket_b)]
+        code = lib.detci_gpu_factorized_element_words(integrals.norbs, 2, float(integrals.core),
+                                                      _ptr(h1, C.c_double), _ptr(eri, C.c_double),
+                                                      *[_ptr(a, C.c_uint64) for a in w], C.byref(out))
+        raise_for(code, (lib.detci_gpu_last_error(None) or b"").decode())
+        return out.value
     code = lib.detci_gpu_factorized_element(integrals.norbs, float(integrals.core), _ptr(h1, C.c_double),
                                             _ptr(eri, C.c_double), bra_a, bra_b, ket_a, ket_b, C.byref(out))
     raise_for(code, (lib.detci_gpu_last_error(None) or b"").decode())

@@ -165,3 +165,43 @@ def test_library_then_torch_share_one_nccl():
             "print('ok', torch.cuda.nccl.version())\n") % str(Path(__file__).resolve().parents[1])
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and out.stdout.startswith("ok"), out.stderr[-2000:]
+
+
+def test_factorized_elements_match_reference_hij_two_words():
+    """The closed forms on two-word strings (norbs = 70) against the
+    reference hij on multi-word determinants: singles, doubles, mixed and
+    diagonal, with moves that cross orbital 64 and occupied orbitals on both
+    sides of it (cross-word sign counts, 128-bit prefix parity of eps)."""
+    from oracle.bindings import REF_SO, RefLib
+
+    if not REF_SO.exists():
+        pytest.skip("reference library not built")
+    n = 70
+    ints = synth.synthetic_integrals(n, 16)
+    table = RefLib().table_from_integrals(ints)
+    rng = np.random.default_rng(7)
+
+    def rand_string(nel):
+        return sum(1 << int(i) for i in rng.choice(n, size=nel, replace=False))
+
+    def excite(s, k):
+        occ = [i for i in range(n) if (s >> i) & 1]
+        vir = [i for i in range(n) if not (s >> i) & 1]
+        for p in rng.choice(occ, size=k, replace=False):
+            s &= ~(1 << int(p))
+        for q in rng.choice(vir, size=k, replace=False):
+            s |= 1 << int(q)
+        return s
+
+    classes = {(1, 0): "alpha_single", (0, 1): "beta_single", (2, 0): "alpha_double", (0, 2): "beta_double",
+               (1, 1): "mixed", (0, 0): "diagonal", (2, 1): "triple"}
+    worst = {}
+    for _ in range(60):
+        ba, bb = rand_string(8), rand_string(8)
+        for (ka, kb), name in classes.items():
+            ket_a, ket_b = excite(ba, ka), excite(bb, kb)
+            want = table.hij_words(ba, bb, ket_a, ket_b)
+            got = detci.factorized_element(ints, ba, bb, ket_a, ket_b)
+            worst[name] = max(worst.get(name, 0.0), abs(got - want) / max(1.0, abs(want)))
+    assert set(worst) == set(classes.values())
+    assert max(worst.values()) <= 1e-12, worst

@@ -8,10 +8,11 @@ reference cannot finish.
 
 * the first iterations of both solvers agree per iteration (Ritz values
   1e-9 relative, same restarts) -- run live;
-* the converged C2 energy of the reference solver (scripts/mixed_oracle.py
-  C2 260, 3,000+ s of serial reference vector work, committed as
-  tests/golden/mixed_oracle_C2.json) equals the device Davidson's within
-  1e-8 Ha.
+* the reference solver's trace at C2 (40 iterations) and C3 (30), made by
+  scripts/mixed_oracle.py and committed as tests/golden/mixed_oracle_C*.json
+  (its single-threaded vector work costs ~20 s per iteration at C2 and ~60 s
+  at C3, so it is not rerun live), equals a live device Davidson's per
+  iteration.
 """
 import json
 
@@ -49,20 +50,26 @@ def test_reference_solver_trace_c2(c2):
         assert bool(r[3]) == it.restarted
 
 
-def test_c2_converged_energy_matches_reference_solver(c2):
-    from paper_2601_16169_b200 import detci
+@pytest.mark.parametrize("cfg", ["C2", "C3"])
+def test_trace_matches_committed_reference_solver(cfg):
+    """The reference solver's Ritz trace over the device sigma, committed
+    from scripts/mixed_oracle.py (40 iterations at C2, 30 at C3: its serial
+    vector work is ~20 s / 60 s per iteration there), against a live device
+    Davidson of the same length, per iteration."""
+    from paper_2601_16169_b200 import detci, synth
 
-    path = GOLDEN / "mixed_oracle_C2.json"
+    path = GOLDEN / f"mixed_oracle_{cfg}.json"
     if not path.exists():
-        pytest.skip("mixed_oracle_C2.json not generated")
+        pytest.skip(f"{path.name} not generated")
     ref = json.loads(path.read_text())
-    rs = ref["reference_solver"]
-    assert rs["status"] == "converged"
-    res = detci.davidson_solve(c2, detci.DavidsonOptions(max_iter=ref["max_iter"], max_subspace=ref["max_subspace"]),
-                               want_vector=False)
-    assert res.converged
-    assert abs(res.energy - rs["energy"]) <= 1e-8
-    assert abs(len(res.iterations) - rs["iterations"]) <= 2
-    # the committed trace of both solvers agreed per iteration when it was made
     tr = np.array(ref["trace"])
-    assert np.max(np.abs(tr[:, 0] - tr[:, 1]) / np.abs(tr[:, 0])) <= 1e-9
+    ints, a, b = synth.synthetic_system(cfg)
+    with detci.GpuBasis(ints.norbs, a, b, ints.core, ints.h1, ints.eri) as g:
+        res = detci.davidson_solve(g, detci.DavidsonOptions(max_iter=ref["max_iter"],
+                                                            max_subspace=ref["max_subspace"]), want_vector=False)
+    assert len(res.iterations) == len(tr) == ref["reference_solver"]["iterations"]
+    ritz = np.array([it.ritz_value for it in res.iterations])
+    resid = np.array([it.residual_norm for it in res.iterations])
+    assert np.max(np.abs(ritz - tr[:, 0]) / np.abs(tr[:, 0])) <= 1e-9
+    assert np.max(np.abs(resid - tr[:, 2]) / tr[:, 2]) <= 1e-6
+    assert abs(res.energy - ref["reference_solver"]["energy"]) <= 1e-9 * abs(res.energy)
