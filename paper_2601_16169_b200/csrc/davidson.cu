@@ -19,6 +19,9 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "handle.hpp"
 #include "sigma_device.cuh"
 
@@ -252,6 +255,11 @@ constexpr int kStMaxStages = 6;
 constexpr size_t kStSmem = 210 * 1024;   // per SM
 
 struct StreamArgs {
+    // kPassRitz with tma2d: V[0..k) and W[0..k) as two 2-D tensor maps (rows
+    // ld apart), one box of k rows x T columns each per tile
+    CUtensorMap tm[2];
+    int tma2d;
+    uint64_t ld;             // row stride (elements) of the V / W blocks (tma2d)
     const double* s[kStMaxS];
     double c[kMaxVec];       // kPassRitz: Ritz coefficients
     int ns, k;
@@ -266,13 +274,21 @@ struct StreamArgs {
     double* partial;         // [reduction][gridDim.x]
 };
 
+__device__ __forceinline__ void tma_2d_g2s(void* dst, const CUtensorMap* map, int c0, int r0, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r0), "r"(smem_u32(bar))
+        : "memory");
+}
+
 template <int MODE, int kStThreads>
 __global__ void __launch_bounds__(kStThreads, 512 / kStThreads)
-k_dav_stream(const StreamArgs a) {
+k_dav_stream(const __grid_constant__ StreamArgs a) {
     constexpr int kStWarps = kStThreads / 32;
     constexpr int kStJ = kMaxVec / kStWarps;   // subspace vectors per warp
     const int kStStages = a.nst;
-    extern __shared__ __align__(16) double st_smem[];
+    extern __shared__ __align__(128) double st_smem[];   // 2-D TMA boxes land 128-byte aligned
     __shared__ uint64_t bars[kStMaxStages];
     __shared__ double sh[32];
     __shared__ double s_coef[kMaxVec];
@@ -289,6 +305,18 @@ k_dav_stream(const StreamArgs a) {
     auto stage = [&](uint32_t st) { return st_smem + static_cast<size_t>(st) * ns * T; };
     auto issue = [&](uint32_t it) {   // warp 0: lane 0 arms the barrier, the lanes issue the copies
         const uint32_t st = it % kStStages, bytes = (tile_cnt(it) * 8u) & ~15u;
+        if (MODE == kPassRitz && a.tma2d) {
+            // two boxes (V, W: k rows x T, zero-filled past n, always full
+            // box bytes) and the diagonal by a 1-D copy
+            if (lane == 0) {
+                mbar_arrive_expect_tx(&bars[st], 2u * static_cast<uint32_t>(k) * T * 8u + bytes);
+                const int c0 = static_cast<int>(tile_base(it));
+                tma_2d_g2s(stage(st), &a.tm[0], c0, 0, &bars[st]);
+                tma_2d_g2s(stage(st) + static_cast<size_t>(k) * T, &a.tm[1], c0, 0, &bars[st]);
+                if (bytes) bulk_g2s(stage(st) + static_cast<size_t>(2 * k) * T, a.s[2 * k] + tile_base(it), bytes, &bars[st]);
+            }
+            return;
+        }
         if (lane == 0) mbar_arrive_expect_tx(&bars[st], bytes * static_cast<uint32_t>(ns));
         __syncwarp();
         if (bytes)
@@ -738,8 +766,11 @@ int sm_count() {
 // [slot, slot + nred).  Stream bases must be 16-byte aligned.
 // Pipeline shape of the fused passes: threads per CTA, CTAs per SM, stages
 // (DETCI_DAV_CFG="threads,ctas,stages" overrides the default 512,1,3).
+// Two stages (C2, 60 iterations, one box: subspace solve + vector work 8.8 ms
+// per iteration at 512 x 1 x 2, 10.7 ms at 512 x 1 x 3, 9.0 ms at 256 x 2 x 2,
+// 11.6 ms at 256 x 2 x 3): larger tiles, fewer barriers per byte.
 struct StreamCfg {
-    int threads = 512, ctas = 1, stages = 3;
+    int threads = 512, ctas = 1, stages = 2;
 };
 StreamCfg stream_cfg() {
     StreamCfg c;
@@ -768,12 +799,73 @@ bool register_stream(int k) {
     return reg && k <= kRsMaxK;
 }
 
+// 2-D tensor map over `rows` vectors of n doubles, ld apart, box T x rows
+// (cuTensorMapEncodeTiled through the runtime's driver entry point).
+bool encode_rows_map(CUtensorMap* m, const double* base, uint64_t n, uint32_t rows, uint64_t ld, uint32_t T) {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    if (!fn || rows == 0 || rows > 256 || T == 0 || T > 256 || (ld * 8) % 16 != 0) return false;
+    const cuuint64_t dims[2] = {n, rows};
+    const cuuint64_t strides[1] = {ld * 8};
+    const cuuint32_t box[2] = {T, rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// DETCI_DAV_TMA2D=1: the Ritz pass stages V and W as two 2-D tensor boxes
+// per tile instead of one 1-D copy per vector.  Measured level or slower
+// (C2, 60 iterations: vector work 7.73-7.87 vs 7.61 ms per iteration; the
+// box width caps T at 256), so the per-copy cost is not what holds the Ritz
+// pass below the others; off by default.
+bool tma2d_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("DETCI_DAV_TMA2D");
+        return e && std::string(e) == "1";
+    }();
+    return on;
+}
+
 template <int MODE>
 void stream_pass(Handle& h, StreamArgs& a, int nred, int slot) {
     for (int s = 0; s < a.ns; ++s)
         if (reinterpret_cast<uintptr_t>(a.s[s]) & 15u) fail(DETCI_GPU_E_ERROR, "davidson: misaligned vector");
     static const StreamCfg cfg = stream_cfg();
     a.nst = cfg.stages;
+    if (MODE == kPassRitz && a.tma2d) {
+        // V rows and W rows must each be one strided block
+        bool ok = tma2d_enabled() && a.k >= 1;
+        for (int j = 0; ok && j < a.k; ++j)
+            ok = a.s[j] == a.s[0] + j * a.ld && a.s[a.k + j] == a.s[a.k] + j * a.ld;
+        const size_t per = static_cast<size_t>(a.nst) * a.ns + 1;
+        const uint32_t T = static_cast<uint32_t>(std::min<size_t>(256, kStSmem / cfg.ctas / 8 / per) & ~size_t{31});
+        ok = ok && T >= 32 && cfg.threads == 512 &&
+             encode_rows_map(&a.tm[0], a.s[0], a.n, static_cast<uint32_t>(a.k), a.ld, T) &&
+             encode_rows_map(&a.tm[1], a.s[a.k], a.n, static_cast<uint32_t>(a.k), a.ld, T);
+        a.tma2d = ok ? 1 : 0;
+        if (ok) {
+            a.T = T;
+            const size_t smem = per * a.T * sizeof(double);
+            const int grid = sm_count() * cfg.ctas;
+            a.partial = h.red.p;
+            ensure_dynamic_smem(reinterpret_cast<const void*>(&k_dav_stream<MODE, 512>), smem);
+            k_dav_stream<MODE, 512><<<grid, 512, smem, h.stream>>>(a);
+            CUDA_LAUNCH_CHECK();
+            if (nred > 0) {
+                k_finalize<<<nred, 32, 0, h.stream>>>(h.red.p, grid, nred, scalar_slot(h, slot));
+                CUDA_LAUNCH_CHECK();
+                allreduce_device(h, scalar_slot(h, slot), nred);
+            }
+            return;
+        }
+    }
     static const bool split = [] {
         const char* e = std::getenv("DETCI_DAV_RITZ_SPLIT");
         return e && std::string(e) == "1";
@@ -1114,6 +1206,8 @@ void davidson_device(Handle& h, const detci_dav_opts& opts, detci_dav_result* re
             ra.s[2 * k] = h.diag.p;
             ra.theta = theta;
             ra.out = corr;
+            ra.tma2d = 1;
+            ra.ld = ld;
             stream_pass<kPassRitz>(h, ra, 2 * k + 2, kSlotRitz);
             std::vector<double> sc(2 * k + 2);
             read_slots(h, kSlotRitz, 2 * k + 2, sc.data());

@@ -117,8 +117,8 @@ def test_build_validation_errors():
         gpu_basis(ints, np.array([0b10000], dtype=np.uint64), np.array([1], dtype=np.uint64))
     with pytest.raises(errors.InputError):            # empty list
         gpu_basis(ints, np.array([], dtype=np.uint64), np.array([1], dtype=np.uint64))
-    with pytest.raises(errors.UnsupportedError):      # norbs > 64 on the device path
-        detci.GpuBasis(65, [1], [1], 0.0, np.zeros(65 * 65), np.zeros(1))
+    with pytest.raises(errors.InputError):            # > 256 spin-orbitals (basis.cpp:83-87)
+        detci.GpuBasis(129, [1], [1], 0.0, np.zeros(129 * 129), np.zeros(1))
     with pytest.raises(errors.CapacityError):         # memory budget (basis.cpp:113-118)
         gpu_basis(ints, np.array([0b0011, 0b0101], dtype=np.uint64), np.array([0b0011], dtype=np.uint64),
                   memory_budget_bytes=64)
