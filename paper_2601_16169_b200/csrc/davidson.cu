@@ -454,7 +454,7 @@ k_dav_stream(const __grid_constant__ StreamArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Register-dot variant of the fused passes (default for k <= 24).  Same
+// Register-dot variant of the fused passes (default for k <= 20).  Same
 // streams, same TMA ring, but one thread owns one element of the tile and
 // keeps every dot of the pass in registers (KMAX accumulators), so a tile
 // costs one barrier and 2k + 1 (Ritz) / k + 1 shared-memory loads per
@@ -470,7 +470,7 @@ k_dav_stream(const __grid_constant__ StreamArgs a) {
 //   |cand2|^2 and rescales in the rare case they disagree), which removes
 //   the normalisation pass.
 // ---------------------------------------------------------------------------
-constexpr int kRsThreads = 256;
+constexpr int kRsThreads = 512;
 
 template <int MODE, int KMAX>
 __global__ void __launch_bounds__(kRsThreads, 1)
@@ -539,13 +539,11 @@ k_dav_stream_r(const StreamArgs a) {
         }
         for (uint32_t i = tid; i < cnt; i += kRsThreads) {
             if constexpr (MODE == kPassRitz) {
-                double vr[KMAX];
                 double r = 0.0, m = 0.0;
 #pragma unroll
                 for (int j = 0; j < KMAX; ++j)
                     if (j < k) {
-                        vr[j] = S[static_cast<size_t>(j) * T + i];
-                        r = fma(a.c[j], vr[j], r);
+                        r = fma(a.c[j], S[static_cast<size_t>(j) * T + i], r);
                         m = fma(a.c[j], S[static_cast<size_t>(k + j) * T + i], m);
                     }
                 const double res = m - a.theta * r;
@@ -559,8 +557,9 @@ k_dav_stream_r(const StreamArgs a) {
 #pragma unroll
                 for (int j = 0; j < KMAX; ++j)
                     if (j < k) {
-                        acc[j] = fma(vr[j], cr, acc[j]);
-                        acc2[j] = fma(vr[j], last, acc2[j]);
+                        const double v = S[static_cast<size_t>(j) * T + i];
+                        acc[j] = fma(v, cr, acc[j]);
+                        acc2[j] = fma(v, last, acc2[j]);
                     }
             } else if constexpr (MODE == kPassProj) {
                 const double x = S[i];
@@ -568,21 +567,17 @@ k_dav_stream_r(const StreamArgs a) {
                 for (int j = 0; j < KMAX; ++j)
                     if (j < k) acc[j] = fma(S[static_cast<size_t>(1 + j) * T + i], x, acc[j]);
             } else {
-                double vr[KMAX];
                 double x = S[i];
 #pragma unroll
                 for (int j = 0; j < KMAX; ++j)
-                    if (j < k) {
-                        vr[j] = S[static_cast<size_t>(1 + j) * T + i];
-                        x = fma(-s_coef[j], vr[j], x);
-                    }
+                    if (j < k) x = fma(-s_coef[j], S[static_cast<size_t>(1 + j) * T + i], x);
                 r2 = fma(x, x, r2);   // Orth1: |corr - sum d v|^2 (scaled below); Orth2: |cand2|^2
                 x *= scale;
                 a.out[base + i] = x;
                 if constexpr (MODE == kPassOrth1) {
 #pragma unroll
                     for (int j = 0; j < KMAX; ++j)
-                        if (j < k) acc[j] = fma(vr[j], x, acc[j]);
+                        if (j < k) acc[j] = fma(S[static_cast<size_t>(1 + j) * T + i], x, acc[j]);
                 }
             }
         }
@@ -786,17 +781,22 @@ StreamCfg stream_cfg() {
     return c;
 }
 
-// DETCI_DAV_STREAM=reg: the register-dot kernel (k_dav_stream_r) for k <= 24.
-// Measured slower than the warp-per-vector dot phase (C2, 12 iterations:
-// 86.9 vs 65.5 ms for the four passes): one element per thread and 8 warps
-// per SM leave the k-long FMA chains and the division exposed.
-constexpr int kRsMaxK = 24;
-bool register_stream(int k) {
-    static const bool reg = [] {
+// Default for k <= 20: the register-dot kernel (k_dav_stream_r, 512 threads).
+// Measured on C2, 12 iterations (ncu launch lists, 2 stages): the four passes
+// 56.6 ms vs 61.1 ms with the warp-per-vector dot phase (Ritz pass 24.7 vs
+// 29.1 ms); at 256 threads it was slower (86.9 vs 65.5 ms at 3 stages): one
+// element per thread needs the full 16 warps to hide its FMA chains.
+// DETCI_DAV_STREAM=warp: the warp-per-vector kernel for every k;
+// DETCI_DAV_STREAM=reg_ritz: the register kernel for the Ritz pass only.
+constexpr int kRsMaxK = 20;
+bool register_stream(int k, int mode = -1) {
+    static const int sel = [] {
         const char* e = std::getenv("DETCI_DAV_STREAM");
-        return e && std::string(e) == "reg";
+        if (e && std::string(e) == "warp") return 0;
+        if (e && std::string(e) == "reg_ritz") return 2;
+        return 1;
     }();
-    return reg && k <= kRsMaxK;
+    return k <= kRsMaxK && (sel == 1 || (sel == 2 && mode == kPassRitz));
 }
 
 // 2-D tensor map over `rows` vectors of n doubles, ld apart, box T x rows
@@ -871,7 +871,7 @@ void stream_pass(Handle& h, StreamArgs& a, int nred, int slot) {
         return e && std::string(e) == "1";
     }();
     a.split = split ? 1 : 0;
-    if (register_stream(a.k)) {
+    if (register_stream(a.k, MODE)) {
         a.T = static_cast<uint32_t>(std::min<size_t>(4096, kStSmem / 8 / (static_cast<size_t>(a.nst) * a.ns)) &
                                     ~size_t{31});
         if (a.T < 32) fail(DETCI_GPU_E_ERROR, "davidson: stream tile below 32 elements");
@@ -883,6 +883,8 @@ void stream_pass(Handle& h, StreamArgs& a, int nred, int slot) {
             kern<<<grid, kRsThreads, smem, h.stream>>>(a);
         };
         if (a.k <= 8) go(&k_dav_stream_r<MODE, 8>);
+        else if (a.k <= 12) go(&k_dav_stream_r<MODE, 12>);
+        else if (a.k <= 16) go(&k_dav_stream_r<MODE, 16>);
         else go(&k_dav_stream_r<MODE, kRsMaxK>);
         CUDA_LAUNCH_CHECK();
         if (nred > 0) {
