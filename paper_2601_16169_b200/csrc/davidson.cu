@@ -634,6 +634,131 @@ k_dav_stream_r(const StreamArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Block (multi-root) residual pass: one stream over V[0..k), W[0..k) and the
+// diagonal forms the preconditioned correction of all m <= 4 roots,
+//   corr_r = (W c_r - theta_r V c_r) / clamp(diag - theta_r),
+// and |res_r|^2, |corr_r|^2 -- 2k + 1 vector reads and m writes instead of
+// m Ritz passes of 2k reads and 3 writes each (Ritz vectors and images are
+// formed only when the subspace collapses onto them, or at the end).
+// One element per thread (512 threads), the same TMA ring as the single-root
+// passes; partials [r] |res_r|^2, [m + r] |corr_r|^2.
+// ---------------------------------------------------------------------------
+constexpr int kBlkMaxRoots = 4;
+struct BlockRitzArgs {
+    const double* s[kStMaxS];        // V[0..k), W[0..k), diag
+    double c[kBlkMaxRoots][kMaxVec]; // Ritz coefficients per root
+    double theta[kBlkMaxRoots];
+    double* out[kBlkMaxRoots];       // corr_r
+    int k, m, ns, nst;
+    uint32_t T;
+    uint64_t n;
+    double* partial;
+};
+
+__global__ void __launch_bounds__(512, 1)
+k_ritz_block(const BlockRitzArgs a) {
+    constexpr int kThreads = 512, kWarps = kThreads / 32;
+    extern __shared__ __align__(16) double st_smem[];
+    __shared__ uint64_t bars[kStMaxStages];
+    __shared__ double s_red[kWarps][2 * kBlkMaxRoots];
+    const int nst = a.nst, ns = a.ns, k = a.k, m = a.m;
+    const uint32_t T = a.T;
+    const uint32_t tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
+    const uint64_t ntiles = (a.n + T - 1) / T;
+    const uint32_t my_tiles = blockIdx.x < ntiles
+                                  ? static_cast<uint32_t>((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x)
+                                  : 0u;
+    auto tile_base = [&](uint32_t it) { return (static_cast<uint64_t>(it) * gridDim.x + blockIdx.x) * T; };
+    auto tile_cnt = [&](uint32_t it) { const uint64_t rem = a.n - tile_base(it); return static_cast<uint32_t>(rem < T ? rem : T); };
+    auto stage = [&](uint32_t st) { return st_smem + static_cast<size_t>(st) * ns * T; };
+    auto issue = [&](uint32_t it) {   // warp 0
+        const uint32_t st = it % nst, bytes = (tile_cnt(it) * 8u) & ~15u;
+        if (lane == 0) mbar_arrive_expect_tx(&bars[st], bytes * static_cast<uint32_t>(ns));
+        __syncwarp();
+        if (bytes)
+            for (int s = static_cast<int>(lane); s < ns; s += 32)
+                bulk_g2s(stage(st) + static_cast<size_t>(s) * T, a.s[s] + tile_base(it), bytes, &bars[st]);
+    };
+    if (tid == 0) {
+        for (int s = 0; s < nst; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    if (warp == 0)
+        for (uint32_t it = 0; it < my_tiles && it < static_cast<uint32_t>(nst); ++it) issue(it);
+    __syncthreads();
+
+    double s1[kBlkMaxRoots], s2[kBlkMaxRoots];
+#pragma unroll
+    for (int r = 0; r < kBlkMaxRoots; ++r) s1[r] = s2[r] = 0.0;
+#pragma unroll 1
+    for (uint32_t it = 0; it < my_tiles; ++it) {
+        const uint32_t st = it % nst;
+        const uint32_t cnt = tile_cnt(it);
+        const uint64_t base = tile_base(it);
+        const double* const S = stage(st);
+        mbar_wait(&bars[st], (it / nst) & 1u);
+        if (cnt & 1u) {
+            if (static_cast<int>(tid) < ns)
+                const_cast<double*>(S)[static_cast<size_t>(tid) * T + cnt - 1] = a.s[tid][base + cnt - 1];
+            __syncthreads();
+        }
+        for (uint32_t i = tid; i < cnt; i += kThreads) {
+            double rv[kBlkMaxRoots], rw[kBlkMaxRoots];
+#pragma unroll
+            for (int r = 0; r < kBlkMaxRoots; ++r) rv[r] = rw[r] = 0.0;
+#pragma unroll 2
+            for (int j = 0; j < k; ++j) {
+                const double v = S[static_cast<size_t>(j) * T + i];
+                const double w = S[static_cast<size_t>(k + j) * T + i];
+#pragma unroll
+                for (int r = 0; r < kBlkMaxRoots; ++r)
+                    if (r < m) {
+                        rv[r] = fma(a.c[r][j], v, rv[r]);
+                        rw[r] = fma(a.c[r][j], w, rw[r]);
+                    }
+            }
+            const double dg = S[static_cast<size_t>(2 * k) * T + i];
+#pragma unroll
+            for (int r = 0; r < kBlkMaxRoots; ++r)
+                if (r < m) {
+                    const double res = rw[r] - a.theta[r] * rv[r];
+                    double denom = dg - a.theta[r];
+                    if (fabs(denom) < 1e-8) denom = copysign(1e-8, denom);
+                    const double cr = res / denom;
+                    a.out[r][base + i] = cr;
+                    s1[r] = fma(res, res, s1[r]);
+                    s2[r] = fma(cr, cr, s2[r]);
+                }
+        }
+        __syncthreads();   // stage consumed
+        if (warp == 0 && it + nst < my_tiles) {
+            fence_proxy_async_smem();
+            issue(it + nst);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < kBlkMaxRoots; ++r) {
+        double x = s1[r], y = s2[r];
+        for (int o = 16; o > 0; o >>= 1) {
+            x += __shfl_down_sync(0xffffffffu, x, o);
+            y += __shfl_down_sync(0xffffffffu, y, o);
+        }
+        if (lane == 0) {
+            s_red[warp][r] = x;
+            s_red[warp][kBlkMaxRoots + r] = y;
+        }
+    }
+    __syncthreads();
+    if (tid < 2 * static_cast<uint32_t>(m)) {
+        const int r = static_cast<int>(tid) % m, which = static_cast<int>(tid) / m;
+        double acc = 0.0;
+        for (int w = 0; w < kWarps; ++w) acc += s_red[w][which * kBlkMaxRoots + r];
+        a.partial[static_cast<size_t>(tid) * gridDim.x + blockIdx.x] = acc;
+    }
+}
+
 __global__ void k_scale_div(double* __restrict__ x, uint64_t n, double divisor) {
     TILE_LOOP(i0, n) {
         double v[kU];
@@ -667,6 +792,44 @@ __global__ void k_argmin(const double* __restrict__ d, uint64_t n, double* __res
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const double v = d[i];
         if (v < bv || (v == bv && i < bi)) {
+            bv = v;
+            bi = i;
+        }
+    }
+    sv[threadIdx.x] = bv;
+    si[threadIdx.x] = bi;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            const double ov = sv[threadIdx.x + s];
+            const uint64_t oi = si[threadIdx.x + s];
+            if (ov < sv[threadIdx.x] || (ov == sv[threadIdx.x] && oi < si[threadIdx.x])) {
+                sv[threadIdx.x] = ov;
+                si[threadIdx.x] = oi;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        pv[blockIdx.x] = sv[0];
+        pi[blockIdx.x] = si[0];
+    }
+}
+
+// Per-block smallest (value, index) pair lexicographically above (v0, i0):
+// round r of the block solver's guesses finds the r-th lowest diagonal entry
+// (lowest index on ties) without sorting the diagonal on the host.
+__global__ void k_argmin_after(const double* __restrict__ d, uint64_t n, double v0, uint64_t i0, int first,
+                               double* __restrict__ pv, uint64_t* __restrict__ pi) {
+    __shared__ double sv[kRedThreads];
+    __shared__ uint64_t si[kRedThreads];
+    double bv = INFINITY;
+    uint64_t bi = ~0ull;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const double v = d[i];
+        const bool above = first || v > v0 || (v == v0 && i > i0);
+        if (above && (v < bv || (v == bv && i < bi))) {
             bv = v;
             bi = i;
         }
@@ -917,6 +1080,16 @@ void stream_pass(Handle& h, StreamArgs& a, int nred, int slot) {
 
 // DETCI_DAVIDSON_FUSED=0: the previous per-operation kernels (k_dot_many,
 // k_ritz, two CGS passes), kept for comparison.
+// DETCI_DAVIDSON_BLOCK_RITZ=0: one k_ritz pass per root in the block solver.
+bool fused_block_ritz(int m, int k, uint64_t n) {
+    const char* e = std::getenv("DETCI_DAVIDSON_BLOCK_RITZ");   // read per call (tests switch it)
+    const bool off = e && std::string(e) == "0";
+    const size_t ns = 2 * static_cast<size_t>(k) + 1;
+    // the block solver's vectors sit n doubles apart: 16-byte bulk copies need n even
+    return !off && m <= kBlkMaxRoots && ns <= static_cast<size_t>(kStMaxS) && n > 0 && n % 2 == 0 &&
+           kStSmem / 8 / (2 * ns) >= 32;
+}
+
 bool fused_passes() {
     const char* e = std::getenv("DETCI_DAVIDSON_FUSED");
     return !(e && std::string(e) == "0");
@@ -1431,20 +1604,37 @@ void davidson_roots_device(Handle& h, const detci_dav_block_opts& opts, detci_da
     auto IM = [&](int r) { return store.p + static_cast<size_t>(2 * ms + m + r) * n; };
     auto CR = [&](int r) { return store.p + static_cast<size_t>(2 * ms + 2 * m + r) * n; };
 
-    // guesses: the m lowest diagonal entries (lowest index first on ties)
+    // guesses: the m lowest diagonal entries (lowest index first on ties),
+    // found on the device one rank-local pick per round
     {
-        std::vector<double> d(n);
-        copy_sync(d.data(), h.diag.p, n * sizeof(double), cudaMemcpyDeviceToHost, h.stream);
-        std::vector<uint64_t> idx(n);
-        for (uint64_t i = 0; i < n; ++i) idx[i] = i;
         const uint64_t keep = std::min<uint64_t>(n, static_cast<uint64_t>(m));
-        std::partial_sort(idx.begin(), idx.begin() + keep, idx.end(), [&](uint64_t x, uint64_t y) {
-            return d[x] < d[y] || (d[x] == d[y] && x < y);
-        });
         std::vector<double> cand(2 * m, INFINITY);  // (value, global index) of local best
+        DevBuf<double> pv;
+        DevBuf<uint64_t> pi;
+        pv.alloc(kRedBlocks);
+        pi.alloc(kRedBlocks);
+        std::vector<double> hv(kRedBlocks);
+        std::vector<uint64_t> hi(kRedBlocks);
+        double v0 = 0.0;
+        uint64_t i0 = 0;
         for (uint64_t r = 0; r < keep; ++r) {
-            cand[2 * r] = d[idx[r]];
-            cand[2 * r + 1] = static_cast<double>(idx[r] + h.a0 * h.nb());
+            k_argmin_after<<<kRedBlocks, kRedThreads, 0, h.stream>>>(h.diag.p, n, v0, i0, r == 0 ? 1 : 0, pv.p, pi.p);
+            CUDA_LAUNCH_CHECK();
+            CUDA_CHECK(cudaMemcpyAsync(hv.data(), pv.p, kRedBlocks * sizeof(double), cudaMemcpyDeviceToHost, h.stream));
+            CUDA_CHECK(cudaMemcpyAsync(hi.data(), pi.p, kRedBlocks * sizeof(uint64_t), cudaMemcpyDeviceToHost, h.stream));
+            CUDA_CHECK(cudaStreamSynchronize(h.stream));
+            double bv = INFINITY;
+            uint64_t bi = ~0ull;
+            for (int b = 0; b < kRedBlocks; ++b)
+                if (hv[b] < bv || (hv[b] == bv && hi[b] < bi)) {
+                    bv = hv[b];
+                    bi = hi[b];
+                }
+            if (bi == ~0ull) break;
+            cand[2 * r] = bv;
+            cand[2 * r + 1] = static_cast<double>(bi + h.a0 * h.nb());
+            v0 = bv;
+            i0 = bi;
         }
         std::vector<double> all(2 * static_cast<size_t>(m) * h.world, 0.0);
         std::copy(cand.begin(), cand.end(), all.begin() + 2 * static_cast<size_t>(m) * h.rank);
@@ -1483,6 +1673,22 @@ void davidson_roots_device(Handle& h, const detci_dav_block_opts& opts, detci_da
         }
     };
 
+    bool ritz_fresh = false;
+    int last_k = 0;
+    // Ritz vector, image and correction of root r from the current
+    // subspace (k vectors) and eigenpairs
+    auto ritz_root = [&](int r, int k) {
+        RitzArgs ra{};
+        for (int j = 0; j < k; ++j) {
+            ra.v[j] = V(j);
+            ra.w[j] = Wv(j);
+            ra.c[j] = evecs[static_cast<size_t>(r) * k + j];
+        }
+        ra.k = k;
+        ra.theta = evals[r];
+        k_ritz<<<kRedBlocks, kRedThreads, 0, h.stream>>>(ra, h.diag.p, n, RZ(r), IM(r), CR(r), h.red.p);
+        CUDA_LAUNCH_CHECK();
+    };
     for (int iter = 0; iter < opts.max_iter; ++iter) {
         detci_dav_iter st{};
         st.restarted = restart_pending ? 1 : 0;
@@ -1507,29 +1713,62 @@ void davidson_roots_device(Handle& h, const detci_dav_block_opts& opts, detci_da
         }
         const int k = k_sub;
         jacobi_eigen(proj, ms, k, evals, evecs);
+        last_k = k;
         st.subspace_solve_seconds = seconds_since(t0);
 
         t0 = std::chrono::steady_clock::now();
         double worst = 0.0;
         std::vector<double> cnorm(m, 0.0);
-        for (int r = 0; r < m; ++r) {
-            RitzArgs ra{};
+        if (fused_block_ritz(m, k, n)) {
+            // all m corrections in one pass; Ritz vectors / images later
+            BlockRitzArgs ba{};
             for (int j = 0; j < k; ++j) {
-                ra.v[j] = V(j);
-                ra.w[j] = Wv(j);
-                ra.c[j] = evecs[static_cast<size_t>(r) * k + j];
+                ba.s[j] = V(j);
+                ba.s[k + j] = Wv(j);
             }
-            ra.k = k;
-            ra.theta = evals[r];
-            k_ritz<<<kRedBlocks, kRedThreads, 0, h.stream>>>(ra, h.diag.p, n, RZ(r), IM(r), CR(r), h.red.p);
+            ba.s[2 * k] = h.diag.p;
+            for (int r = 0; r < m; ++r) {
+                for (int j = 0; j < k; ++j) ba.c[r][j] = evecs[static_cast<size_t>(r) * k + j];
+                ba.theta[r] = evals[r];
+                ba.out[r] = CR(r);
+            }
+            ba.k = k;
+            ba.m = m;
+            ba.ns = 2 * k + 1;
+            ba.nst = 2;
+            ba.n = n;
+            ba.T = static_cast<uint32_t>(std::min<size_t>(4096, kStSmem / 8 / (2 * static_cast<size_t>(ba.ns))) &
+                                         ~size_t{31});
+            ba.partial = h.red.p;
+            const size_t smem = 2 * static_cast<size_t>(ba.ns) * ba.T * sizeof(double);
+            const int grid = sm_count();
+            ensure_dynamic_smem(reinterpret_cast<const void*>(&k_ritz_block), smem);
+            k_ritz_block<<<grid, 512, smem, h.stream>>>(ba);
             CUDA_LAUNCH_CHECK();
-            finalize_to(h, 2, 0);
-            double nn2[2];
-            read_slots(h, 0, 2, nn2);
-            theta[r] = evals[r];
-            rnorm[r] = std::sqrt(nn2[0]);
-            cnorm[r] = std::sqrt(nn2[1]);
-            worst = std::max(worst, rnorm[r]);
+            k_finalize<<<2 * m, 32, 0, h.stream>>>(h.red.p, grid, 2 * m, scalar_slot(h, 0));
+            CUDA_LAUNCH_CHECK();
+            allreduce_device(h, scalar_slot(h, 0), 2 * m);
+            std::vector<double> nn(2 * m);
+            read_slots(h, 0, 2 * m, nn.data());
+            for (int r = 0; r < m; ++r) {
+                theta[r] = evals[r];
+                rnorm[r] = std::sqrt(nn[r]);
+                cnorm[r] = std::sqrt(nn[m + r]);
+                worst = std::max(worst, rnorm[r]);
+            }
+            ritz_fresh = false;
+        } else {
+            for (int r = 0; r < m; ++r) {
+                ritz_root(r, k);
+                finalize_to(h, 2, 0);
+                double nn2[2];
+                read_slots(h, 0, 2, nn2);
+                theta[r] = evals[r];
+                rnorm[r] = std::sqrt(nn2[0]);
+                cnorm[r] = std::sqrt(nn2[1]);
+                worst = std::max(worst, rnorm[r]);
+            }
+            ritz_fresh = true;
         }
         double gdev = 0.0;
         for (int i = 0; i < k; ++i)
@@ -1552,6 +1791,12 @@ void davidson_roots_device(Handle& h, const detci_dav_block_opts& opts, detci_da
         int unconverged = 0;
         for (int r = 0; r < m; ++r) unconverged += rnorm[r] > opts.tol && cnorm[r] > 0.0;
         if (k_sub + unconverged > ms) {  // collapse to the m Ritz pairs
+            if (!ritz_fresh) {
+                // Ritz vectors and images (and, again, the corrections) by
+                // the per-root pass before V[0..m) is overwritten
+                for (int r = 0; r < m; ++r) ritz_root(r, k);
+                ritz_fresh = true;
+            }
             for (int r = 0; r < m; ++r) {
                 CUDA_CHECK(cudaMemcpyAsync(V(r), RZ(r), n * 8, cudaMemcpyDeviceToDevice, h.stream));
                 CUDA_CHECK(cudaMemcpyAsync(Wv(r), IM(r), n * 8, cudaMemcpyDeviceToDevice, h.stream));
@@ -1602,6 +1847,8 @@ void davidson_roots_device(Handle& h, const detci_dav_block_opts& opts, detci_da
     res->status = status;
     res->converged = status == 0;
     res->iterations = iters;
+    if (res->eigenvectors && !ritz_fresh && last_k > 0)
+        for (int r = 0; r < m; ++r) ritz_root(r, last_k);
     for (int r = 0; r < m; ++r) {
         if (res->energies) res->energies[r] = theta[r];
         if (res->residuals) res->residuals[r] = rnorm[r];

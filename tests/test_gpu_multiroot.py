@@ -63,3 +63,25 @@ def test_multiroot_option_validation():
             detci.davidson_roots(b, 3, max_subspace=4)
         with pytest.raises(errors.InputError):
             detci.davidson_roots(b, 5, max_subspace=12)   # dim 4
+
+
+def test_fused_block_residual_pass_matches_per_root(monkeypatch):
+    """The one-pass multi-root residual (k_ritz_block, default for m <= 4 and
+    an even local dimension) against the per-root Ritz passes
+    (DETCI_DAVIDSON_BLOCK_RITZ=0) and dense eigh, through restarts."""
+    ints = synth.synthetic_integrals(12, 6)
+    s = synth.synthetic_strings(12, 3, 60)
+    assert (len(s) * len(s)) % 2 == 0
+    want = np.linalg.eigvalsh(dense_h(ints, s, s))[:4]
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("DETCI_DAVIDSON_BLOCK_RITZ", mode)
+        with gpu_basis(ints, s, s) as b:
+            res = detci.davidson_roots(b, 4, max_subspace=12)
+            assert res.converged
+            assert any(it.restarted for it in res.iterations)
+            for r in range(4):
+                assert np.linalg.norm(detci.matvec(b, res.eigenvectors[r]) - res.energies[r] * res.eigenvectors[r]) <= 1e-6
+        out[mode] = res
+    assert np.max(np.abs(out["1"].energies - want) / np.abs(want)) <= 1e-10
+    assert np.max(np.abs(out["1"].energies - out["0"].energies) / np.abs(want)) <= 1e-12
