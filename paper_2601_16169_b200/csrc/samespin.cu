@@ -172,11 +172,14 @@ constexpr int kSSMinBlocks = 32;
 // kV2 (M = 1, full chunks, 16-byte aligned rows): each lane owns two pairs
 // of adjacent columns and reads them with one 16-byte load each, halving
 // the load instructions per element.
-template <bool kTail, int M, int GW, bool kV2 = false>
+// RT > 0 (tail launches): RT column groups of 32 per lane instead of the
+// default R, so the partial last chunk (e.g. 40 of 128 columns at C3) does not
+// walk every entry for R x 32 clamped columns.
+template <bool kTail, int M, int GW, bool kV2 = false, int RT = 0>
 __global__ void __launch_bounds__(GW * kWarp, kSSMinBlocks / GW)
 k_samespin_g(const SameSpinArgs a, uint32_t chunk0, uint32_t ngroups) {
     constexpr int kGW = GW;
-    constexpr int R = SSR<M>::value;
+    constexpr int R = RT > 0 ? RT : SSR<M>::value;
     static_assert(!kV2 || (M == 1 && !kTail && R == 4), "kV2: one vector, full chunks");
     __shared__ uint32_t s_ja[kGW][kGStage];
     __shared__ double s_v[kGW][kGStage];
@@ -188,7 +191,7 @@ k_samespin_g(const SameSpinArgs a, uint32_t chunk0, uint32_t ngroups) {
     const uint32_t r = group * kGW + warp;
     if (r >= a.nrows) return;   // no CTA-wide barriers below
     const uint32_t row = a.row0 + r;
-    const uint32_t col0 = chunk * (kWarp * R) + lane;
+    const uint32_t col0 = chunk * (kWarp * SSR<M>::value) + lane;
 
     uint32_t col[R];
     double acc[R][M];
@@ -348,7 +351,16 @@ void launch_samespin_g(const SameSpinArgs& s, cudaStream_t st) {
         CUDA_LAUNCH_CHECK();
     }
     if (tail) {
-        k_samespin_g<true, M, GW><<<ngroups, GW * kWarp, 0, st>>>(s, static_cast<uint32_t>(full), ngroups);
+        const uint32_t tail_cols = s.ncols - static_cast<uint32_t>(full) * kChunk;
+        if (SSR<M>::value > 1 && tail_cols <= kWarp) {
+            ensure_carveout(reinterpret_cast<const void*>(k_samespin_g<true, M, GW, false, 1>), 10);
+            k_samespin_g<true, M, GW, false, 1><<<ngroups, GW * kWarp, 0, st>>>(s, static_cast<uint32_t>(full), ngroups);
+        } else if (SSR<M>::value > 2 && tail_cols <= 2 * kWarp) {
+            ensure_carveout(reinterpret_cast<const void*>(k_samespin_g<true, M, GW, false, 2>), 10);
+            k_samespin_g<true, M, GW, false, 2><<<ngroups, GW * kWarp, 0, st>>>(s, static_cast<uint32_t>(full), ngroups);
+        } else {
+            k_samespin_g<true, M, GW><<<ngroups, GW * kWarp, 0, st>>>(s, static_cast<uint32_t>(full), ngroups);
+        }
         CUDA_LAUNCH_CHECK();
     }
 }
