@@ -9,6 +9,7 @@ the all-CPU reference cannot finish (one reference sigma at C3 is ~5 h on
 16 cores).
 
     python scripts/mixed_oracle.py C2 260 [max_subspace] > profiles/mixed_oracle_C2.json
+    python scripts/mixed_oracle.py C2:7000 300   # C2 integrals, 7000 strings per channel
 
 Prints one JSON object: per-iteration Ritz values / residuals of both
 solvers, the largest per-iteration differences, and both final energies.
@@ -31,7 +32,14 @@ if not REF_SO.exists():
     sys.exit("reference library not built (oracle/_ref)")
 
 t0 = time.time()
-ints, a, b = synth.synthetic_system(cfg)
+if ":" in cfg:   # "C2:7000": the config's integrals, its first 7000 strings per channel
+    name, count = cfg.split(":")
+    norbs, nelec, _ = synth.CONFIGS[name]
+    ints = synth.synthetic_integrals(norbs, nelec)
+    a = synth.synthetic_strings(norbs, nelec // 2, int(count))
+    b = a.copy()
+else:
+    ints, a, b = synth.synthetic_system(cfg)
 basis = detci.GpuBasis(ints.norbs, a, b, ints.core, ints.h1, ints.eri)
 diag = basis.diag()
 print(f"{cfg}: dim {len(diag)}, setup {time.time() - t0:.1f} s", file=sys.stderr, flush=True)
